@@ -1,0 +1,201 @@
+"""Oracle multigrid: Alg. `gmg`, MG as stand-alone solver
+and MG-preconditioned GMRES.  TEST INFRASTRUCTURE ONLY.
+
+Written step by step in the paper's order and notation; every heavy operation
+is one of the plain per-op C definitions in oracle/__init__.py.
+Readings: Z3 coarse solve exact (LU) by default, "several steps of
+the smoothing iteration" as option; Z5 right preconditioning, MGS,
+restart m, stop at |g_{j+1}| <= rtol * beta_0; Z6 Euclidean norm over all
+DOFs; Z21 the coarse solve ignores the incoming x; iteration count = number of
+preconditioner applications.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import (block_diag_inverse, bsr_to_dense, csr_transpose, dot, jacobi_sweep, lu_factor,
+               lu_solve, nrm2, residual, spmv, transfer)
+
+
+@dataclass
+class MgLevel:
+    n: int
+    bs: int
+    rp: np.ndarray
+    col: np.ndarray
+    val: np.ndarray
+    P: tuple | None = None        # (rp, col, w) n x n_{l-1}: prolongation from level l-1
+    wpe: int = 1
+    dinv: np.ndarray | None = None
+    R: tuple | None = None        # R_{l-1} = P_{l-1}^T (built here)
+
+
+@dataclass
+class MgHierarchy:
+    levels: list                  # coarse -> fine
+    omega: float = 0.8
+    nu_pre: int = 2
+    nu_post: int = 2
+    coarse: str = "direct"        # "direct" | "smooth"
+    coarse_sweeps: int = 20
+    H: tuple | None = None        # fine-level hanging matrix
+    lu: tuple | None = field(default=None, repr=False)
+
+    @classmethod
+    def from_arrays(cls, levels, omega=0.8, nu_pre=2, nu_post=2, coarse="direct", coarse_sweeps=20, H=None):
+        """levels: list (coarse -> fine) of objects with n, bs, row_ptr, col, val,
+        P (or None), wpe."""
+        out = []
+        for l, L in enumerate(levels):
+            lv = MgLevel(L.n, L.bs, np.asarray(L.row_ptr, np.int64), np.asarray(L.col, np.int64),
+                         np.asarray(L.val, np.float64), L.P if l > 0 else None, getattr(L, "wpe", 1))
+            lv.dinv = block_diag_inverse(lv.n, lv.bs, lv.rp, lv.col, lv.val)
+            if l > 0:
+                prp, pcol, pw = lv.P
+                lv.R = csr_transpose(lv.n, out[-1].n, prp, pcol, pw, lv.wpe)
+            out.append(lv)
+        h = cls(out, omega, nu_pre, nu_post, coarse, coarse_sweeps, H)
+        if coarse == "direct":
+            c = out[0]
+            h.lu = lu_factor(bsr_to_dense(c.n, c.bs, c.rp, c.col, c.val))
+        return h
+
+    # --- the operations of Alg. gmg on level l -------------------------------
+    def A(self, l, x):
+        L = self.levels[l]
+        return spmv(L.n, L.bs, L.rp, L.col, L.val, x)
+
+    def smooth(self, l, x, b):
+        """S_l(x, b): one damped block-Jacobi step x + omega D^{-1}(b - A x)."""
+        L = self.levels[l]
+        return jacobi_sweep(L.n, L.bs, L.rp, L.col, L.val, L.dinv, self.omega, x, b)
+
+    def restrict(self, l, r):
+        """R_{l-1} r with R = P^T."""
+        L = self.levels[l]
+        rrp, rcol, rw = L.R
+        return transfer(self.levels[l - 1].n, L.bs, rrp, rcol, rw, L.wpe, r)
+
+    def prolongate_add(self, l, x, y):
+        """x + P_{l-1} y."""
+        L = self.levels[l]
+        prp, pcol, pw = L.P
+        return transfer(L.n, L.bs, prp, pcol, pw, L.wpe, y, x)
+
+    def coarse_solve(self, b):
+        """Step 0: A_0^{-1} b_0, or coarse_sweeps smoothing steps from 0."""
+        if self.coarse == "direct":
+            return lu_solve(self.lu[0], self.lu[1], b)
+        x = np.zeros_like(b)
+        for _ in range(self.coarse_sweeps):
+            x = self.smooth(0, x, b)
+        return x
+
+
+def vcycle(h: MgHierarchy, l: int, x: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """GMG(l, x_l, b_l) of Alg. `gmg`."""
+    if l == 0:                                           # Step 0
+        return h.coarse_solve(b)
+    for _ in range(h.nu_pre):                            # Step 1: pre-smooth
+        x = h.smooth(l, x, b)
+    L = h.levels[l]
+    d = h.restrict(l, residual(L.n, L.bs, L.rp, L.col, L.val, x, b))   # Step 2
+    y = vcycle(h, l - 1, np.zeros(h.levels[l - 1].n * L.bs), d)         # Step 3
+    x = h.prolongate_add(l, x, y)                        # Step 4
+    for _ in range(h.nu_post):                           # Step 5: post-smooth
+        x = h.smooth(l, x, b)
+    return x
+
+
+def richardson(h: MgHierarchy, b, x0=None, rtol=1e-10, max_iter=100):
+    """x^{(n)} = GMG(L, x^{(n-1)}, b) until ||b - A x|| <= rtol ||b - A x0||.
+    Returns x, iterations, residual history."""
+    Lf = len(h.levels) - 1
+    F = h.levels[-1]
+    x = np.zeros(F.n * F.bs) if x0 is None else np.array(x0, np.float64)
+    r0 = nrm2(residual(F.n, F.bs, F.rp, F.col, F.val, x, b))
+    hist = [r0]
+    if r0 == 0.0:
+        return x, 0, hist
+    for it in range(1, max_iter + 1):
+        x = vcycle(h, Lf, x, b)
+        hist.append(nrm2(residual(F.n, F.bs, F.rp, F.col, F.val, x, b)))
+        if hist[-1] <= rtol * r0:
+            return x, it, hist
+    return x, max_iter, hist
+
+
+def gmres(h: MgHierarchy, b, x0=None, rtol=1e-10, restart=30, max_iter=200, precondition=True):
+    """Right-preconditioned GMRES(m) with modified Gram-Schmidt and Givens
+    rotations (Saad §6.5.3 as cited at P:346; stored-Z form, reading O8/Z5).
+    The iteration count is the number of preconditioner applications.
+    Returns x, iterations, history of |g_{j+1}| / beta_0 estimates, true rel. residual."""
+    Lf = len(h.levels) - 1
+    F = h.levels[-1]
+    N = F.n * F.bs
+    x = np.zeros(N) if x0 is None else np.array(x0, np.float64)
+    r = residual(F.n, F.bs, F.rp, F.col, F.val, x, b)
+    beta0 = nrm2(r)
+    hist = [1.0]
+    if beta0 == 0.0:
+        return x, 0, hist, 0.0
+    its = 0
+    beta = beta0
+    while its < max_iter:
+        m = min(restart, max_iter - its)
+        V = np.zeros((m + 1, N))
+        Z = np.zeros((m, N))
+        Hh = np.zeros((m + 1, m))
+        cs = np.zeros(m)
+        sn = np.zeros(m)
+        g = np.zeros(m + 1)
+        V[0] = r / beta
+        g[0] = beta
+        k = 0
+        done = False
+        for j in range(m):
+            Z[j] = vcycle(h, Lf, np.zeros(N), V[j]) if precondition else V[j]
+            its += 1
+            w = h.A(Lf, Z[j])
+            for i in range(j + 1):                       # modified Gram-Schmidt
+                Hh[i, j] = dot(w, V[i])
+                w = w - Hh[i, j] * V[i]
+            hn = nrm2(w)
+            Hh[j + 1, j] = hn
+            for i in range(j):                           # previous rotations
+                t = cs[i] * Hh[i, j] + sn[i] * Hh[i + 1, j]
+                Hh[i + 1, j] = -sn[i] * Hh[i, j] + cs[i] * Hh[i + 1, j]
+                Hh[i, j] = t
+            rho = np.hypot(Hh[j, j], Hh[j + 1, j])
+            cs[j] = Hh[j, j] / rho
+            sn[j] = Hh[j + 1, j] / rho
+            breakdown = hn == 0.0
+            Hh[j, j] = rho
+            Hh[j + 1, j] = 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            hist.append(abs(g[j + 1]) / beta0)
+            k = j + 1
+            if abs(g[j + 1]) <= rtol * beta0 or breakdown:
+                done = True
+                break
+            V[j + 1] = w / hn
+        y = np.zeros(k)                                  # back substitution H y = g
+        for i in range(k - 1, -1, -1):
+            y[i] = (g[i] - Hh[i, i + 1:k] @ y[i + 1:k]) / Hh[i, i]
+        for i in range(k):
+            x = x + y[i] * Z[i]
+        r = residual(F.n, F.bs, F.rp, F.col, F.val, x, b)
+        beta = nrm2(r)
+        if done or beta <= rtol * beta0:
+            break
+    return x, its, hist, beta / beta0
+
+
+def apply_H(H, x, bs):
+    """x <- H x after the solve (reading Z7)."""
+    rp, col, w = H
+    n = len(rp) - 1
+    return transfer(n, bs, rp, col, w, 1, x)
