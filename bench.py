@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the fp64 GMG hot path of arXiv 2405.05047 on B200.
+
+A step = one pass of the whole hot path over the
+synthetic workload: GMRES(30) preconditioned by one V(2,2)-cycle per
+iteration (Alg. gmg; GMRES P:343-347), from x0 = 0 to a 1e-10
+relative residual, followed by the hanging-node interpolation x <- H x
+(P:144).  Metric (BASELINE.json): V-cycles/s (= preconditioner applications
+per second inside the solve), with DOF-cycles/s and the fine-level fused
+smoother's HBM roofline fraction alongside.
+
+Default workload: C3 -- 3D Q1 linear elasticity, 3x3 blocks,
+face-refined octree with hanging nodes, 10,329,843 DOFs, 7 levels: the
+north-star ">=10M-DOF adaptive 3D mesh" configuration.  Inputs (7 GB of
+operators) are far larger than L2 (126 MB), so no explicit flush is needed.
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
+        N > 1: torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c3": "C3: 3D Q1 elasticity (M + dt^2 K_e), 3x3 blocks, face-refined octree (9^3 root, 6 band steps), "
+          "hanging nodes, 7 levels, GMRES(30)+V(2,2) block-Jacobi omega=0.5, direct coarse solve",
+    "c2": "C2: 2D transport-diffusion Q1, quadtree band-refined toward y=0 (32^2 root, 7 steps), 8 levels, "
+          "GMRES(30)+V(2,2) Jacobi omega=0.8, direct coarse solve",
+    "c1": "C1: 2D transport-diffusion Q1, uniform 32x32 (1089 DOFs), 4 levels",
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def level_bytes(info, bs, zero):
+    """Algorithmic bytes of one V(2,2) on one level; info from mgi_level_info."""
+    n, z = info["n"], info["nnzb"]
+    a_stream = z * (8 * bs * bs + 4) + 8 * (n + 1)
+    sweep = a_stream + 8 * bs * n * 3 + 8 * bs * bs * n
+    sweep0 = 16 * bs * n + 8 * bs * bs * n
+    resid = a_stream + 24 * bs * n
+    return sweep, sweep0, resid
+
+
+def vcycle_bytes(infos, bs, nu=(2, 2), zero=True, coarse_direct=True):
+    """Algorithmic bytes of one V-cycle (fine level from zero guess if zero)."""
+    total = 0
+    L = len(infos) - 1
+    for l in range(L, 0, -1):
+        sweep, sweep0, resid = level_bytes(infos[l], bs, zero)
+        first_zero = zero or l < L
+        total += (sweep0 + (nu[0] - 1) * sweep) if first_zero else nu[0] * sweep
+        total += resid + nu[1] * sweep
+        nf, nc = infos[l]["n"], infos[l - 1]["n"]
+        zp = infos[l]["nnz_p"]
+        total += 12 * zp + 8 * (nc + 1) + 8 * bs * (nf + nc)         # restrict
+        total += 12 * zp + 8 * (nf + 1) + 8 * bs * (nc + 2 * nf)     # prolong-add
+    n0 = infos[0]["n"] * bs
+    total += 8 * n0 * n0 if coarse_direct else 0
+    return total
+
+
+def build_problem(name):
+    from problems import configs
+    t = time.time()
+    P = configs.build(name, keep_geometry=False)
+    log(f"[bench] generated {name}: {P.n_dof} DOFs, levels {[l.n for l in P.levels]} in {time.time() - t:.1f}s")
+    return P
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def oracle_vcycle_rate(P, n_cycles=1, warmup=0):
+    """The oracle (as it stands) timed on the host cores: V-cycles/s of
+    GMG(L, 0, b) -- the preconditioner application of one GMRES step."""
+    import oracle
+    cores = cpu_cores()
+    oracle.set_threads(cores)
+    t = time.time()
+    h = oracle.MgHierarchy.from_arrays(P.levels, omega=P.omega, nu_pre=P.nu_pre, nu_post=P.nu_post)
+    log(f"[bench] oracle setup {time.time() - t:.1f}s on {cores} cores")
+    L = len(P.levels) - 1
+    for _ in range(warmup):
+        oracle.vcycle(h, L, np.zeros_like(P.b), P.b)
+    times = []
+    for _ in range(n_cycles):
+        t = time.perf_counter()
+        oracle.vcycle(h, L, np.zeros_like(P.b), P.b)
+        times.append(time.perf_counter() - t)
+    return times, cores
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    P = build_problem(args.config)
+    times, cores = oracle_vcycle_rate(P, n_cycles=args.steps, warmup=args.warmup)
+    tot = sum(times)
+    val = args.steps / tot
+    line = {
+        "impl": "reference", "metric": "V-cycles/s", "value": val, "unit": "V-cycles/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "n_dof": P.n_dof, "levels": len(P.levels)},
+        "cpu_baseline": {"value": val, "unit": "V-cycles/s", "cores": cores, "kind": "oracle",
+                         "sample": f"each step = one oracle V(2,2) GMG(L,0,b) on the full {args.config} "
+                                   f"({P.n_dof} DOFs): one preconditioner application of the GMRES step"},
+        "e2e": {"value": val, "unit": "V-cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "dof_cycles_per_s": val * P.n_dof,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+    torch.cuda.set_device(dev)
+    import paper_2405_05047_b200 as mg
+
+    P = build_problem(args.config)
+    bs = P.bs
+    stream = torch.cuda.current_stream()
+    t = time.time()
+    solver = mg.Multigrid(P.levels, bs, omega=P.omega, nu_pre=P.nu_pre, nu_post=P.nu_post, H=P.fine.H,
+                          device=dev, stream=stream)
+    torch.cuda.synchronize()
+    log(f"[bench] rank {rank}: library setup {time.time() - t:.1f}s")
+    ctx = solver.ctx
+    L = len(P.levels) - 1
+    infos = [mg.level_info(ctx, l) for l in range(L + 1)]
+    N = P.n_dof
+    b_host = torch.from_numpy(P.b).pin_memory()
+    b = b_host.cuda()
+    x = torch.zeros(N, dtype=torch.float64, device="cuda")
+    opts = dict(restart=30, max_iter=200, rtol=args.rtol)
+
+    def step(xv, bv):
+        xv.zero_()
+        st, its, rel, conv = solver.solve(xv, bv, **opts)
+        if not conv:
+            raise RuntimeError(f"solve did not converge: {its} its, rel {rel:.3e}")
+        solver.apply_constraints(xv)
+        return its, rel
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        its0, rel0 = step(x, b)
+    # ---------------- timed region (device events, max over ranks) ------------
+    sampler = ClockSampler(dev)
+    sampler.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    l0 = mg.launch_count(ctx)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    total_its = 0
+    for _ in range(args.steps):
+        its, rel = step(x, b)
+        total_its += its
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    t_ms = e0.elapsed_time(e1)
+    launches = mg.launch_count(ctx) - l0
+    clocks = sampler.stop()
+    if ws > 1:
+        tt = torch.tensor([t_ms, float(total_its)], dtype=torch.float64, device="cuda")
+        tmax = tt.clone()
+        torch.distributed.all_reduce(tmax[:1], op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(tt[1:], op=torch.distributed.ReduceOp.SUM)
+        t_ms, total_its_all = float(tmax[0]), int(tt[1])
+    else:
+        total_its_all = total_its
+    value = total_its_all / (t_ms / 1e3)
+
+    # ---------------- e2e: host buffers through the public API -----------------
+    x_host = torch.empty(N, dtype=torch.float64).pin_memory()
+    barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    e2e_its = 0
+    for _ in range(args.steps):
+        b.copy_(b_host, non_blocking=True)
+        its, _ = step(x, b)
+        x_host.copy_(x, non_blocking=True)
+        e2e_its += its
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    if ws > 1:
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(tt[0])
+    e2e_val = e2e_its * ws / (e2e_ms / 1e3)
+
+    # ---------------- pure V-cycle rate (graph replay of mg_vcycle_zero) -------
+    z = torch.zeros_like(x)
+    for _ in range(3):
+        solver.precondition(z, b)
+    nv = 20
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(nv):
+        solver.precondition(z, b)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    vc_ms = e0.elapsed_time(e1) / nv
+    vc_bytes = vcycle_bytes(infos, bs, (P.nu_pre, P.nu_post), zero=True)
+
+    # ---------------- dominant kernel: fine-level fused block-Jacobi sweep -----
+    peak, peak_src = measured_peaks()
+    xin = torch.randn(N, dtype=torch.float64, device="cuda")
+    xout = torch.empty_like(xin)
+    for _ in range(3):
+        mg.mg_sweep(ctx, L, xin, b, xout)
+    ns = 20
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ns)]
+    torch.cuda.synchronize()
+    for a, c in evs:
+        a.record(stream)
+        mg.mg_sweep(ctx, L, xin, b, xout)
+        c.record(stream)
+    torch.cuda.synchronize()
+    sw_ms = sum(a.elapsed_time(c) for a, c in evs) / ns
+    sweep_b, _, _ = level_bytes(infos[L], bs, False)
+    achieved = sweep_b / (sw_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(args.config, {}).get("sweep_fine_dram_bytes")
+
+    # ---------------- CPU baseline: the oracle on the host cores ----------------
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        times, cores = oracle_vcycle_rate(P, n_cycles=1)
+        cpu = {"value": 1.0 / times[0], "unit": "V-cycles/s", "cores": cores, "kind": "oracle",
+               "sample": f"one oracle V(2,2) GMG(L,0,b) on the full {args.config} ({N} DOFs), "
+                         f"{times[0]:.2f} s, OpenMP over rows"}
+
+    if rank == 0:
+        line = {
+            "metric": "V-cycles/s", "value": value, "unit": "V-cycles/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config], "n_dof": N, "n_dof_per_gpu": N,
+                       "levels": len(P.levels), "level_rows": [i["n"] for i in infos],
+                       "nnzb_fine": infos[L]["nnzb"], "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                       "solver": "GMRES(30) + V(2,2) block-Jacobi, rtol 1e-10, x0 = 0, then x <- Hx",
+                       "l2": "operator 7 GB >> L2 126 MB (no flush needed)",
+                       "iterations_per_solve": total_its // args.steps},
+            "dof_cycles_per_s": value * N,
+            "solve_ms": t_ms / args.steps,
+            "vcycle_only": {"ms": vc_ms, "per_s": 1e3 / vc_ms, "alg_bytes": vc_bytes,
+                            "alg_gbs": vc_bytes / (vc_ms / 1e3) / 1e9,
+                            "frac": vc_bytes / (vc_ms / 1e3) / 1e9 / peak},
+            "roofline": {"bound": "hbm", "kernel": "k_sell_apply<3,SWEEP> fine level", "achieved": achieved,
+                         "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "alg_bytes_per_launch": sweep_b, "avg_launch_ms": sw_ms},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": "V-cycles/s", "h2d_bytes_per_step": 8 * N,
+                    "d2h_bytes_per_step": 8 * N},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(WORKLOADS), default="c3")
+    ap.add_argument("--rtol", type=float, default=1e-10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("[bench] warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,291 @@
+"""paper_2405_05047_b200 -- B200-native fp64 geometric multigrid (arXiv 2405.05047).
+
+Thin ctypes binding over libmgb200.so (include/mg.h): the same names as the C
+ABI, argument marshalling only.  Every step of the solve runs in the CUDA
+library; there is no CPU fallback -- importing this package fails loudly if
+the extension has not been built (``python -m paper_2405_05047_b200.build``).
+
+Vectors and arrays may be torch tensors (CUDA -> device pointer, CPU -> host
+pointer) or numpy arrays (host pointer).  Compute calls take CUDA tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmgb200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2405_05047_b200.build` "
+                      "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+MG_OK, MG_NOT_CONVERGED = 0, 1
+MG_ERR_INVALID_ARG, MG_ERR_DIMENSION, MG_ERR_STRUCTURE, MG_ERR_NONFINITE = -1, -2, -3, -4
+MG_ERR_SINGULAR, MG_ERR_STATE, MG_ERR_CUDA, MG_ERR_NCCL, MG_ERR_OOM = -5, -6, -7, -8, -9
+MG_MEM_HOST, MG_MEM_DEVICE = 0, 1
+MG_COARSE_DIRECT, MG_COARSE_SMOOTH = 0, 1
+MG_GMRES, MG_RICHARDSON = 0, 1
+
+STATUS_NAMES = {0: "MG_OK", 1: "MG_NOT_CONVERGED", -1: "MG_ERR_INVALID_ARG", -2: "MG_ERR_DIMENSION",
+                -3: "MG_ERR_STRUCTURE", -4: "MG_ERR_NONFINITE", -5: "MG_ERR_SINGULAR", -6: "MG_ERR_STATE",
+                -7: "MG_ERR_CUDA", -8: "MG_ERR_NCCL", -9: "MG_ERR_OOM"}
+
+
+class mg_config(ctypes.Structure):
+    _fields_ = [("n_levels", ctypes.c_int), ("block_size", ctypes.c_int), ("nu_pre", ctypes.c_int),
+                ("nu_post", ctypes.c_int), ("omega", ctypes.c_double), ("coarse_mode", ctypes.c_int),
+                ("coarse_sweeps", ctypes.c_int), ("use_graphs", ctypes.c_int)]
+
+
+class mg_comm(ctypes.Structure):
+    _fields_ = [("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_id", ctypes.c_ubyte * 128)]
+
+
+class mg_solve_opts(ctypes.Structure):
+    _fields_ = [("method", ctypes.c_int), ("restart", ctypes.c_int), ("max_iter", ctypes.c_int),
+                ("rtol", ctypes.c_double)]
+
+
+class mg_solve_info(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int), ("rel_residual", ctypes.c_double), ("converged", ctypes.c_int)]
+
+
+class MgError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = _lib.mg_last_error().decode()
+        super().__init__(f"{where}: {STATUS_NAMES.get(status, status)}: {msg}")
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_I64 = ctypes.c_int64
+_D = ctypes.c_double
+
+_SIGS = {
+    "mg_get_unique_id": [_P],
+    "mg_create": [ctypes.POINTER(_P), ctypes.POINTER(mg_config), _I, _P, ctypes.POINTER(mg_comm)],
+    "mg_create_level": [_P, _I, _I64, _I64, _I64],
+    "mg_set_matrix": [_P, _I, _P, _P, _P, _I64, _I],
+    "mg_set_transfer": [_P, _I, _P, _P, _P, _I64, _I, _I],
+    "mg_set_smoother": [_P, _I, _D, _I, _I, _P, _I],
+    "mg_set_constraints": [_P, _P, _P, _P, _I64, _I],
+    "mg_setup": [_P],
+    "mg_destroy": [_P],
+    "mg_vcycle": [_P, _P, _P],
+    "mg_vcycle_zero": [_P, _P, _P],
+    "mg_solve": [_P, _P, _P, ctypes.POINTER(mg_solve_opts), ctypes.POINTER(mg_solve_info)],
+    "mg_spmv": [_P, _I, _D, _P, _D, _P],
+    "mg_sweep": [_P, _I, _P, _P, _P],
+    "mg_residual": [_P, _I, _P, _P, _P],
+    "mg_smooth": [_P, _I, _P, _P, _I],
+    "mg_restrict": [_P, _I, _P, _P],
+    "mg_prolong_add": [_P, _I, _P, _P],
+    "mg_coarse_solve": [_P, _P, _P],
+    "mg_apply_constraints": [_P, _P],
+    "mg_dot": [_P, _I, _P, _P, ctypes.POINTER(_D)],
+}
+for _name, _args in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = ctypes.c_int
+_lib.mg_last_error.restype = ctypes.c_char_p
+_lib.mg_last_error.argtypes = []
+_lib.mg_version.restype = ctypes.c_char_p
+_lib.mg_version.argtypes = []
+_lib.mgi_launch_count.restype = ctypes.c_int64
+_lib.mgi_launch_count.argtypes = [_P]
+_lib.mgi_level_info.restype = ctypes.c_int
+_lib.mgi_level_info.argtypes = [_P, _I] + [ctypes.POINTER(ctypes.c_int64)] * 6
+
+EXPORTED = sorted(list(_SIGS) + ["mg_last_error", "mg_version"])
+
+
+def lib():
+    return _lib
+
+
+def _check(st: int, where: str, ok=(MG_OK,)) -> int:
+    if st not in ok:
+        raise MgError(st, where)
+    return st
+
+
+def _ptr(a, dtype=None):
+    """(pointer, mem) of a torch tensor or numpy array (contiguity and dtype checked)."""
+    if a is None:
+        return None, MG_MEM_HOST
+    if isinstance(a, np.ndarray):
+        if dtype is not None and a.dtype != dtype:
+            raise TypeError(f"expected {dtype}, got {a.dtype}")
+        if not a.flags.c_contiguous:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data, MG_MEM_HOST
+    # torch tensor
+    if not a.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    if dtype is not None and str(a.dtype).replace("torch.", "") != np.dtype(dtype).name:
+        raise TypeError(f"expected {dtype}, got {a.dtype}")
+    return a.data_ptr(), (MG_MEM_DEVICE if a.is_cuda else MG_MEM_HOST)
+
+
+def _dptr(a) -> int:
+    """device pointer of a CUDA fp64 tensor (compute calls)."""
+    if not getattr(a, "is_cuda", False):
+        raise TypeError("compute calls take CUDA tensors")
+    p, _ = _ptr(a, np.float64)
+    return p
+
+
+def _same_mem(*arrs):
+    mems = {_ptr(a)[1] for a in arrs if a is not None}
+    if len(mems) > 1:
+        raise ValueError("all arrays of one call must live in the same memory (host or device)")
+    return mems.pop() if mems else MG_MEM_HOST
+
+
+# ----------------------------------------------------------------------------
+# the C ABI, same names
+# ----------------------------------------------------------------------------
+
+def mg_version() -> str:
+    return _lib.mg_version().decode()
+
+
+def mg_last_error() -> str:
+    return _lib.mg_last_error().decode()
+
+
+def mg_get_unique_id() -> bytes:
+    buf = (ctypes.c_ubyte * 128)()
+    _check(_lib.mg_get_unique_id(buf), "mg_get_unique_id")
+    return bytes(buf)
+
+
+def mg_create(n_levels, block_size, *, nu_pre=2, nu_post=2, omega=0.8, coarse_mode=MG_COARSE_DIRECT,
+              coarse_sweeps=20, use_graphs=True, device=0, stream=None, comm=None):
+    """Returns an opaque context handle (int).  stream: a torch.cuda.Stream, a
+    raw cudaStream_t int, or None (internal blocking stream)."""
+    cfg = mg_config(n_levels, block_size, nu_pre, nu_post, omega, coarse_mode, coarse_sweeps, int(bool(use_graphs)))
+    h = _P()
+    s = getattr(stream, "cuda_stream", stream)
+    cm = None
+    if comm is not None:
+        nranks, rank, uid = comm
+        cm = mg_comm(nranks, rank, (ctypes.c_ubyte * 128)(*uid))
+    _check(_lib.mg_create(ctypes.byref(h), ctypes.byref(cfg), device, s, ctypes.byref(cm) if cm else None),
+           "mg_create")
+    return h.value
+
+
+def mg_create_level(ctx, level, n_rows_global, row_begin=0, row_end=None):
+    _check(_lib.mg_create_level(ctx, level, n_rows_global, row_begin,
+                                n_rows_global if row_end is None else row_end), "mg_create_level")
+
+
+def mg_set_matrix(ctx, level, row_ptr, col, vals):
+    mem = _same_mem(row_ptr, col, vals)
+    nnzb = int(col.shape[0])
+    _check(_lib.mg_set_matrix(ctx, level, _ptr(row_ptr, np.int64)[0], _ptr(col, np.int64)[0],
+                              _ptr(vals, np.float64)[0], nnzb, mem), "mg_set_matrix")
+
+
+def mg_set_transfer(ctx, fine_level, row_ptr, col, w, weights_per_entry=1):
+    mem = _same_mem(row_ptr, col, w)
+    _check(_lib.mg_set_transfer(ctx, fine_level, _ptr(row_ptr, np.int64)[0], _ptr(col, np.int64)[0],
+                                _ptr(w, np.float64)[0], int(col.shape[0]), weights_per_entry, mem),
+           "mg_set_transfer")
+
+
+def mg_set_smoother(ctx, level, omega=0.0, nu_pre=-1, nu_post=-1, dinv=None):
+    p, mem = _ptr(dinv, np.float64)
+    _check(_lib.mg_set_smoother(ctx, level, omega, nu_pre, nu_post, p, mem), "mg_set_smoother")
+
+
+def mg_set_constraints(ctx, row_ptr, col, w):
+    mem = _same_mem(row_ptr, col, w)
+    _check(_lib.mg_set_constraints(ctx, _ptr(row_ptr, np.int64)[0], _ptr(col, np.int64)[0],
+                                   _ptr(w, np.float64)[0], int(col.shape[0]), mem), "mg_set_constraints")
+
+
+def mg_setup(ctx):
+    _check(_lib.mg_setup(ctx), "mg_setup")
+
+
+def mg_destroy(ctx):
+    _check(_lib.mg_destroy(ctx), "mg_destroy")
+
+
+def mg_vcycle(ctx, x, b):
+    _check(_lib.mg_vcycle(ctx, _dptr(x), _dptr(b)), "mg_vcycle")
+
+
+def mg_vcycle_zero(ctx, z, v):
+    _check(_lib.mg_vcycle_zero(ctx, _dptr(z), _dptr(v)), "mg_vcycle_zero")
+
+
+def mg_solve(ctx, x, b, method=MG_GMRES, restart=30, max_iter=200, rtol=1e-10, raise_on_nonconv=False):
+    """Returns (status, iterations, rel_residual, converged)."""
+    o = mg_solve_opts(method, restart, max_iter, rtol)
+    info = mg_solve_info()
+    st = _lib.mg_solve(ctx, _dptr(x), _dptr(b), ctypes.byref(o), ctypes.byref(info))
+    _check(st, "mg_solve", ok=(MG_OK,) if raise_on_nonconv else (MG_OK, MG_NOT_CONVERGED))
+    return st, info.iterations, info.rel_residual, bool(info.converged)
+
+
+def mg_spmv(ctx, level, alpha, x, beta, y):
+    _check(_lib.mg_spmv(ctx, level, alpha, _dptr(x), beta, _dptr(y)), "mg_spmv")
+
+
+def mg_sweep(ctx, level, x, b, x_out):
+    _check(_lib.mg_sweep(ctx, level, _dptr(x), _dptr(b), _dptr(x_out)), "mg_sweep")
+
+
+def mg_residual(ctx, level, x, b, r):
+    _check(_lib.mg_residual(ctx, level, _dptr(x), _dptr(b), _dptr(r)), "mg_residual")
+
+
+def mg_smooth(ctx, level, x, b, sweeps=1):
+    _check(_lib.mg_smooth(ctx, level, _dptr(x), _dptr(b), sweeps), "mg_smooth")
+
+
+def mg_restrict(ctx, fine_level, r_fine, d_coarse):
+    _check(_lib.mg_restrict(ctx, fine_level, _dptr(r_fine), _dptr(d_coarse)), "mg_restrict")
+
+
+def mg_prolong_add(ctx, fine_level, y_coarse, x_fine):
+    _check(_lib.mg_prolong_add(ctx, fine_level, _dptr(y_coarse), _dptr(x_fine)), "mg_prolong_add")
+
+
+def mg_coarse_solve(ctx, d, y):
+    _check(_lib.mg_coarse_solve(ctx, _dptr(d), _dptr(y)), "mg_coarse_solve")
+
+
+def mg_apply_constraints(ctx, x):
+    _check(_lib.mg_apply_constraints(ctx, _dptr(x)), "mg_apply_constraints")
+
+
+def mg_dot(ctx, level, a, b) -> float:
+    out = _D()
+    _check(_lib.mg_dot(ctx, level, _dptr(a), _dptr(b), ctypes.byref(out)), "mg_dot")
+    return out.value
+
+
+def launch_count(ctx) -> int:
+    """Kernels launched by the context so far (eager + CUDA-graph kernel nodes)."""
+    return int(_lib.mgi_launch_count(ctx))
+
+
+def level_info(ctx, level) -> dict:
+    v = [ctypes.c_int64() for _ in range(6)]
+    _check(_lib.mgi_level_info(ctx, level, *[ctypes.byref(x) for x in v]), "mgi_level_info")
+    keys = ("n", "nnzb", "sell_entries", "nnz_p", "sell_entries_p", "sell_entries_r")
+    return {k: x.value for k, x in zip(keys, v)}
+
+
+from .solver import Multigrid  # noqa: E402,F401

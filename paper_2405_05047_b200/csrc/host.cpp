@@ -1,0 +1,268 @@
+// Host-side setup of libmgb200.so: validation, the SELL-32-sigma device
+// layout, R = P^T, inverse diagonal blocks, coarse dense inverse, and the
+// multi-GPU column localisation.  No CUDA calls here (CPU-testable through the
+// mgi_* exports of include/mg_internal.h).  Independent of oracle/.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "../../include/mg.h"
+#include "../../include/mg_internal.h"
+
+namespace {
+constexpr int kSlice = 32;  // rows per slice = lanes per warp
+
+inline void put_entry(double *val, int64_t e, int lane, int vpe, const double *src) {
+  // chunked layout, see mg_internal.h
+  double *base = val + (e - lane) * vpe;
+  const int half = vpe / 2;
+  for (int j = 0; j < half; ++j) {
+    base[64 * j + 2 * lane + 0] = src ? src[2 * j + 0] : 0.0;
+    base[64 * j + 2 * lane + 1] = src ? src[2 * j + 1] : 0.0;
+  }
+  if (vpe & 1) base[64 * half + lane] = src ? src[vpe - 1] : 0.0;
+}
+
+// Gauss-Jordan with partial pivoting on one bs x bs block (bs <= 8).
+int gj_block(int bs, const double *a_in, double *out) {
+  double a[64], inv[64];
+  std::memcpy(a, a_in, sizeof(double) * bs * bs);
+  for (int i = 0; i < bs * bs; ++i) inv[i] = 0.0;
+  for (int i = 0; i < bs; ++i) inv[i * bs + i] = 1.0;
+  for (int k = 0; k < bs; ++k) {
+    int p = k;
+    double best = std::fabs(a[k * bs + k]);
+    for (int r = k + 1; r < bs; ++r) {
+      double v = std::fabs(a[r * bs + k]);
+      if (v > best) { best = v; p = r; }
+    }
+    if (!(best > 0.0)) return MG_ERR_SINGULAR;
+    if (p != k)
+      for (int c = 0; c < bs; ++c) {
+        std::swap(a[k * bs + c], a[p * bs + c]);
+        std::swap(inv[k * bs + c], inv[p * bs + c]);
+      }
+    const double d = a[k * bs + k];
+    for (int c = 0; c < bs; ++c) { a[k * bs + c] /= d; inv[k * bs + c] /= d; }
+    for (int r = 0; r < bs; ++r) {
+      if (r == k) continue;
+      const double f = a[r * bs + k];
+      if (f == 0.0) continue;
+      for (int c = 0; c < bs; ++c) {
+        a[r * bs + c] -= f * a[k * bs + c];
+        inv[r * bs + c] -= f * inv[k * bs + c];
+      }
+    }
+  }
+  for (int i = 0; i < bs * bs; ++i)
+    if (!std::isfinite(inv[i])) return MG_ERR_SINGULAR;
+  std::memcpy(out, inv, sizeof(double) * bs * bs);
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int mgi_validate_csr(int64_t n, int64_t n_cols, const int64_t *rp, const int64_t *col,
+                     const double *val, int64_t vpe, int need_diag) {
+  if (n < 0 || !rp) return MG_ERR_INVALID_ARG;
+  if (rp[0] != 0) return MG_ERR_STRUCTURE;
+  int bad = 0, nonfinite = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad, nonfinite)
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t a = rp[i], b = rp[i + 1];
+    if (b < a) { bad |= 1; continue; }
+    bool diag = false;
+    for (int64_t k = a; k < b; ++k) {
+      const int64_t c = col[k];
+      if (c < 0 || c >= n_cols || (k > a && c <= col[k - 1])) bad |= 1;
+      if (c == i) diag = true;
+    }
+    if (need_diag && i < n_cols && !diag) bad |= 1;
+    if (val)
+      for (int64_t t = a * vpe; t < b * vpe; ++t)
+        if (!std::isfinite(val[t])) nonfinite |= 1;
+  }
+  if (bad) return MG_ERR_STRUCTURE;
+  if (nonfinite) return MG_ERR_NONFINITE;
+  return 0;
+}
+
+int mgi_sell_size(int64_t n, const int64_t *rp, int sigma, int64_t *n_slices, int64_t *n_entries) {
+  if (n < 0 || sigma < kSlice || sigma % kSlice) return MG_ERR_INVALID_ARG;
+  const int64_t ns = (n + kSlice - 1) / kSlice;
+  const int64_t nw = (n + sigma - 1) / sigma;
+  int64_t total = 0;
+#pragma omp parallel for schedule(static) reduction(+ : total)
+  for (int64_t w = 0; w < nw; ++w) {
+    const int64_t r0 = w * sigma, r1 = std::min<int64_t>(n, r0 + sigma);
+    std::vector<int64_t> len(r1 - r0);
+    for (int64_t i = r0; i < r1; ++i) len[i - r0] = rp[i + 1] - rp[i];
+    std::sort(len.begin(), len.end(), std::greater<int64_t>());
+    for (size_t s = 0; s < len.size(); s += kSlice) total += len[s] * kSlice;
+  }
+  *n_slices = ns;
+  *n_entries = total;
+  return 0;
+}
+
+int mgi_sell_fill(int64_t n, const int64_t *rp, const int64_t *col_in, const double *val_in, int vpe,
+                  int sigma, int64_t *slice_ptr, int32_t *perm, int32_t *col, double *val) {
+  if (n < 0 || sigma < kSlice || sigma % kSlice || vpe < 1) return MG_ERR_INVALID_ARG;
+  if (n >= (int64_t(1) << 31)) return MG_ERR_DIMENSION;
+  const int64_t ns = (n + kSlice - 1) / kSlice;
+  const int64_t nw = (n + sigma - 1) / sigma;
+  // 1. permutation: stable sort by length (descending) inside each window
+#pragma omp parallel for schedule(static)
+  for (int64_t w = 0; w < nw; ++w) {
+    const int64_t r0 = w * sigma, r1 = std::min<int64_t>(n, r0 + sigma);
+    std::vector<int32_t> idx(r1 - r0);
+    std::iota(idx.begin(), idx.end(), int32_t(r0));
+    std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) {
+      return (rp[a + 1] - rp[a]) > (rp[b + 1] - rp[b]);
+    });
+    std::copy(idx.begin(), idx.end(), perm + r0);
+  }
+  for (int64_t t = n; t < ns * kSlice; ++t) perm[t] = -1;
+  // 2. slice pointers
+  slice_ptr[0] = 0;
+  for (int64_t s = 0; s < ns; ++s) {
+    const int32_t r = perm[s * kSlice];
+    const int64_t len = r >= 0 ? rp[r + 1] - rp[r] : 0;
+    slice_ptr[s + 1] = slice_ptr[s] + len * kSlice;
+  }
+  // 3. entries
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t s = 0; s < ns; ++s) {
+    const int64_t len = (slice_ptr[s + 1] - slice_ptr[s]) / kSlice;
+    for (int lane = 0; lane < kSlice; ++lane) {
+      const int32_t r = perm[s * kSlice + lane];
+      const int64_t rl = r >= 0 ? rp[r + 1] - rp[r] : 0;
+      for (int64_t k = 0; k < len; ++k) {
+        const int64_t e = slice_ptr[s] + k * kSlice + lane;
+        if (k < rl) {
+          col[e] = int32_t(col_in[rp[r] + k]);
+          if (val) put_entry(val, e, lane, vpe, val_in + (rp[r] + k) * vpe);
+        } else {
+          // padding: zero value at a valid column (the row's last real column,
+          // or 0 for empty rows / padding lanes) -- valid for rectangular P, R too
+          col[e] = rl > 0 ? int32_t(col_in[rp[r] + rl - 1]) : 0;
+          if (val) put_entry(val, e, lane, vpe, nullptr);
+        }
+      }
+    }
+  }
+  return 0;
+}
+
+int mgi_csr_transpose(int64_t n_rows, int64_t n_cols, const int64_t *rp, const int64_t *col,
+                      const double *w, int wpe, int64_t *orp, int64_t *ocol, double *ow) {
+  if (n_rows < 0 || n_cols < 0 || wpe < 1) return MG_ERR_INVALID_ARG;
+  std::fill(orp, orp + n_cols + 1, int64_t(0));
+  const int64_t nnz = rp[n_rows];
+  for (int64_t t = 0; t < nnz; ++t) {
+    if (col[t] < 0 || col[t] >= n_cols) return MG_ERR_STRUCTURE;
+    orp[col[t] + 1]++;
+  }
+  for (int64_t j = 0; j < n_cols; ++j) orp[j + 1] += orp[j];
+  std::vector<int64_t> next(orp, orp + n_cols);
+  for (int64_t i = 0; i < n_rows; ++i)
+    for (int64_t t = rp[i]; t < rp[i + 1]; ++t) {
+      const int64_t d = next[col[t]]++;
+      ocol[d] = i;
+      for (int q = 0; q < wpe; ++q) ow[d * wpe + q] = w[t * wpe + q];
+    }
+  return 0;
+}
+
+int mgi_block_diag_inverse(int64_t n, int bs, const int64_t *rp, const int64_t *col,
+                           const double *val, double *dinv) {
+  if (bs < 1 || bs > 8) return MG_ERR_INVALID_ARG;
+  int status = 0;
+#pragma omp parallel for schedule(static) reduction(min : status)
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t kd = -1;
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
+      if (col[k] == i) { kd = k; break; }
+    if (kd < 0) { status = std::min(status, int(MG_ERR_STRUCTURE)); continue; }
+    const int st = gj_block(bs, val + kd * bs * bs, dinv + i * bs * bs);
+    if (st) status = std::min(status, st);
+  }
+  return status;
+}
+
+int mgi_dense_inverse(int64_t N, double *a, double *inv) {
+  if (N < 1) return MG_ERR_INVALID_ARG;
+  for (int64_t i = 0; i < N * N; ++i) inv[i] = 0.0;
+  for (int64_t i = 0; i < N; ++i) inv[i * N + i] = 1.0;
+  for (int64_t k = 0; k < N; ++k) {
+    int64_t p = k;
+    double best = std::fabs(a[k * N + k]);
+    for (int64_t r = k + 1; r < N; ++r) {
+      const double v = std::fabs(a[r * N + k]);
+      if (v > best) { best = v; p = r; }
+    }
+    if (!(best > 0.0)) return MG_ERR_SINGULAR;
+    if (p != k) {
+      std::swap_ranges(a + k * N, a + (k + 1) * N, a + p * N);
+      std::swap_ranges(inv + k * N, inv + (k + 1) * N, inv + p * N);
+    }
+    const double d = a[k * N + k];
+    for (int64_t c = 0; c < N; ++c) { a[k * N + c] /= d; inv[k * N + c] /= d; }
+    const double *ak = a + k * N;
+    const double *ik = inv + k * N;
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < N; ++r) {
+      if (r == k) continue;
+      const double f = a[r * N + k];
+      if (f == 0.0) continue;
+      double *ar = a + r * N;
+      double *ir = inv + r * N;
+      for (int64_t c = k; c < N; ++c) ar[c] -= f * ak[c];
+      for (int64_t c = 0; c < N; ++c) ir[c] -= f * ik[c];
+    }
+  }
+  for (int64_t i = 0; i < N * N; ++i)
+    if (!std::isfinite(inv[i])) return MG_ERR_SINGULAR;
+  return 0;
+}
+
+int mgi_bsr_to_dense(int64_t n, int bs, const int64_t *rp, const int64_t *col, const double *val,
+                     double *dense) {
+  const int64_t N = n * bs;
+  std::fill(dense, dense + N * N, 0.0);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
+      for (int r = 0; r < bs; ++r)
+        for (int c = 0; c < bs; ++c)
+          dense[(i * bs + r) * N + col[k] * bs + c] += val[(k * bs + r) * bs + c];
+  return 0;
+}
+
+int mgi_localize_columns(int64_t row_begin, int64_t row_end, const int64_t *rp, const int64_t *col,
+                         int64_t *local_col, int64_t *ghosts, int64_t *n_ghost) {
+  const int64_t n = row_end - row_begin;
+  if (n < 0) return MG_ERR_INVALID_ARG;
+  const int64_t nnz = rp[n];
+  int64_t ng = 0;
+  for (int64_t t = 0; t < nnz; ++t)
+    if (col[t] < row_begin || col[t] >= row_end) ghosts[ng++] = col[t];
+  std::sort(ghosts, ghosts + ng);
+  ng = std::unique(ghosts, ghosts + ng) - ghosts;
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < nnz; ++t) {
+    const int64_t c = col[t];
+    if (c >= row_begin && c < row_end) local_col[t] = c - row_begin;
+    else local_col[t] = n + (std::lower_bound(ghosts, ghosts + ng, c) - ghosts);
+  }
+  *n_ghost = ng;
+  return 0;
+}
+
+int mgi_owner(int64_t g, const int64_t *bounds, int nranks) {
+  return int(std::upper_bound(bounds, bounds + nranks + 1, g) - bounds) - 1;
+}
+
+}  // extern "C"

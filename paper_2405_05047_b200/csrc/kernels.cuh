@@ -1,0 +1,354 @@
+// Device kernels of libmgb200.so (sm_100a).  fp64, HBM-bandwidth bound.
+//
+// Every sparse operator (A_l, P_l, R_l = P_l^T, H) is stored in the
+// SELL-32-sigma layout of include/mg_internal.h: one warp per slice of 32
+// rows, lane = row, so the k-th entries of the 32 rows of a slice are
+// contiguous and a warp reads its matrix values with fully coalesced 16-byte
+// loads (2304 contiguous bytes per 3x3-block step), its column indices with
+// one 128-byte load, and never needs a cross-lane reduction.  Rows are
+// length-sorted inside windows of sigma rows so padding stays < 1%.
+//
+// Paper references (PAPER.md line numbers): residual SpMV r = b - A x
+// (Alg. gmg Step 2), smoother x + omega D^-1 (b - A x),
+// prolongation / restriction, coarse solve, GMRES MGS and
+// Givens.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mgk {
+
+constexpr int kWarpsPerCta = 8;
+constexpr int kCta = 32 * kWarpsPerCta;
+constexpr int kRedThreads = 512;
+
+struct Sell {
+  const int64_t *slice_ptr;  // [n_slices+1] entry offsets (multiples of 32)
+  const int32_t *perm;       // [n_slices*32] row of each lane, -1 = padding
+  const int32_t *col;        // [n_entries]
+  const double *val;         // [n_entries*vpe], chunked (mg_internal.h)
+  int64_t n_slices;
+};
+
+// ---------------------------------------------------------------------------
+// loads.  STREAM: data read once per pass (matrix values / columns of large
+// levels) -> evict-first (.cs); otherwise keep in cache (.nc / __ldg).
+// ---------------------------------------------------------------------------
+template <bool STREAM>
+__device__ __forceinline__ double2 ld_val2(const double *p) {
+  if constexpr (STREAM) return __ldcs(reinterpret_cast<const double2 *>(p));
+  else return __ldg(reinterpret_cast<const double2 *>(p));
+}
+template <bool STREAM>
+__device__ __forceinline__ double ld_val1(const double *p) {
+  if constexpr (STREAM) return __ldcs(p);
+  else return __ldg(p);
+}
+template <bool STREAM>
+__device__ __forceinline__ int ld_col(const int32_t *p) {
+  if constexpr (STREAM) return __ldcs(p);
+  else return __ldg(p);
+}
+
+// values of entry e of lane `lane`; gval = val + (e - lane) * VPE
+template <int VPE, bool STREAM>
+__device__ __forceinline__ void load_entry(const double *__restrict__ gval, int lane, double (&v)[VPE]) {
+#pragma unroll
+  for (int j = 0; j < VPE / 2; ++j) {
+    const double2 t = ld_val2<STREAM>(gval + 64 * j + 2 * lane);
+    v[2 * j] = t.x;
+    v[2 * j + 1] = t.y;
+  }
+  if constexpr (VPE & 1) v[VPE - 1] = ld_val1<STREAM>(gval + 64 * (VPE / 2) + lane);
+}
+
+// ---------------------------------------------------------------------------
+// A-pass kernels: y = alpha A x + beta y, r = b - A x, fused block-Jacobi
+// sweep out = x + omega D^-1 (b - A x).  Accumulation per output component in
+// CSR order (the oracle's order), with FMA.
+// ---------------------------------------------------------------------------
+enum { OP_SPMV = 0, OP_RESID = 1, OP_SWEEP = 2 };
+
+template <int BS, int OP, bool STREAM>
+__global__ void __launch_bounds__(kCta) k_sell_apply(Sell A, const double *__restrict__ x,
+                                                     const double *__restrict__ b,
+                                                     const double *__restrict__ dinv,
+                                                     double *__restrict__ out, double alpha, double beta) {
+  constexpr int V = BS * BS;
+  const int lane = threadIdx.x & 31;
+  const int64_t s = (int64_t(blockIdx.x) * kCta + threadIdx.x) >> 5;
+  if (s >= A.n_slices) return;
+  const int64_t e0 = A.slice_ptr[s], e1 = A.slice_ptr[s + 1];
+  const int row = A.perm[s * 32 + lane];
+  double acc[BS];
+#pragma unroll
+  for (int r = 0; r < BS; ++r) acc[r] = 0.0;
+#pragma unroll 4
+  for (int64_t g = e0; g < e1; g += 32) {
+    const int c = ld_col<STREAM>(A.col + g + lane);
+    double v[V];
+    load_entry<V, STREAM>(A.val + g * V, lane, v);
+    const double *xc = x + int64_t(c) * BS;
+    double xv[BS];
+#pragma unroll
+    for (int q = 0; q < BS; ++q) xv[q] = __ldg(xc + q);
+#pragma unroll
+    for (int r = 0; r < BS; ++r)
+#pragma unroll
+      for (int q = 0; q < BS; ++q) acc[r] = fma(v[r * BS + q], xv[q], acc[r]);
+  }
+  if (row < 0) return;
+  const int64_t o = int64_t(row) * BS;
+  if constexpr (OP == OP_SPMV) {
+#pragma unroll
+    for (int r = 0; r < BS; ++r) out[o + r] = (beta == 0.0) ? alpha * acc[r] : alpha * acc[r] + beta * out[o + r];
+  } else if constexpr (OP == OP_RESID) {
+#pragma unroll
+    for (int r = 0; r < BS; ++r) out[o + r] = __ldg(b + o + r) - acc[r];
+  } else {
+    double t[BS];
+#pragma unroll
+    for (int r = 0; r < BS; ++r) t[r] = __ldg(b + o + r) - acc[r];
+    double d[V];
+    load_entry<V, STREAM>(dinv + s * 32 * V, lane, d);
+#pragma unroll
+    for (int r = 0; r < BS; ++r) {
+      double u = 0.0;
+#pragma unroll
+      for (int q = 0; q < BS; ++q) u = fma(d[r * BS + q], t[q], u);
+      out[o + r] = fma(alpha, u, __ldg(x + o + r));
+    }
+  }
+}
+
+// First smoothing step from the zero guess: x = omega D^-1 b, A-free.
+template <int BS>
+__global__ void __launch_bounds__(kCta) k_sweep0(int64_t n_slices, const int32_t *__restrict__ perm,
+                                                 const double *__restrict__ dinv, const double *__restrict__ b,
+                                                 double *__restrict__ x, double omega) {
+  constexpr int V = BS * BS;
+  const int lane = threadIdx.x & 31;
+  const int64_t s = (int64_t(blockIdx.x) * kCta + threadIdx.x) >> 5;
+  if (s >= n_slices) return;
+  const int row = perm[s * 32 + lane];
+  double d[V];
+  load_entry<V, true>(dinv + s * 32 * V, lane, d);
+  if (row < 0) return;
+  const int64_t o = int64_t(row) * BS;
+  double t[BS];
+#pragma unroll
+  for (int q = 0; q < BS; ++q) t[q] = __ldg(b + o + q);
+#pragma unroll
+  for (int r = 0; r < BS; ++r) {
+    double u = 0.0;
+#pragma unroll
+    for (int q = 0; q < BS; ++q) u = fma(d[r * BS + q], t[q], u);
+    x[o + r] = omega * u;
+  }
+}
+
+// Transfer y = T x (ACCUM = 0) or y += T x (ACCUM = 1) with scalar weights
+// (WPE = 1) or per-component weights (WPE = BS): restriction R r (P:131,
+// P:337), prolongation x + P y, hanging interpolation H x.
+template <int BS, int WPE, bool ACCUM, bool STREAM>
+__global__ void __launch_bounds__(kCta) k_transfer(Sell T, const double *__restrict__ in,
+                                                   double *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = (int64_t(blockIdx.x) * kCta + threadIdx.x) >> 5;
+  if (s >= T.n_slices) return;
+  const int64_t e0 = T.slice_ptr[s], e1 = T.slice_ptr[s + 1];
+  const int row = T.perm[s * 32 + lane];
+  double acc[BS];
+#pragma unroll
+  for (int q = 0; q < BS; ++q) acc[q] = 0.0;
+#pragma unroll 4
+  for (int64_t g = e0; g < e1; g += 32) {
+    const int c = ld_col<STREAM>(T.col + g + lane);
+    double w[WPE];
+    load_entry<WPE, STREAM>(T.val + g * WPE, lane, w);
+    const double *xc = in + int64_t(c) * BS;
+#pragma unroll
+    for (int q = 0; q < BS; ++q) acc[q] = fma(w[WPE == 1 ? 0 : q], __ldg(xc + q), acc[q]);
+  }
+  if (row < 0) return;
+  const int64_t o = int64_t(row) * BS;
+#pragma unroll
+  for (int q = 0; q < BS; ++q) out[o + q] = ACCUM ? out[o + q] + acc[q] : acc[q];
+}
+
+// Coarse solve y = A_0^{-1} d with the dense inverse (row stride ld, even,
+// zero padded): one warp per row, 16-byte loads, shuffle reduction.
+__global__ void __launch_bounds__(kCta) k_dense_gemv(int64_t N, int64_t ld, const double *__restrict__ M,
+                                                     const double *__restrict__ d, double *__restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t(blockIdx.x) * kCta + threadIdx.x) >> 5;
+  if (r >= N) return;
+  const double *row = M + r * ld;
+  double acc = 0.0;
+  for (int64_t c = 2 * lane; c < N; c += 64) {
+    const double2 m = __ldg(reinterpret_cast<const double2 *>(row + c));
+    acc = fma(m.x, __ldg(d + c), acc);
+    if (c + 1 < N) acc = fma(m.y, __ldg(d + c + 1), acc);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) y[r] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// Reductions: deterministic single-pass grid reduction.  Each CTA reduces its
+// grid-stride share (warp shuffles + shared memory) to part[blockIdx.x]; the
+// last CTA to arrive (ticket) sums the partials in CTA order and writes the
+// result, so the value depends only on n and the fixed grid size.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (w == 0) {
+    t = lane < int(blockDim.x >> 5) ? sh[lane] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+  }
+  return t;  // valid in thread 0
+}
+
+// finish: last CTA sums part[0..gridDim) in order; result -> *res (sqrt if
+// SQRT); also copies to *res2 if non-null.
+template <bool SQRT>
+__device__ __forceinline__ void grid_finish(double blocksum, double *part, unsigned *ticket, double *res,
+                                            double *res2, double *sh) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = blocksum;
+    __threadfence();
+    last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double v = 0.0;
+  for (int i = threadIdx.x; i < int(gridDim.x); i += blockDim.x) v += __ldcg(part + i);
+  // ordered: each thread's strided sum, then a fixed tree
+  v = block_sum(v, sh);
+  if (threadIdx.x == 0) {
+    const double r = SQRT ? sqrt(v) : v;
+    *res = r;
+    if (res2) *res2 = r;
+    *ticket = 0u;
+  }
+}
+
+// MODE 0: res = (a, b).  MODE 1 (MGS step): a -= (*h) * c; res = (a_new, b)
+// (b == nullptr => res = ||a_new||_2, written also to *res2).
+template <int MODE, bool SQRT>
+__global__ void __launch_bounds__(kRedThreads) k_reduce(int64_t n, double *__restrict__ a, const double *__restrict__ b,
+                                                        const double *__restrict__ c, const double *__restrict__ h,
+                                                        double *part, unsigned *ticket, double *res, double *res2) {
+  __shared__ double sh[32];
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  double s = 0.0;
+  if constexpr (MODE == 0) {
+    for (int64_t i = tid; i < n; i += stride) s = fma(__ldg(a + i), __ldg(b + i), s);
+  } else {
+    const double hv = *h;
+    for (int64_t i = tid; i < n; i += stride) {
+      const double v = fma(-hv, __ldg(c + i), a[i]);
+      a[i] = v;
+      s = fma(v, b ? __ldg(b + i) : v, s);
+    }
+  }
+  const double bsum = block_sum(s, sh);
+  grid_finish<SQRT>(bsum, part, ticket, res, res2, sh);
+}
+
+// ---------------------------------------------------------------------------
+// GMRES helpers (right preconditioning, MGS, Givens, reading O8).
+// H column-major with leading dimension m+1.
+// ---------------------------------------------------------------------------
+struct GmresDev {
+  double *H;      // (m+1) x m
+  double *cs, *sn, *g, *y;
+  double *hn;     // [m] ||w|| before normalisation
+  double *beta;   // current restart residual norm
+  double *beta0;  // initial residual norm
+  double *out;    // [4]: est = |g_{j+1}|/beta0, flag, ...
+  int m;
+};
+
+// v0 = r / beta; g = (beta, 0, ...)
+__global__ void k_gmres_start(GmresDev st) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    for (int i = 0; i <= st.m; ++i) st.g[i] = 0.0;
+    st.g[0] = *st.beta;
+  }
+}
+
+__global__ void k_scale_div(int64_t n, const double *in, const double *den, double *out) {
+  const double d = *den;
+  if (d == 0.0) return;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = in[i] / d;
+}
+
+// Apply the previous rotations to column j, form the new one, update g and
+// the convergence flag (|g_{j+1}| <= rtol * beta0, or breakdown h_{j+1,j} = 0).
+__global__ void k_givens(GmresDev st, int j, double rtol) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int ld = st.m + 1;
+  double *h = st.H + int64_t(j) * ld;
+  const double hn = h[j + 1];
+  st.hn[j] = hn;
+  for (int i = 0; i < j; ++i) {
+    const double t = st.cs[i] * h[i] + st.sn[i] * h[i + 1];
+    h[i + 1] = -st.sn[i] * h[i] + st.cs[i] * h[i + 1];
+    h[i] = t;
+  }
+  const double rho = hypot(h[j], h[j + 1]);
+  st.cs[j] = h[j] / rho;
+  st.sn[j] = h[j + 1] / rho;
+  h[j] = rho;
+  h[j + 1] = 0.0;
+  st.g[j + 1] = -st.sn[j] * st.g[j];
+  st.g[j] = st.cs[j] * st.g[j];
+  const double b0 = *st.beta0;
+  st.out[0] = fabs(st.g[j + 1]) / b0;
+  st.out[1] = (fabs(st.g[j + 1]) <= rtol * b0 || hn == 0.0) ? 1.0 : 0.0;
+  st.out[2] = hn;
+}
+
+// Back substitution H(0:k,0:k) y = g(0:k).
+__global__ void k_backsolve(GmresDev st, int k) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int ld = st.m + 1;
+  for (int i = k - 1; i >= 0; --i) {
+    double s = 0.0;
+    for (int l = i + 1; l < k; ++l) s += st.H[int64_t(l) * ld + i] * st.y[l];
+    st.y[i] = (st.g[i] - s) / st.H[int64_t(i) * ld + i];
+  }
+}
+
+// x += sum_{t<k} y_t Z_t  (Z: k vectors of length n, contiguous).
+__global__ void k_update_x(int64_t n, int k, const double *__restrict__ y, const double *__restrict__ Z,
+                           double *__restrict__ x) {
+  __shared__ double ys[64];
+  if (threadIdx.x < k) ys[threadIdx.x] = y[threadIdx.x];
+  __syncthreads();
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    double v = x[i];
+    for (int t = 0; t < k; ++t) v = fma(ys[t], __ldg(Z + int64_t(t) * n + i), v);
+    x[i] = v;
+  }
+}
+
+// Finite check of a vector (any NaN/Inf -> *flag = 1).
+__global__ void k_nonfinite(int64_t n, const double *__restrict__ a, int *flag) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    if (!isfinite(a[i])) *flag = 1;
+}
+
+}  // namespace mgk

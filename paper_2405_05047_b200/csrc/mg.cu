@@ -1,0 +1,1040 @@
+// libmgb200.so: the C ABI of include/mg.h.  Context and level state, device
+// upload of the SELL-32-sigma operators built by host.cpp, the V-cycle of
+// Alg. `gmg` with CUDA-graph capture, and the MG iteration /
+// MG-preconditioned GMRES drivers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/mg.h"
+#include "../../include/mg_internal.h"
+#include "kernels.cuh"
+
+#define MGB200_VERSION "mgb200 0.1 (sm_100a, fp64, SELL-32-sigma)"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_tally = 0;  // kernel launches issued by this thread (bench accounting)
+
+mg_status fail(mg_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CU(x)                                                                           \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess) {                                                            \
+      if (e_ == cudaErrorMemoryAllocation) return fail(MG_ERR_OOM, "%s: out of memory", #x); \
+      return fail(MG_ERR_CUDA, "%s: %s", #x, cudaGetErrorString(e_));                   \
+    }                                                                                   \
+  } while (0)
+#define TRY(x)                   \
+  do {                           \
+    mg_status s_ = (x);          \
+    if (s_ != MG_OK) return s_;  \
+  } while (0)
+
+constexpr int kSigma = 4096;                       // sorting window of SELL-32-sigma
+constexpr size_t kStreamBytes = size_t(32) << 20;  // operators larger than this use evict-first loads
+
+template <class T>
+struct DevArray {
+  T *p = nullptr;
+  size_t n = 0;
+  DevArray() = default;
+  DevArray(const DevArray &) = delete;
+  DevArray &operator=(const DevArray &) = delete;
+  DevArray(DevArray &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DevArray &operator=(DevArray &&o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p, n = o.n;
+      o.p = nullptr, o.n = 0;
+    }
+    return *this;
+  }
+  ~DevArray() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  mg_status alloc(size_t count) {
+    release();
+    if (count == 0) count = 1;
+    CU(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+    return MG_OK;
+  }
+  mg_status upload(const T *h, size_t count) {
+    TRY(alloc(count));
+    if (h && count) CU(cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice));
+    return MG_OK;
+  }
+};
+
+struct SellOp {
+  DevArray<int64_t> slice_ptr;
+  DevArray<int32_t> perm, col;
+  DevArray<double> val;
+  std::vector<int32_t> perm_host;
+  int64_t n_rows = 0, n_slices = 0, n_entries = 0;
+  int vpe = 0;
+  bool stream = false;
+  bool set = false;
+  mgk::Sell view() const { return mgk::Sell{slice_ptr.p, perm.p, col.p, val.p, n_slices}; }
+};
+
+// Build SELL-32-sigma on the host and upload it.
+mg_status build_sell(SellOp &op, int64_t n, const int64_t *rp, const int64_t *col, const double *val, int vpe) {
+  int64_t ns = 0, ne = 0;
+  int st = mgi_sell_size(n, rp, kSigma, &ns, &ne);
+  if (st) return fail(mg_status(st), "sell layout: invalid input");
+  std::vector<int64_t> sp(ns + 1);
+  std::vector<int32_t> perm(ns * 32), c(ne);
+  std::vector<double> v(ne * vpe);
+  st = mgi_sell_fill(n, rp, col, val, vpe, kSigma, sp.data(), perm.data(), c.data(), v.data());
+  if (st) return fail(mg_status(st), "sell layout: fill failed (%d)", st);
+  TRY(op.slice_ptr.upload(sp.data(), sp.size()));
+  TRY(op.perm.upload(perm.data(), perm.size()));
+  TRY(op.col.upload(c.data(), c.size()));
+  TRY(op.val.upload(v.data(), v.size()));
+  op.perm_host.swap(perm);
+  op.n_rows = n;
+  op.n_slices = ns;
+  op.n_entries = ne;
+  op.vpe = vpe;
+  op.stream = size_t(ne) * (8 * vpe + 4) > kStreamBytes;
+  op.set = true;
+  return MG_OK;
+}
+
+// Host copies of (possibly device-resident) input arrays.
+template <class T>
+mg_status fetch(std::vector<T> &dst, const T *src, size_t count, int mem) {
+  dst.resize(count);
+  if (count == 0) return MG_OK;
+  if (!src) return fail(MG_ERR_INVALID_ARG, "NULL input array");
+  if (mem == MG_MEM_DEVICE) CU(cudaMemcpy(dst.data(), src, count * sizeof(T), cudaMemcpyDeviceToHost));
+  else if (mem == MG_MEM_HOST) std::memcpy(dst.data(), src, count * sizeof(T));
+  else return fail(MG_ERR_INVALID_ARG, "mem must be MG_MEM_HOST or MG_MEM_DEVICE");
+  return MG_OK;
+}
+
+struct Level {
+  bool declared = false;
+  int64_t n_global = 0, row_begin = 0, row_end = 0, n = 0;
+  SellOp A;
+  int64_t nnzb = 0;
+  std::vector<double> diag_host;  // diagonal blocks until D^-1 is built
+  std::vector<double> dinv_host;  // user-supplied D^-1 (row-major blocks)
+  std::vector<int64_t> rp0, col0;  // level-0 copy for the dense coarse inverse
+  std::vector<double> val0;
+  DevArray<double> dinv;          // sliced D^-1 (chunked like a 1-entry slice)
+  bool dinv_ready = false;
+  SellOp P, R;  // P_{l-1}: level l-1 -> l, R_{l-1} = P^T
+  int wpe = 1;
+  int64_t nnz_p = 0;
+  double omega = 0.0;
+  int nu_pre = -1, nu_post = -1;
+  DevArray<double> x, b, w;  // correction, restricted rhs, work (ping-pong / residual)
+};
+
+struct GraphExec {
+  cudaGraphExec_t exec = nullptr;
+  int64_t kernels = 0;
+};
+
+struct GraphKey {
+  const double *x;
+  const double *b;
+  int zero;
+  bool operator<(const GraphKey &o) const { return std::tie(x, b, zero) < std::tie(o.x, o.b, o.zero); }
+};
+
+}  // namespace
+
+struct mg_ctx_s {
+  mg_config cfg{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int n_sm = 148;
+  std::vector<Level> lv;
+  SellOp H;
+  DevArray<double> cinv;  // dense A_0^-1, row stride cld
+  int64_t cN = 0, cld = 0;
+  DevArray<double> red_part, scal;
+  DevArray<unsigned> ticket;
+  bool finalized = false;
+  std::map<GraphKey, GraphExec> graphs;
+  int64_t launches = 0;
+  // GMRES workspace
+  int gm_m = 0;
+  DevArray<double> gm_V, gm_Z, gm_state;
+  double *gm_host = nullptr;  // pinned [8]
+  mgk::GmresDev gm{};
+  ~mg_ctx_s() {
+    for (auto &kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+    if (gm_host) cudaFreeHost(gm_host);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+  void invalidate() {
+    for (auto &kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+    graphs.clear();
+    finalized = false;
+  }
+  int bs() const { return cfg.block_size; }
+  int L() const { return cfg.n_levels - 1; }
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+inline unsigned grid_for_slices(int64_t n_slices) {
+  return unsigned((n_slices + mgk::kWarpsPerCta - 1) / mgk::kWarpsPerCta);
+}
+
+mg_status check_launch(const char *what = "kernel") {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(MG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return MG_OK;
+}
+
+// --- dispatch over block size / op / cache hint ---------------------------
+template <int BS, int OP>
+void launch_apply_t(const SellOp &A, const double *x, const double *b, const double *dinv, double *out, double alpha,
+                    double beta, cudaStream_t st) {
+  if (A.n_slices == 0) return;
+  const unsigned g = grid_for_slices(A.n_slices);
+  if (A.stream)
+    ++g_tally, mgk::k_sell_apply<BS, OP, true><<<g, mgk::kCta, 0, st>>>(A.view(), x, b, dinv, out, alpha, beta);
+  else
+    ++g_tally, mgk::k_sell_apply<BS, OP, false><<<g, mgk::kCta, 0, st>>>(A.view(), x, b, dinv, out, alpha, beta);
+}
+
+template <int OP>
+mg_status launch_apply(int bs, const SellOp &A, const double *x, const double *b, const double *dinv, double *out,
+                       double alpha, double beta, cudaStream_t st) {
+  switch (bs) {
+    case 1: launch_apply_t<1, OP>(A, x, b, dinv, out, alpha, beta, st); break;
+    case 2: launch_apply_t<2, OP>(A, x, b, dinv, out, alpha, beta, st); break;
+    case 3: launch_apply_t<3, OP>(A, x, b, dinv, out, alpha, beta, st); break;
+    case 4: launch_apply_t<4, OP>(A, x, b, dinv, out, alpha, beta, st); break;
+    default: return fail(MG_ERR_INVALID_ARG, "block size %d not supported", bs);
+  }
+  return check_launch(OP == mgk::OP_SWEEP ? "sweep" : OP == mgk::OP_RESID ? "residual" : "spmv");
+}
+
+template <int BS>
+void launch_sweep0_t(const SellOp &A, const double *dinv, const double *b, double *x, double omega, cudaStream_t st) {
+  if (A.n_slices == 0) return;
+  ++g_tally, mgk::k_sweep0<BS><<<grid_for_slices(A.n_slices), mgk::kCta, 0, st>>>(A.n_slices, A.perm.p, dinv, b, x, omega);
+}
+
+mg_status launch_sweep0(int bs, const SellOp &A, const double *dinv, const double *b, double *x, double omega,
+                        cudaStream_t st) {
+  switch (bs) {
+    case 1: launch_sweep0_t<1>(A, dinv, b, x, omega, st); break;
+    case 2: launch_sweep0_t<2>(A, dinv, b, x, omega, st); break;
+    case 3: launch_sweep0_t<3>(A, dinv, b, x, omega, st); break;
+    case 4: launch_sweep0_t<4>(A, dinv, b, x, omega, st); break;
+    default: return fail(MG_ERR_INVALID_ARG, "block size %d not supported", bs);
+  }
+  return check_launch("sweep0");
+}
+
+template <int BS, int WPE, bool ACC>
+void launch_transfer_t(const SellOp &T, const double *in, double *out, cudaStream_t st) {
+  if (T.n_slices == 0) return;
+  const unsigned g = grid_for_slices(T.n_slices);
+  if (T.stream)
+    ++g_tally, mgk::k_transfer<BS, WPE, ACC, true><<<g, mgk::kCta, 0, st>>>(T.view(), in, out);
+  else
+    ++g_tally, mgk::k_transfer<BS, WPE, ACC, false><<<g, mgk::kCta, 0, st>>>(T.view(), in, out);
+}
+
+template <int BS, bool ACC>
+void launch_transfer_bs(const SellOp &T, const double *in, double *out, cudaStream_t st) {
+  if (T.vpe == 1 || BS == 1) launch_transfer_t<BS, 1, ACC>(T, in, out, st);
+  else launch_transfer_t<BS, BS, ACC>(T, in, out, st);
+}
+
+mg_status launch_transfer(int bs, bool acc, const SellOp &T, const double *in, double *out, cudaStream_t st) {
+  switch (bs) {
+    case 1: acc ? launch_transfer_bs<1, true>(T, in, out, st) : launch_transfer_bs<1, false>(T, in, out, st); break;
+    case 2: acc ? launch_transfer_bs<2, true>(T, in, out, st) : launch_transfer_bs<2, false>(T, in, out, st); break;
+    case 3: acc ? launch_transfer_bs<3, true>(T, in, out, st) : launch_transfer_bs<3, false>(T, in, out, st); break;
+    case 4: acc ? launch_transfer_bs<4, true>(T, in, out, st) : launch_transfer_bs<4, false>(T, in, out, st); break;
+    default: return fail(MG_ERR_INVALID_ARG, "block size %d not supported", bs);
+  }
+  return check_launch(acc ? "prolong-add" : "transfer");
+}
+
+// --- reductions --------------------------------------------------------------
+unsigned red_grid(const mg_ctx_s *c, int64_t n) {
+  const int64_t want = (n + mgk::kRedThreads * 4 - 1) / (mgk::kRedThreads * 4);
+  return unsigned(std::max<int64_t>(1, std::min<int64_t>(want, 2 * c->n_sm)));
+}
+
+// res (device) = (a, b)
+mg_status dev_dot(mg_ctx_s *c, int64_t n, const double *a, const double *b, double *res, bool sqrt_) {
+  const unsigned g = red_grid(c, n);
+  if (sqrt_)
+    ++g_tally, mgk::k_reduce<0, true><<<g, mgk::kRedThreads, 0, c->stream>>>(n, const_cast<double *>(a), b, nullptr, nullptr,
+                                                                   c->red_part.p, c->ticket.p, res, nullptr);
+  else
+    ++g_tally, mgk::k_reduce<0, false><<<g, mgk::kRedThreads, 0, c->stream>>>(n, const_cast<double *>(a), b, nullptr, nullptr,
+                                                                    c->red_part.p, c->ticket.p, res, nullptr);
+  return check_launch("dot");
+}
+
+// MGS step: a -= (*h) v ; res = (a, u) or ||a|| (u == nullptr; also -> res2)
+mg_status dev_axpy_dot(mg_ctx_s *c, int64_t n, double *a, const double *v, const double *h, const double *u,
+                       double *res) {
+  const unsigned g = red_grid(c, n);
+  if (u)
+    ++g_tally, mgk::k_reduce<1, false><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, u, v, h, c->red_part.p, c->ticket.p, res,
+                                                                    nullptr);
+  else
+    ++g_tally, mgk::k_reduce<1, true><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, nullptr, v, h, c->red_part.p, c->ticket.p,
+                                                                   res, nullptr);
+  return check_launch("axpy-dot");
+}
+
+// --- dense coarse inverse on the device (in-place Gauss-Jordan, partial pivoting)
+__global__ void k_gj_pivot(int64_t N, int64_t ld, double *a, int64_t k, int64_t *piv, double *f, int *singular) {
+  __shared__ double bv[1024];
+  __shared__ int64_t bi[1024];
+  double best = -1.0;
+  int64_t bidx = k;
+  for (int64_t r = k + threadIdx.x; r < N; r += blockDim.x) {
+    const double v = fabs(a[r * ld + k]);
+    if (v > best) { best = v; bidx = r; }
+  }
+  bv[threadIdx.x] = best;
+  bi[threadIdx.x] = bidx;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const double v2 = bv[threadIdx.x + s];
+      const int64_t i2 = bi[threadIdx.x + s];
+      if (v2 > bv[threadIdx.x] || (v2 == bv[threadIdx.x] && i2 < bi[threadIdx.x])) {
+        bv[threadIdx.x] = v2;
+        bi[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  const int64_t p = bi[0];
+  const double pmax = bv[0];
+  if (!(pmax > 0.0)) {
+    if (threadIdx.x == 0) *singular = 1;
+    return;
+  }
+  if (threadIdx.x == 0) piv[k] = p;
+  if (p != k)
+    for (int64_t c = threadIdx.x; c < N; c += blockDim.x) {
+      const double t = a[k * ld + c];
+      a[k * ld + c] = a[p * ld + c];
+      a[p * ld + c] = t;
+    }
+  __syncthreads();
+  const double d = a[k * ld + k];
+  __syncthreads();
+  if (threadIdx.x == 0) a[k * ld + k] = 1.0;
+  __syncthreads();
+  for (int64_t c = threadIdx.x; c < N; c += blockDim.x) a[k * ld + c] /= d;
+  for (int64_t r = threadIdx.x; r < N; r += blockDim.x) {
+    if (r == k) { f[r] = 0.0; continue; }
+    f[r] = a[r * ld + k];
+    a[r * ld + k] = 0.0;
+  }
+}
+
+__global__ void k_gj_eliminate(int64_t N, int64_t ld, double *a, int64_t k, const double *f) {
+  const int64_t r = blockIdx.y;
+  const double fr = f[r];
+  if (r == k || fr == 0.0) return;
+  const double *ak = a + k * ld;
+  double *ar = a + r * ld;
+  for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < N; c += int64_t(gridDim.x) * blockDim.x)
+    ar[c] = fma(-fr, ak[c], ar[c]);
+}
+
+__global__ void k_gj_unswap(int64_t N, int64_t ld, double *a, const int64_t *piv) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= N) return;
+  double *ar = a + r * ld;
+  for (int64_t k = N - 1; k >= 0; --k) {
+    const int64_t p = piv[k];
+    if (p != k) {
+      const double t = ar[k];
+      ar[k] = ar[p];
+      ar[p] = t;
+    }
+  }
+}
+
+mg_status build_coarse_inverse(mg_ctx_s *c) {
+  Level &L0 = c->lv[0];
+  const int bs = c->bs();
+  const int64_t N = L0.n * bs;
+  const int64_t ld = (N + 1) & ~int64_t(1);
+  std::vector<double> dense(size_t(N) * N);
+  mgi_bsr_to_dense(L0.n, bs, L0.rp0.data(), L0.col0.data(), L0.val0.data(), dense.data());
+  std::vector<double> padded(size_t(N) * ld, 0.0);
+  for (int64_t r = 0; r < N; ++r) std::memcpy(&padded[r * ld], &dense[r * N], N * sizeof(double));
+  TRY(c->cinv.upload(padded.data(), padded.size()));
+  DevArray<int64_t> piv;
+  DevArray<double> f;
+  DevArray<int> sing;
+  TRY(piv.alloc(N));
+  TRY(f.alloc(N));
+  TRY(sing.alloc(1));
+  CU(cudaMemsetAsync(sing.p, 0, sizeof(int), c->stream));
+  const unsigned gx = unsigned(std::min<int64_t>((N + 255) / 256, 64));
+  for (int64_t k = 0; k < N; ++k) {
+    k_gj_pivot<<<1, 1024, 0, c->stream>>>(N, ld, c->cinv.p, k, piv.p, f.p, sing.p);
+    k_gj_eliminate<<<dim3(gx, unsigned(N)), 256, 0, c->stream>>>(N, ld, c->cinv.p, k, f.p);
+  }
+  k_gj_unswap<<<unsigned((N + 255) / 256), 256, 0, c->stream>>>(N, ld, c->cinv.p, piv.p);
+  TRY(check_launch());
+  int s = 0;
+  CU(cudaMemcpyAsync(&s, sing.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (s) return fail(MG_ERR_SINGULAR, "coarse matrix A_0 is singular");
+  c->cN = N;
+  c->cld = ld;
+  return MG_OK;
+}
+
+// sliced D^-1 from row-major blocks (lane order = A's perm)
+mg_status upload_dinv(Level &L, int bs, const std::vector<double> &blocks) {
+  const int V = bs * bs;
+  const int64_t ns = L.A.n_slices;
+  std::vector<double> sl(size_t(ns) * 32 * V, 0.0);
+  for (int64_t s = 0; s < ns; ++s)
+    for (int lane = 0; lane < 32; ++lane) {
+      const int32_t r = L.A.perm_host[s * 32 + lane];
+      if (r < 0) continue;
+      double *base = &sl[size_t(s) * 32 * V];
+      const double *src = &blocks[size_t(r) * V];
+      for (int j = 0; j < V / 2; ++j) {
+        base[64 * j + 2 * lane] = src[2 * j];
+        base[64 * j + 2 * lane + 1] = src[2 * j + 1];
+      }
+      if (V & 1) base[64 * (V / 2) + lane] = src[V - 1];
+    }
+  TRY(L.dinv.upload(sl.data(), sl.size()));
+  L.dinv_ready = true;
+  return MG_OK;
+}
+
+double lv_omega(const mg_ctx_s *c, const Level &L) { return L.omega > 0.0 ? L.omega : c->cfg.omega; }
+int lv_nu_pre(const mg_ctx_s *c, const Level &L) { return L.nu_pre >= 0 ? L.nu_pre : c->cfg.nu_pre; }
+int lv_nu_post(const mg_ctx_s *c, const Level &L) { return L.nu_post >= 0 ? L.nu_post : c->cfg.nu_post; }
+
+mg_status finalize(mg_ctx_s *c) {
+  if (c->finalized) return MG_OK;
+  const int bs = c->bs();
+  for (int l = 0; l <= c->L(); ++l) {
+    Level &L = c->lv[l];
+    if (!L.declared) return fail(MG_ERR_STATE, "level %d not created (mg_create_level)", l);
+    if (!L.A.set) return fail(MG_ERR_STATE, "level %d has no matrix (mg_set_matrix)", l);
+    if (l > 0 && !L.P.set) return fail(MG_ERR_STATE, "level %d has no transfer (mg_set_transfer)", l);
+  }
+  for (int l = 0; l <= c->L(); ++l) {
+    Level &L = c->lv[l];
+    if (!L.dinv_ready) {
+      if (!L.dinv_host.empty()) {
+        TRY(upload_dinv(L, bs, L.dinv_host));
+      } else {
+        const int V = bs * bs;
+        std::vector<double> inv(size_t(L.n) * V);
+        // identity row pointers over the stored diagonal blocks
+        std::vector<int64_t> rp(L.n + 1), cl(L.n);
+        for (int64_t i = 0; i <= L.n; ++i) rp[i] = i;
+        for (int64_t i = 0; i < L.n; ++i) cl[i] = i;
+        const int st = mgi_block_diag_inverse(L.n, bs, rp.data(), cl.data(), L.diag_host.data(), inv.data());
+        if (st == MG_ERR_SINGULAR) return fail(MG_ERR_SINGULAR, "level %d: singular diagonal block", l);
+        if (st) return fail(mg_status(st), "level %d: D^-1 failed", l);
+        TRY(upload_dinv(L, bs, inv));
+      }
+      std::vector<double>().swap(L.diag_host);
+    }
+    const size_t nv = size_t(L.n) * bs;
+    if (L.w.n < nv) TRY(L.w.alloc(nv));
+    if (l < c->L()) {
+      if (L.x.n < nv) TRY(L.x.alloc(nv));
+      if (L.b.n < nv) TRY(L.b.alloc(nv));
+    }
+  }
+  if (c->cfg.coarse_mode == MG_COARSE_DIRECT && c->cN == 0) TRY(build_coarse_inverse(c));
+  if (!c->red_part.p) {
+    TRY(c->red_part.alloc(2 * c->n_sm + 8));
+    TRY(c->ticket.alloc(1));
+    CU(cudaMemset(c->ticket.p, 0, sizeof(unsigned)));
+    TRY(c->scal.alloc(16));
+  }
+  c->finalized = true;
+  return MG_OK;
+}
+
+// --- V-cycle pieces (stream-ordered, capturable) -----------------------------
+mg_status smooth(mg_ctx_s *c, int l, double *x, const double *b, int k, bool zero) {
+  Level &L = c->lv[l];
+  const int bs = c->bs();
+  const double om = lv_omega(c, L);
+  if (k <= 0) {
+    if (zero) CU(cudaMemsetAsync(x, 0, size_t(L.n) * bs * sizeof(double), c->stream));
+    return MG_OK;
+  }
+  if (zero) {
+    TRY(launch_sweep0(bs, L.A, L.dinv.p, b, x, om, c->stream));
+    --k;
+  }
+  double *src = x, *dst = L.w.p;
+  for (int i = 0; i < k; ++i) {
+    TRY(launch_apply<mgk::OP_SWEEP>(bs, L.A, src, b, L.dinv.p, dst, om, 0.0, c->stream));
+    std::swap(src, dst);
+  }
+  if (src != x) CU(cudaMemcpyAsync(x, src, size_t(L.n) * bs * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  return MG_OK;
+}
+
+mg_status coarse_solve(mg_ctx_s *c, const double *b, double *x) {
+  if (c->cfg.coarse_mode == MG_COARSE_DIRECT) {
+    const unsigned g = unsigned((c->cN + mgk::kWarpsPerCta - 1) / mgk::kWarpsPerCta);
+    ++g_tally, mgk::k_dense_gemv<<<g, mgk::kCta, 0, c->stream>>>(c->cN, c->cld, c->cinv.p, b, x);
+    return check_launch();
+  }
+  return smooth(c, 0, x, b, std::max(1, c->cfg.coarse_sweeps), true);
+}
+
+// GMG(l, x, b) of Alg. gmg; zero: x enters as 0.
+mg_status vcycle_rec(mg_ctx_s *c, int l, double *x, const double *b, bool zero) {
+  if (l == 0) return coarse_solve(c, b, x);  // Step 0; ignores x (Z21)
+  Level &L = c->lv[l];
+  Level &C = c->lv[l - 1];
+  const int bs = c->bs();
+  TRY(smooth(c, l, x, b, lv_nu_pre(c, L), zero));                                             // Step 1
+  TRY(launch_apply<mgk::OP_RESID>(bs, L.A, x, b, nullptr, L.w.p, 1.0, 0.0, c->stream));       // Step 2
+  TRY(launch_transfer(bs, false, L.R, L.w.p, C.b.p, c->stream));                                //  d = R r
+  TRY(vcycle_rec(c, l - 1, C.x.p, C.b.p, true));                                               // Step 3
+  TRY(launch_transfer(bs, true, L.P, C.x.p, x, c->stream));                                    // Step 4
+  return smooth(c, l, x, b, lv_nu_post(c, L), false);                                          // Step 5
+}
+
+mg_status run_vcycle(mg_ctx_s *c, double *x, const double *b, bool zero) {
+  if (!c->cfg.use_graphs) return vcycle_rec(c, c->L(), x, b, zero);
+  const GraphKey key{x, b, zero ? 1 : 0};
+  auto it = c->graphs.find(key);
+  if (it == c->graphs.end()) {
+    cudaGraph_t graph = nullptr;
+    const int64_t t0 = g_tally;
+    CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const mg_status st = vcycle_rec(c, c->L(), x, b, zero);
+    const int64_t captured = g_tally - t0;
+    g_tally = t0;
+    const cudaError_t ee = cudaStreamEndCapture(c->stream, &graph);
+    if (st != MG_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    if (ee != cudaSuccess) return fail(MG_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ee));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) return fail(MG_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ie));
+    if (c->graphs.size() > 256) {
+      for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
+      c->graphs.clear();
+    }
+    it = c->graphs.emplace(key, GraphExec{exec, captured}).first;
+  }
+  CU(cudaGraphLaunch(it->second.exec, c->stream));
+  g_tally += it->second.kernels;
+  return MG_OK;
+}
+
+struct Tally {
+  mg_ctx_s *c;
+  int64_t t0;
+  explicit Tally(mg_ctx_s *ctx) : c(ctx), t0(g_tally) {}
+  ~Tally() {
+    if (c) c->launches += g_tally - t0;
+  }
+};
+
+mg_status check_ctx(mg_ctx_s *c) {
+  if (!c) return fail(MG_ERR_INVALID_ARG, "NULL context");
+  return MG_OK;
+}
+
+mg_status check_level(mg_ctx_s *c, int level) {
+  TRY(check_ctx(c));
+  if (level < 0 || level > c->L()) return fail(MG_ERR_INVALID_ARG, "level %d out of range [0, %d]", level, c->L());
+  if (!c->lv[level].declared) return fail(MG_ERR_STATE, "level %d not created", level);
+  return MG_OK;
+}
+
+mg_status ensure_gmres(mg_ctx_s *c, int m) {
+  const int64_t N = c->lv[c->L()].n * c->bs();
+  if (c->gm_m >= m && c->gm_V.p) return MG_OK;
+  TRY(c->gm_V.alloc(size_t(m + 1) * N));
+  TRY(c->gm_Z.alloc(size_t(m) * N));
+  const size_t ns = size_t(m + 1) * m + 6 * size_t(m + 1) + 16;
+  TRY(c->gm_state.alloc(ns));
+  CU(cudaMemset(c->gm_state.p, 0, ns * sizeof(double)));
+  if (!c->gm_host) CU(cudaMallocHost(&c->gm_host, 16 * sizeof(double)));
+  double *p = c->gm_state.p;
+  mgk::GmresDev &g = c->gm;
+  g.m = m;
+  g.H = p; p += size_t(m + 1) * m;
+  g.cs = p; p += m + 1;
+  g.sn = p; p += m + 1;
+  g.g = p; p += m + 1;
+  g.y = p; p += m + 1;
+  g.hn = p; p += m + 1;
+  g.beta = p; p += 1;
+  g.beta0 = p; p += 1;
+  g.out = p; p += 4;
+  c->gm_m = m;
+  return MG_OK;
+}
+
+}  // namespace
+
+// =============================================================================
+// C ABI
+// =============================================================================
+extern "C" {
+
+const char *mg_last_error(void) { return g_err.c_str(); }
+const char *mg_version(void) { return MGB200_VERSION; }
+
+mg_status mg_create(mg_ctx *out, const mg_config *cfg, int device, void *cuda_stream, const mg_comm *comm) {
+  if (!out || !cfg) return fail(MG_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  if (cfg->n_levels < 1 || cfg->n_levels > 64) return fail(MG_ERR_INVALID_ARG, "n_levels must be in [1, 64]");
+  if (cfg->block_size < 1 || cfg->block_size > 4) return fail(MG_ERR_INVALID_ARG, "block_size must be in [1, 4]");
+  if (cfg->nu_pre < 0 || cfg->nu_post < 0) return fail(MG_ERR_INVALID_ARG, "nu_pre/nu_post must be >= 0");
+  if (!(cfg->omega > 0.0) || !std::isfinite(cfg->omega)) return fail(MG_ERR_INVALID_ARG, "omega must be > 0");
+  if (cfg->coarse_mode != MG_COARSE_DIRECT && cfg->coarse_mode != MG_COARSE_SMOOTH)
+    return fail(MG_ERR_INVALID_ARG, "bad coarse_mode");
+  if (comm && comm->nranks > 1) return fail(MG_ERR_INVALID_ARG, "multi-GPU contexts are not built into this library");
+  DeviceGuard dg(device);
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(MG_ERR_INVALID_ARG, "device %d out of range", device);
+  auto *c = new mg_ctx_s();
+  c->cfg = *cfg;
+  c->device = device;
+  cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device);
+  if (cuda_stream) {
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+  } else {
+    if (cudaStreamCreate(&c->stream) != cudaSuccess) {
+      delete c;
+      return fail(MG_ERR_CUDA, "cudaStreamCreate failed");
+    }
+    c->own_stream = true;
+  }
+  c->lv.resize(cfg->n_levels);
+  *out = c;
+  return MG_OK;
+}
+
+mg_status mg_destroy(mg_ctx ctx) {
+  if (!ctx) return MG_OK;
+  DeviceGuard dg(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  delete ctx;
+  return MG_OK;
+}
+
+mg_status mg_create_level(mg_ctx c, int level, int64_t n_rows_global, int64_t row_begin, int64_t row_end) {
+  TRY(check_ctx(c));
+  if (level < 0 || level > c->L()) return fail(MG_ERR_INVALID_ARG, "level %d out of range", level);
+  if (n_rows_global < 1 || n_rows_global >= (int64_t(1) << 31))
+    return fail(MG_ERR_DIMENSION, "n_rows_global must be in [1, 2^31)");
+  if (row_begin != 0 || row_end != n_rows_global)
+    return fail(MG_ERR_INVALID_ARG, "single-GPU context: a level must own all rows");
+  Level &L = c->lv[level];
+  L.declared = true;
+  L.n_global = n_rows_global;
+  L.row_begin = row_begin;
+  L.row_end = row_end;
+  L.n = row_end - row_begin;
+  c->invalidate();
+  return MG_OK;
+}
+
+mg_status mg_set_matrix(mg_ctx c, int level, const int64_t *row_ptr, const int64_t *col, const double *vals,
+                        int64_t nnzb, int mem) {
+  TRY(check_level(c, level));
+  DeviceGuard dg(c->device);
+  Level &L = c->lv[level];
+  const int bs = c->bs(), V = bs * bs;
+  if (nnzb < 0) return fail(MG_ERR_DIMENSION, "nnzb < 0");
+  std::vector<int64_t> rp, cl;
+  std::vector<double> v;
+  TRY(fetch(rp, row_ptr, size_t(L.n + 1), mem));
+  if (rp[L.n] != nnzb) return fail(MG_ERR_DIMENSION, "row_ptr[n] = %lld != nnzb = %lld", (long long)rp[L.n], (long long)nnzb);
+  TRY(fetch(cl, col, size_t(nnzb), mem));
+  TRY(fetch(v, vals, size_t(nnzb) * V, mem));
+  const int st = mgi_validate_csr(L.n, L.n_global, rp.data(), cl.data(), v.data(), V, 1);
+  if (st == MG_ERR_NONFINITE) return fail(MG_ERR_NONFINITE, "level %d: non-finite matrix value", level);
+  if (st) return fail(MG_ERR_STRUCTURE, "level %d: invalid BSR structure (row_ptr/cols/diagonal)", level);
+  TRY(build_sell(L.A, L.n, rp.data(), cl.data(), v.data(), V));
+  L.nnzb = nnzb;
+  L.diag_host.assign(size_t(L.n) * V, 0.0);
+  for (int64_t i = 0; i < L.n; ++i)
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
+      if (cl[k] == i) std::memcpy(&L.diag_host[size_t(i) * V], &v[size_t(k) * V], V * sizeof(double));
+  L.dinv_ready = false;  // (re)built at finalize; a user D^-1 is re-sliced with the new permutation
+  if (level == 0) {
+    L.rp0.swap(rp);
+    L.col0.swap(cl);
+    L.val0.swap(v);
+    c->cN = 0;
+  }
+  c->invalidate();
+  return MG_OK;
+}
+
+mg_status mg_set_transfer(mg_ctx c, int fine_level, const int64_t *row_ptr, const int64_t *col, const double *w,
+                          int64_t nnz, int weights_per_entry, int mem) {
+  TRY(check_level(c, fine_level));
+  if (fine_level < 1) return fail(MG_ERR_INVALID_ARG, "fine_level must be >= 1");
+  if (!c->lv[fine_level - 1].declared) return fail(MG_ERR_STATE, "level %d not created", fine_level - 1);
+  DeviceGuard dg(c->device);
+  Level &L = c->lv[fine_level];
+  const int64_t nc = c->lv[fine_level - 1].n;
+  const int wpe = weights_per_entry;
+  if (wpe != 1 && wpe != c->bs()) return fail(MG_ERR_INVALID_ARG, "weights_per_entry must be 1 or bs");
+  std::vector<int64_t> rp, cl;
+  std::vector<double> v;
+  TRY(fetch(rp, row_ptr, size_t(L.n + 1), mem));
+  if (rp[L.n] != nnz) return fail(MG_ERR_DIMENSION, "row_ptr[n] != nnz");
+  TRY(fetch(cl, col, size_t(nnz), mem));
+  TRY(fetch(v, w, size_t(nnz) * wpe, mem));
+  const int st = mgi_validate_csr(L.n, nc, rp.data(), cl.data(), v.data(), wpe, 0);
+  if (st == MG_ERR_NONFINITE) return fail(MG_ERR_NONFINITE, "transfer %d: non-finite weight", fine_level);
+  if (st) return fail(MG_ERR_STRUCTURE, "transfer %d: invalid CSR structure", fine_level);
+  TRY(build_sell(L.P, L.n, rp.data(), cl.data(), v.data(), wpe));
+  std::vector<int64_t> rrp(nc + 1), rcl(nnz);
+  std::vector<double> rv(size_t(nnz) * wpe);
+  mgi_csr_transpose(L.n, nc, rp.data(), cl.data(), v.data(), wpe, rrp.data(), rcl.data(), rv.data());
+  TRY(build_sell(L.R, nc, rrp.data(), rcl.data(), rv.data(), wpe));
+  L.wpe = wpe;
+  L.nnz_p = nnz;
+  c->invalidate();
+  return MG_OK;
+}
+
+mg_status mg_set_smoother(mg_ctx c, int level, double omega, int nu_pre, int nu_post, const double *dinv, int mem) {
+  TRY(check_level(c, level));
+  DeviceGuard dg(c->device);
+  Level &L = c->lv[level];
+  if (!std::isfinite(omega)) return fail(MG_ERR_INVALID_ARG, "omega not finite");
+  L.omega = omega > 0.0 ? omega : 0.0;
+  if (nu_pre >= 0) L.nu_pre = nu_pre;
+  if (nu_post >= 0) L.nu_post = nu_post;
+  if (dinv) {
+    const int V = c->bs() * c->bs();
+    TRY(fetch(L.dinv_host, dinv, size_t(L.n) * V, mem));
+    for (double d : L.dinv_host)
+      if (!std::isfinite(d)) return fail(MG_ERR_NONFINITE, "non-finite D^-1");
+    L.dinv_ready = false;
+  }
+  c->invalidate();
+  return MG_OK;
+}
+
+mg_status mg_set_constraints(mg_ctx c, const int64_t *H_row_ptr, const int64_t *H_col, const double *H_w, int64_t nnz,
+                             int mem) {
+  TRY(check_ctx(c));
+  TRY(check_level(c, c->L()));
+  DeviceGuard dg(c->device);
+  const int64_t n = c->lv[c->L()].n;
+  std::vector<int64_t> rp, cl;
+  std::vector<double> v;
+  TRY(fetch(rp, H_row_ptr, size_t(n + 1), mem));
+  if (rp[n] != nnz) return fail(MG_ERR_DIMENSION, "H row_ptr[n] != nnz");
+  TRY(fetch(cl, H_col, size_t(nnz), mem));
+  TRY(fetch(v, H_w, size_t(nnz), mem));
+  const int st = mgi_validate_csr(n, n, rp.data(), cl.data(), v.data(), 1, 0);
+  if (st == MG_ERR_NONFINITE) return fail(MG_ERR_NONFINITE, "H: non-finite weight");
+  if (st) return fail(MG_ERR_STRUCTURE, "H: invalid CSR structure");
+  TRY(build_sell(c->H, n, rp.data(), cl.data(), v.data(), 1));
+  return MG_OK;
+}
+
+mg_status mg_setup(mg_ctx c) {
+  TRY(check_ctx(c));
+  DeviceGuard dg(c->device);
+  return finalize(c);
+}
+
+mg_status mg_vcycle(mg_ctx c, double *x, const double *b) {
+  TRY(check_ctx(c));
+  if (!x || !b || x == b) return fail(MG_ERR_INVALID_ARG, "x, b must be distinct non-NULL device pointers");
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  TRY(finalize(c));
+  return run_vcycle(c, x, b, false);
+}
+
+mg_status mg_vcycle_zero(mg_ctx c, double *z, const double *v) {
+  TRY(check_ctx(c));
+  if (!z || !v || z == v) return fail(MG_ERR_INVALID_ARG, "z, v must be distinct non-NULL device pointers");
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  TRY(finalize(c));
+  return run_vcycle(c, z, v, true);
+}
+
+mg_status mg_spmv(mg_ctx c, int level, double alpha, const double *x, double beta, double *y) {
+  TRY(check_level(c, level));
+  if (!x || !y || x == y) return fail(MG_ERR_INVALID_ARG, "x, y must be distinct non-NULL device pointers");
+  if (!c->lv[level].A.set) return fail(MG_ERR_STATE, "level %d has no matrix", level);
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  return launch_apply<mgk::OP_SPMV>(c->bs(), c->lv[level].A, x, nullptr, nullptr, y, alpha, beta, c->stream);
+}
+
+mg_status mg_sweep(mg_ctx c, int level, const double *x, const double *b, double *x_out) {
+  TRY(check_level(c, level));
+  if (!x || !b || !x_out || x_out == x || x_out == b) return fail(MG_ERR_INVALID_ARG, "x_out must not alias x or b");
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  TRY(finalize(c));
+  Level &L = c->lv[level];
+  return launch_apply<mgk::OP_SWEEP>(c->bs(), L.A, x, b, L.dinv.p, x_out, lv_omega(c, L), 0.0, c->stream);
+}
+
+mg_status mg_residual(mg_ctx c, int level, const double *x, const double *b, double *r) {
+  TRY(check_level(c, level));
+  if (!x || !b || !r || r == x || r == b) return fail(MG_ERR_INVALID_ARG, "r must not alias x or b");
+  if (!c->lv[level].A.set) return fail(MG_ERR_STATE, "level %d has no matrix", level);
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  return launch_apply<mgk::OP_RESID>(c->bs(), c->lv[level].A, x, b, nullptr, r, 1.0, 0.0, c->stream);
+}
+
+mg_status mg_smooth(mg_ctx c, int level, double *x, const double *b, int sweeps) {
+  TRY(check_level(c, level));
+  if (!x || !b || x == b) return fail(MG_ERR_INVALID_ARG, "x, b must be distinct non-NULL device pointers");
+  if (sweeps < 0) return fail(MG_ERR_INVALID_ARG, "sweeps < 0");
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  TRY(finalize(c));
+  return smooth(c, level, x, b, sweeps, false);
+}
+
+mg_status mg_restrict(mg_ctx c, int fine_level, const double *r_fine, double *d_coarse) {
+  TRY(check_level(c, fine_level));
+  if (fine_level < 1 || !c->lv[fine_level].P.set) return fail(MG_ERR_STATE, "no transfer into level %d", fine_level);
+  if (!r_fine || !d_coarse) return fail(MG_ERR_INVALID_ARG, "NULL vector");
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  return launch_transfer(c->bs(), false, c->lv[fine_level].R, r_fine, d_coarse, c->stream);
+}
+
+mg_status mg_prolong_add(mg_ctx c, int fine_level, const double *y_coarse, double *x_fine) {
+  TRY(check_level(c, fine_level));
+  if (fine_level < 1 || !c->lv[fine_level].P.set) return fail(MG_ERR_STATE, "no transfer into level %d", fine_level);
+  if (!y_coarse || !x_fine) return fail(MG_ERR_INVALID_ARG, "NULL vector");
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  return launch_transfer(c->bs(), true, c->lv[fine_level].P, y_coarse, x_fine, c->stream);
+}
+
+mg_status mg_coarse_solve(mg_ctx c, const double *d, double *y) {
+  TRY(check_ctx(c));
+  if (!d || !y || d == y) return fail(MG_ERR_INVALID_ARG, "d, y must be distinct non-NULL device pointers");
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  TRY(finalize(c));
+  return coarse_solve(c, d, y);
+}
+
+mg_status mg_apply_constraints(mg_ctx c, double *x) {
+  TRY(check_ctx(c));
+  if (!x) return fail(MG_ERR_INVALID_ARG, "NULL vector");
+  if (!c->H.set) return fail(MG_ERR_STATE, "no hanging-node matrix (mg_set_constraints)");
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  TRY(finalize(c));
+  Level &F = c->lv[c->L()];
+  TRY(launch_transfer(c->bs(), false, c->H, x, F.w.p, c->stream));
+  CU(cudaMemcpyAsync(x, F.w.p, size_t(F.n) * c->bs() * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  return MG_OK;
+}
+
+mg_status mg_dot(mg_ctx c, int level, const double *a, const double *b, double *out_host) {
+  TRY(check_level(c, level));
+  if (!a || !b || !out_host) return fail(MG_ERR_INVALID_ARG, "NULL argument");
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  TRY(finalize(c));
+  TRY(dev_dot(c, c->lv[level].n * c->bs(), a, b, c->scal.p, false));
+  CU(cudaMemcpyAsync(out_host, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return MG_OK;
+}
+
+int64_t mgi_launch_count(mgi_ctx c) { return c ? c->launches : -1; }
+
+int mgi_level_info(mgi_ctx c, int level, int64_t *n, int64_t *nnzb, int64_t *sell_entries, int64_t *nnz_p,
+                   int64_t *sell_entries_p, int64_t *sell_entries_r) {
+  if (!c || level < 0 || level > c->L()) return MG_ERR_INVALID_ARG;
+  const Level &L = c->lv[level];
+  if (n) *n = L.n;
+  if (nnzb) *nnzb = L.nnzb;
+  if (sell_entries) *sell_entries = L.A.n_entries;
+  if (nnz_p) *nnz_p = L.nnz_p;
+  if (sell_entries_p) *sell_entries_p = L.P.n_entries;
+  if (sell_entries_r) *sell_entries_r = L.R.n_entries;
+  return 0;
+}
+
+mg_status mg_get_unique_id(unsigned char out[128]) {
+  if (!out) return fail(MG_ERR_INVALID_ARG, "NULL argument");
+  return fail(MG_ERR_NCCL, "multi-GPU support is not built into this library");
+}
+
+mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *opts, mg_solve_info *info) {
+  TRY(check_ctx(c));
+  if (!x || !b || !opts || x == b) return fail(MG_ERR_INVALID_ARG, "bad arguments");
+  if (opts->max_iter < 0 || !(opts->rtol >= 0.0)) return fail(MG_ERR_INVALID_ARG, "bad options");
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  TRY(finalize(c));
+  Level &F = c->lv[c->L()];
+  const int bs = c->bs();
+  const int64_t N = F.n * bs;
+  const double rtol = opts->rtol;
+  int its = 0;
+  double rel = 0.0;
+  bool conv = false;
+  double *hst = nullptr;
+  if (!c->gm_host) CU(cudaMallocHost(&c->gm_host, 16 * sizeof(double)));
+  hst = c->gm_host;
+
+  if (opts->method == MG_RICHARDSON) {
+    TRY(launch_apply<mgk::OP_RESID>(bs, F.A, x, b, nullptr, F.w.p, 1.0, 0.0, c->stream));
+    TRY(dev_dot(c, N, F.w.p, F.w.p, c->scal.p, true));
+    CU(cudaMemcpyAsync(hst, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    const double r0 = hst[0];
+    if (!std::isfinite(r0)) return fail(MG_ERR_NONFINITE, "non-finite initial residual");
+    if (r0 == 0.0) conv = true;
+    while (!conv && its < opts->max_iter) {
+      TRY(run_vcycle(c, x, b, false));
+      ++its;
+      TRY(launch_apply<mgk::OP_RESID>(bs, F.A, x, b, nullptr, F.w.p, 1.0, 0.0, c->stream));
+      TRY(dev_dot(c, N, F.w.p, F.w.p, c->scal.p, true));
+      CU(cudaMemcpyAsync(hst, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      if (!std::isfinite(hst[0])) return fail(MG_ERR_NONFINITE, "non-finite residual at iteration %d", its);
+      rel = hst[0] / r0;
+      if (hst[0] <= rtol * r0) conv = true;
+    }
+  } else if (opts->method == MG_GMRES) {
+    const int m = std::max(1, std::min(opts->restart > 0 ? opts->restart : 30, 64));
+    TRY(ensure_gmres(c, m));
+    mgk::GmresDev g = c->gm;
+    double *V = c->gm_V.p, *Z = c->gm_Z.p;
+    TRY(launch_apply<mgk::OP_RESID>(bs, F.A, x, b, nullptr, V, 1.0, 0.0, c->stream));
+    TRY(dev_dot(c, N, V, V, g.beta0, true));
+    CU(cudaMemcpyAsync(g.beta, g.beta0, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaMemcpyAsync(hst, g.beta0, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    const double beta0 = hst[0];
+    if (!std::isfinite(beta0)) return fail(MG_ERR_NONFINITE, "non-finite initial residual");
+    if (beta0 == 0.0) conv = true;
+    const unsigned eg = unsigned(std::min<int64_t>((N + 255) / 256, 8 * c->n_sm));
+    while (!conv && its < opts->max_iter) {
+      const int mm = std::min(m, opts->max_iter - its);
+      ++g_tally, mgk::k_gmres_start<<<1, 32, 0, c->stream>>>(g);
+      ++g_tally, mgk::k_scale_div<<<eg, 256, 0, c->stream>>>(N, V, g.beta, V);
+      TRY(check_launch());
+      int k = 0;
+      bool done = false;
+      for (int j = 0; j < mm; ++j) {
+        double *vj = V + size_t(j) * N, *zj = Z + size_t(j) * N, *w = V + size_t(j + 1) * N;
+        TRY(run_vcycle(c, zj, vj, true));  // z_j = GMG(L, 0, v_j)
+        ++its;
+        TRY(launch_apply<mgk::OP_SPMV>(bs, F.A, zj, nullptr, nullptr, w, 1.0, 0.0, c->stream));  // w = A z_j
+        double *hcol = g.H + size_t(j) * (g.m + 1);  // leading dimension of the allocated state
+        TRY(dev_dot(c, N, w, V, hcol + 0, false));  // h_0j = (w, v_0)
+        for (int i = 0; i < j; ++i)                 // w -= h_ij v_i ; h_{i+1,j} = (w, v_{i+1})
+          TRY(dev_axpy_dot(c, N, w, V + size_t(i) * N, hcol + i, V + size_t(i + 1) * N, hcol + i + 1));
+        TRY(dev_axpy_dot(c, N, w, vj, hcol + j, nullptr, hcol + j + 1));  // w -= h_jj v_j ; h_{j+1,j} = ||w||
+        ++g_tally, mgk::k_givens<<<1, 32, 0, c->stream>>>(g, j, rtol);
+        ++g_tally, mgk::k_scale_div<<<eg, 256, 0, c->stream>>>(N, w, g.hn + j, w);  // v_{j+1} = w / h_{j+1,j}
+        TRY(check_launch());
+        CU(cudaMemcpyAsync(hst, g.out, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        k = j + 1;
+        if (!std::isfinite(hst[0])) return fail(MG_ERR_NONFINITE, "non-finite GMRES residual estimate");
+        if (hst[1] != 0.0) {
+          done = true;
+          break;
+        }
+      }
+      ++g_tally, mgk::k_backsolve<<<1, 32, 0, c->stream>>>(g, k);
+      ++g_tally, mgk::k_update_x<<<eg, 256, 0, c->stream>>>(N, k, g.y, Z, x);
+      TRY(check_launch());
+      TRY(launch_apply<mgk::OP_RESID>(bs, F.A, x, b, nullptr, V, 1.0, 0.0, c->stream));
+      TRY(dev_dot(c, N, V, V, g.beta, true));
+      CU(cudaMemcpyAsync(hst, g.beta, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      rel = hst[0] / beta0;
+      if (!std::isfinite(rel)) return fail(MG_ERR_NONFINITE, "non-finite residual");
+      if (done || hst[0] <= rtol * beta0) {
+        conv = true;
+        break;
+      }
+    }
+  } else {
+    return fail(MG_ERR_INVALID_ARG, "unknown method %d", opts->method);
+  }
+  if (info) {
+    info->iterations = its;
+    info->rel_residual = rel;
+    info->converged = conv ? 1 : 0;
+  }
+  return conv ? MG_OK : MG_NOT_CONVERGED;
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+"""Convenience wrapper owning one mg_ctx (argument marshalling only; every
+operation is a call into libmgb200.so)."""
+from __future__ import annotations
+
+from . import (MG_COARSE_DIRECT, MG_GMRES, mg_apply_constraints, mg_create, mg_create_level, mg_destroy,
+               mg_set_constraints, mg_set_matrix, mg_set_smoother, mg_set_transfer, mg_setup, mg_solve,
+               mg_vcycle, mg_vcycle_zero)
+
+
+class Multigrid:
+    """levels: coarse -> fine sequence of objects with attributes
+    n, row_ptr, col, val (BSR, val shaped (nnzb, bs, bs) or flat), and for
+    l >= 1 P = (row_ptr, col, w) (n_l x n_{l-1}) and wpe.  H (optional):
+    (row_ptr, col, w) hanging matrix of the finest level."""
+
+    def __init__(self, levels, bs, *, omega=0.8, nu_pre=2, nu_post=2, coarse_mode=MG_COARSE_DIRECT,
+                 coarse_sweeps=20, use_graphs=True, device=0, stream=None, H=None, omegas=None):
+        self.bs = bs
+        self.n = [int(L.n) for L in levels]
+        self.ctx = mg_create(len(levels), bs, nu_pre=nu_pre, nu_post=nu_post, omega=omega,
+                             coarse_mode=coarse_mode, coarse_sweeps=coarse_sweeps, use_graphs=use_graphs,
+                             device=device, stream=stream)
+        try:
+            for l, L in enumerate(levels):
+                mg_create_level(self.ctx, l, int(L.n))
+            for l, L in enumerate(levels):
+                val = L.val.reshape(-1) if hasattr(L.val, "reshape") else L.val
+                mg_set_matrix(self.ctx, l, L.row_ptr, L.col, val)
+                if l > 0:
+                    rp, col, w = L.P
+                    mg_set_transfer(self.ctx, l, rp, col, w, getattr(L, "wpe", 1))
+                if omegas is not None:
+                    mg_set_smoother(self.ctx, l, omegas[l])
+            if H is not None:
+                mg_set_constraints(self.ctx, *H)
+            mg_setup(self.ctx)
+        except Exception:
+            mg_destroy(self.ctx)
+            self.ctx = None
+            raise
+
+    @property
+    def n_dof(self) -> int:
+        return self.n[-1] * self.bs
+
+    def vcycle(self, x, b):
+        mg_vcycle(self.ctx, x, b)
+
+    def precondition(self, z, v):
+        mg_vcycle_zero(self.ctx, z, v)
+
+    def solve(self, x, b, method=MG_GMRES, restart=30, max_iter=200, rtol=1e-10):
+        return mg_solve(self.ctx, x, b, method=method, restart=restart, max_iter=max_iter, rtol=rtol)
+
+    def apply_constraints(self, x):
+        mg_apply_constraints(self.ctx, x)
+
+    def close(self):
+        if self.ctx is not None:
+            mg_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,148 @@
+"""GPU parity at BASELINE.json's full sizes, in bench.py's launch
+configuration (graph-captured V-cycles, SELL-32-4096 operators, C2 and C3):
+sampled rows against the oracle computed row by row on the same inputs, and
+properties that hold at any size (exact scaling by 2, determinism, residual
+contraction, GMRES convergence; iteration parity +-1 on C2)."""
+import functools
+
+import numpy as np
+import pytest
+
+from gpu_util import TOL_OP, build_gpu, dev, host
+
+import oracle
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@functools.lru_cache(maxsize=None)
+def full(name):
+    from problems import configs
+    P = configs.build(name, keep_geometry=False)
+    mg = build_gpu(P.levels, P.bs, omega=P.omega, H=P.fine.H)
+    return P, mg
+
+
+def sample_rows(n, k=3000, seed=0):
+    g = np.random.default_rng(seed)
+    rows = np.unique(np.concatenate([g.integers(0, n, size=k), np.arange(min(n, 64)),
+                                     np.arange(max(0, n - 4200), n)]))   # ragged last window + slice tail
+    return rows
+
+
+def sub_csr(rp, col, val, rows, vpe):
+    """Row subset of a CSR/BSR matrix (input slicing only)."""
+    cnt = rp[rows + 1] - rp[rows]
+    srp = np.zeros(len(rows) + 1, np.int64)
+    srp[1:] = np.cumsum(cnt)
+    idx = np.concatenate([np.arange(rp[r], rp[r + 1]) for r in rows]) if len(rows) else np.zeros(0, np.int64)
+    v = val.reshape(len(col), -1)[idx] if vpe else None
+    return srp, col[idx], v
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_fullsize_residual_sweep_sampled(name):
+    import paper_2405_05047_b200 as m
+    P, mg = full(name)
+    bs = P.bs
+    Lf = len(P.levels) - 1
+    for l in (Lf, Lf - 1):
+        L = P.levels[l]
+        g = np.random.default_rng(100 + l)
+        x = g.standard_normal(L.n * bs)
+        b = g.standard_normal(L.n * bs)
+        r = dev(np.zeros(L.n * bs))
+        m.mg_residual(mg.ctx, l, dev(x), dev(b), r)
+        xo = dev(np.zeros(L.n * bs))
+        m.mg_sweep(mg.ctx, l, dev(x), dev(b), xo)
+        rows = sample_rows(L.n, seed=l)
+        srp, scol, sval = sub_csr(L.row_ptr, L.col, L.val, rows, bs * bs)
+        sval = sval.reshape(-1, bs, bs)
+        bsub = b.reshape(-1, bs)[rows].reshape(-1)
+        exp = oracle.residual(len(rows), bs, srp, scol, sval, x, bsub)
+        sc = oracle.spmv(len(rows), bs, srp, scol, np.abs(sval), np.abs(x)) + np.abs(bsub)
+        got = host(r).reshape(-1, bs)[rows].reshape(-1)
+        assert np.max(np.abs(got - exp)) <= TOL_OP * np.max(sc), f"{name} residual level {l}"
+        # sweep: x + omega D^-1 t on the same rows
+        dinv = oracle.block_diag_inverse(L.n, bs, L.row_ptr, L.col, L.val)[rows]
+        t = exp.reshape(-1, bs)
+        e_sw = x.reshape(-1, bs)[rows] + P.omega * np.einsum("nij,nj->ni", dinv, t)
+        sc_sw = np.abs(x.reshape(-1, bs)[rows]) + P.omega * np.einsum("nij,nj->ni", np.abs(dinv),
+                                                                        sc.reshape(-1, bs))
+        got = host(xo).reshape(-1, bs)[rows]
+        assert np.max(np.abs(got - e_sw)) <= 10 * TOL_OP * np.max(sc_sw), f"{name} sweep level {l}"
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_fullsize_transfers_sampled(name):
+    import paper_2405_05047_b200 as m
+    P, mg = full(name)
+    bs = P.bs
+    Lf = len(P.levels) - 1
+    L, C = P.levels[Lf], P.levels[Lf - 1]
+    g = np.random.default_rng(7)
+    r = g.standard_normal(L.n * bs)
+    d = dev(np.full(C.n * bs, np.nan))
+    m.mg_restrict(mg.ctx, Lf, dev(r), d)
+    prp, pcol, pw = L.P
+    rrp, rcol, rw = oracle.csr_transpose(L.n, C.n, prp, pcol, pw)
+    rows = sample_rows(C.n, seed=3)
+    srp, scol, sw = sub_csr(rrp, rcol, rw, rows, 1)
+    exp = oracle.transfer(len(rows), bs, srp, scol, sw.reshape(-1), 1, r)
+    got = host(d).reshape(-1, bs)[rows].reshape(-1)
+    sc = oracle.transfer(len(rows), bs, srp, scol, np.abs(sw.reshape(-1)), 1, np.abs(r))
+    assert np.max(np.abs(got - exp)) <= TOL_OP * np.max(sc)
+    y = g.standard_normal(C.n * bs)
+    x0 = g.standard_normal(L.n * bs)
+    x = dev(x0)
+    m.mg_prolong_add(mg.ctx, Lf, dev(y), x)
+    rows = sample_rows(L.n, seed=4)
+    srp, scol, sw = sub_csr(prp, pcol, pw, rows, 1)
+    exp = oracle.transfer(len(rows), bs, srp, scol, sw.reshape(-1), 1, y, x0.reshape(-1, bs)[rows].reshape(-1))
+    got = host(x).reshape(-1, bs)[rows].reshape(-1)
+    assert np.max(np.abs(got - exp)) <= TOL_OP * (np.max(np.abs(x0)) + np.max(np.abs(y)))
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_fullsize_vcycle_properties(name):
+    import paper_2405_05047_b200 as m
+    P, mg = full(name)
+    b = dev(P.b)
+    z1 = dev(np.zeros(P.n_dof))
+    z2 = dev(np.zeros(P.n_dof))
+    z3 = dev(np.zeros(P.n_dof))
+    m.mg_vcycle_zero(mg.ctx, z1, b)
+    m.mg_vcycle_zero(mg.ctx, z3, b)
+    b2 = b * 2.0
+    m.mg_vcycle_zero(mg.ctx, z2, b2)
+    h1, h2, h3 = host(z1), host(z2), host(z3)
+    assert np.array_equal(h1, h3)                       # deterministic (no atomics)
+    assert np.array_equal(2.0 * h1, h2)                 # linear in b, exactly (power-of-two scaling)
+    r = dev(np.zeros(P.n_dof))
+    m.mg_residual(mg.ctx, len(P.levels) - 1, z1, b, r)
+    rn = np.sqrt(m.mg_dot(mg.ctx, len(P.levels) - 1, r, r))
+    bn = np.linalg.norm(P.b)
+    assert rn < 0.75 * bn                               # one V-cycle contracts (C3 rho ~ 0.5, C2 ~ 0.15)
+
+
+def test_fullsize_gmres_c3_converges():
+    import paper_2405_05047_b200 as m
+    P, mg = full("c3")
+    x = dev(np.zeros(P.n_dof))
+    st, its, rel, conv = m.mg_solve(mg.ctx, x, dev(P.b), rtol=1e-10)
+    assert conv and rel <= 2e-10 and its <= 40
+    r = dev(np.zeros(P.n_dof))
+    m.mg_residual(mg.ctx, len(P.levels) - 1, x, dev(P.b), r)
+    rn = np.sqrt(m.mg_dot(mg.ctx, len(P.levels) - 1, r, r))
+    assert rn <= 2e-10 * np.linalg.norm(P.b)
+
+
+def test_fullsize_gmres_c2_iterations_match_oracle():
+    import paper_2405_05047_b200 as m
+    P, mg = full("c2")
+    x = dev(np.zeros(P.n_dof))
+    st, its, rel, conv = m.mg_solve(mg.ctx, x, dev(P.b), rtol=1e-10)
+    h = oracle.MgHierarchy.from_arrays(P.levels, omega=P.omega)
+    xe, ite, _, rele = oracle.gmres(h, P.b, rtol=1e-10)
+    assert conv and abs(its - ite) <= 1, (its, ite)
+    assert np.linalg.norm(host(x) - xe) <= 1e-8 * np.linalg.norm(xe)
