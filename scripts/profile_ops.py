@@ -1,0 +1,59 @@
+"""Profiling driver for ncu (run under `ncu --profile-from-start off`).
+
+mode step:    one bench step (GMRES+MG solve from 0 + x <- Hx) inside the
+              profiler range -> the launch list of a step.
+mode kernels: the fine-level kernels once each (fused sweep, residual, SpMV,
+              restriction, prolongation, A-free first sweep via a V-cycle
+              from zero) -> `--set full` captures.
+"""
+import argparse
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import paper_2405_05047_b200 as m  # noqa: E402
+from problems import configs  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("mode", choices=["step", "kernels"])
+ap.add_argument("--config", default="c3")
+a = ap.parse_args()
+
+t = time.time()
+P = configs.build(a.config, keep_geometry=False)
+print(f"gen {a.config} {P.n_dof} DOFs {time.time() - t:.1f}s", file=sys.stderr, flush=True)
+S = m.Multigrid(P.levels, P.bs, omega=P.omega, H=P.fine.H)
+ctx = S.ctx
+Lf = len(P.levels) - 1
+b = torch.from_numpy(P.b).cuda()
+x = torch.zeros_like(b)
+for _ in range(3):
+    x.zero_()
+    S.solve(x, b)
+torch.cuda.synchronize()
+if a.mode == "step":
+    torch.cuda.profiler.start()
+    x.zero_()
+    st, its, rel, conv = S.solve(x, b)
+    S.apply_constraints(x)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+    print(f"step: {its} iterations, rel {rel:.2e}", file=sys.stderr)
+else:
+    xin = torch.randn_like(b)
+    out = torch.empty_like(b)
+    nc = P.levels[Lf - 1].n * P.bs
+    d = torch.empty(nc, dtype=torch.float64, device="cuda")
+    m.mg_sweep(ctx, Lf, xin, b, out)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    m.mg_sweep(ctx, Lf, xin, b, out)            # k_sell_apply<3,2,1>
+    m.mg_residual(ctx, Lf, xin, b, out)         # k_sell_apply<3,1,1>
+    m.mg_spmv(ctx, Lf, 1.0, xin, 0.0, out)      # k_sell_apply<3,0,1>
+    m.mg_restrict(ctx, Lf, out, d)              # k_transfer<3,1,0,1>
+    m.mg_prolong_add(ctx, Lf, d, out)           # k_transfer<3,1,1,1>
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
