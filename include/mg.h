@@ -76,6 +76,7 @@ typedef enum {
 } mg_status;
 
 enum { MG_MEM_HOST = 0, MG_MEM_DEVICE = 1 };
+enum { MG_TRANSPORT_NCCL = 0, MG_TRANSPORT_LOCAL = 1 };
 enum { MG_COARSE_DIRECT = 0, MG_COARSE_SMOOTH = 1 };
 enum { MG_GMRES = 0, MG_RICHARDSON = 1 };
 
@@ -96,12 +97,22 @@ typedef struct {
   int use_graphs;
 } mg_config;
 
-/* Multi-GPU communicator description: NULL => single GPU.  All ranks pass the
- * same 128-byte NCCL unique id (made by mg_get_unique_id on rank 0 and
- * broadcast by the caller, e.g. via torch.distributed). */
+/* Multi-GPU communicator description: NULL (or nranks == 1) => single GPU.
+ * Row-partitioned solve, one rank per GPU (the paper is
+ * single-GPU and names multi-GPU as future work).
+ * transport = MG_TRANSPORT_NCCL: one process per GPU; all ranks pass the same
+ *   128-byte NCCL unique id (mg_get_unique_id on rank 0, broadcast by the
+ *   caller, e.g. via torch.distributed).  Halos: grouped ncclSend/ncclRecv;
+ *   dots: ncclAllReduce; agglomeration: all-gather.
+ * transport = MG_TRANSPORT_LOCAL: all ranks are host threads of ONE process
+ *   sharing one device (a test transport: the full distributed algorithm on a
+ *   single GPU); nccl_id is any 128-byte group key shared by the ranks.
+ * With nranks > 1 every mg_* call below is collective: all ranks call it, in
+ * the same order, with their own rows. */
 typedef struct {
   int nranks;
   int rank;
+  int transport;
   unsigned char nccl_id[128];
 } mg_comm;
 
@@ -132,7 +143,8 @@ typedef struct {
 /* Context and levels                                                          */
 /* -------------------------------------------------------------------------- */
 
-/* NCCL unique id for a multi-GPU context (call on one rank only). */
+/* NCCL unique id for a multi-GPU context (call on one rank only).
+ * MG_ERR_NCCL if libnccl.so.2 cannot be loaded. */
 mg_status mg_get_unique_id(unsigned char out[128]);
 
 /* Create a context on CUDA device `device`, ordering work on `cuda_stream`
@@ -142,13 +154,21 @@ mg_status mg_create(mg_ctx *out, const mg_config *cfg, int device, void *cuda_st
                     const mg_comm *comm);
 
 /* Declare level `level` with n_rows_global block rows, of which this rank owns
- * rows [row_begin, row_end).  Single GPU: row_begin = 0, row_end = n_rows_global. */
+ * rows [row_begin, row_end).  Single GPU: row_begin = 0, row_end = n_rows_global.
+ * Multi-GPU: either the ranks' ranges tile [0, n_rows_global) in rank order
+ * (a DISTRIBUTED level) or every rank passes [0, n_rows_global) (a
+ * REPLICATED level, computed redundantly on every rank).  Levels below a
+ * replicated level must be replicated; the restricted residual entering the
+ * first replicated level is all-gathered (agglomeration).  With the direct
+ * coarse solve, level 0 must be replicated. */
 mg_status mg_create_level(mg_ctx ctx, int level, int64_t n_rows_global, int64_t row_begin,
                           int64_t row_end);
 
 /* Set the (condensed, constrained) system matrix A_l of level `level` as BSR
  * (see layout above).  Rows are this rank's owned rows; columns are GLOBAL
- * block indices.  Every row must contain its diagonal block.  The matrix is
+ * block indices.  Every row must contain its diagonal block (global column
+ * row_begin + i for local row i).  Multi-GPU: the library renumbers columns
+ * into owned + ghost and builds the halo plan itself.  The matrix is
  * copied to the device once and is immutable afterwards; calling
  * again replaces it (the Newton re-upload of P:821). */
 mg_status mg_set_matrix(mg_ctx ctx, int level, const int64_t *row_ptr, const int64_t *col,

@@ -17,10 +17,10 @@ extern "C" {
 
 /* Validate a BSR / CSR matrix: row_ptr[0] == 0, non-decreasing, row_ptr[n] ==
  * nnz; columns strictly increasing within a row and in [0, n_cols); values
- * (nnz * vpe) finite; if need_diag, every row i < n_cols holds column i.
+ * (nnz * vpe) finite; if need_diag, every row i holds column diag_offset + i.
  * Returns 0, MG_ERR_STRUCTURE (-3) or MG_ERR_NONFINITE (-4). */
 int mgi_validate_csr(int64_t n, int64_t n_cols, const int64_t *row_ptr, const int64_t *col,
-                     const double *val, int64_t vpe, int need_diag);
+                     const double *val, int64_t vpe, int need_diag, int64_t diag_offset);
 
 /* Sliced-ELL layout ("SELL-32-sigma") used on the device for every sparse
  * operator: rows are sorted by length
@@ -66,20 +66,30 @@ int mgi_dense_inverse(int64_t N, double *a, double *inv);
 int mgi_bsr_to_dense(int64_t n, int bs, const int64_t *row_ptr, const int64_t *col,
                      const double *val, double *dense);
 
-/* Multi-GPU row-partition plan: given this rank's owned rows
- * [row_begin, row_end) of a level and the GLOBAL block columns of its local
- * matrix (CSR, n_local rows), produce
- *   - local_col[nnz]: columns renumbered to [0, n_local) for owned columns,
- *     n_local + g for the g-th ghost (ghosts sorted by global index);
+/* Multi-GPU row-partition plan: given the GLOBAL columns of
+ * an n_rows-row local CSR operator whose column space is a level of which this
+ * rank owns rows [col_begin, col_end), produce
+ *   - local_col[nnz]: owned columns renumbered to c - col_begin, the g-th
+ *     ghost (ghosts sorted by global index) to (col_end - col_begin) + g;
  *   - ghosts[*n_ghost] (capacity nnz): global indices of the ghost columns.
  * Returns 0. */
-int mgi_localize_columns(int64_t row_begin, int64_t row_end, const int64_t *row_ptr,
+int mgi_localize_columns(int64_t n_rows, int64_t col_begin, int64_t col_end, const int64_t *row_ptr,
                          const int64_t *col, int64_t *local_col, int64_t *ghosts,
                          int64_t *n_ghost);
 
 /* Owner rank of global row g under contiguous splitters
  * bounds[0..nranks] (bounds[r] <= g < bounds[r+1]). */
 int mgi_owner(int64_t g, const int64_t *bounds, int nranks);
+
+/* Rows of R = P^T owned by this rank, from the P entries every rank routed
+ * to it (multi-GPU restriction setup).  Input: m entries (J = global coarse
+ * row, i = global fine row, w[wpe]) in arrival order (source ranks ascending,
+ * each in its CSR order); output: CSR rows r0 .. r0+nr-1 (out_row_ptr[nr+1]),
+ * out_col = global fine rows, out_w[m*wpe].  Stable counting sort on J, so
+ * each row lists fine rows ascending -- identical to the single-GPU
+ * transpose.  Returns 0 or MG_ERR_STRUCTURE (J outside [r0, r0+nr)). */
+int mgi_assemble_routed_rows(int64_t m, const int64_t *J, const int64_t *i, const double *w, int wpe, int64_t r0,
+                             int64_t nr, int64_t *out_row_ptr, int64_t *out_col, double *out_w);
 
 /* Number of device kernels the context has launched so far (eager launches
  * plus the kernel nodes of every CUDA-graph launch).  Bench accounting. */

@@ -30,6 +30,7 @@ MG_ERR_SINGULAR, MG_ERR_STATE, MG_ERR_CUDA, MG_ERR_NCCL, MG_ERR_OOM = -5, -6, -7
 MG_MEM_HOST, MG_MEM_DEVICE = 0, 1
 MG_COARSE_DIRECT, MG_COARSE_SMOOTH = 0, 1
 MG_GMRES, MG_RICHARDSON = 0, 1
+MG_TRANSPORT_NCCL, MG_TRANSPORT_LOCAL = 0, 1
 
 STATUS_NAMES = {0: "MG_OK", 1: "MG_NOT_CONVERGED", -1: "MG_ERR_INVALID_ARG", -2: "MG_ERR_DIMENSION",
                 -3: "MG_ERR_STRUCTURE", -4: "MG_ERR_NONFINITE", -5: "MG_ERR_SINGULAR", -6: "MG_ERR_STATE",
@@ -43,7 +44,8 @@ class mg_config(ctypes.Structure):
 
 
 class mg_comm(ctypes.Structure):
-    _fields_ = [("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_id", ctypes.c_ubyte * 128)]
+    _fields_ = [("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("transport", ctypes.c_int),
+                ("nccl_id", ctypes.c_ubyte * 128)]
 
 
 class mg_solve_opts(ctypes.Structure):
@@ -170,14 +172,17 @@ def mg_get_unique_id() -> bytes:
 def mg_create(n_levels, block_size, *, nu_pre=2, nu_post=2, omega=0.8, coarse_mode=MG_COARSE_DIRECT,
               coarse_sweeps=20, use_graphs=True, device=0, stream=None, comm=None):
     """Returns an opaque context handle (int).  stream: a torch.cuda.Stream, a
-    raw cudaStream_t int, or None (internal blocking stream)."""
+    raw cudaStream_t int, or None (internal blocking stream).  comm: None
+    (single GPU) or (nranks, rank, id_bytes[, transport])."""
     cfg = mg_config(n_levels, block_size, nu_pre, nu_post, omega, coarse_mode, coarse_sweeps, int(bool(use_graphs)))
     h = _P()
     s = getattr(stream, "cuda_stream", stream)
     cm = None
     if comm is not None:
-        nranks, rank, uid = comm
-        cm = mg_comm(nranks, rank, (ctypes.c_ubyte * 128)(*uid))
+        nranks, rank, uid = comm[:3]
+        transport = comm[3] if len(comm) > 3 else MG_TRANSPORT_NCCL
+        uid = bytes(uid).ljust(128, b"\0")[:128]
+        cm = mg_comm(nranks, rank, transport, (ctypes.c_ubyte * 128)(*uid))
     _check(_lib.mg_create(ctypes.byref(h), ctypes.byref(cfg), device, s, ctypes.byref(cm) if cm else None),
            "mg_create")
     return h.value

@@ -66,7 +66,7 @@ int gj_block(int bs, const double *a_in, double *out) {
 extern "C" {
 
 int mgi_validate_csr(int64_t n, int64_t n_cols, const int64_t *rp, const int64_t *col,
-                     const double *val, int64_t vpe, int need_diag) {
+                     const double *val, int64_t vpe, int need_diag, int64_t diag_offset) {
   if (n < 0 || !rp) return MG_ERR_INVALID_ARG;
   if (rp[0] != 0) return MG_ERR_STRUCTURE;
   int bad = 0, nonfinite = 0;
@@ -78,9 +78,9 @@ int mgi_validate_csr(int64_t n, int64_t n_cols, const int64_t *rp, const int64_t
     for (int64_t k = a; k < b; ++k) {
       const int64_t c = col[k];
       if (c < 0 || c >= n_cols || (k > a && c <= col[k - 1])) bad |= 1;
-      if (c == i) diag = true;
+      if (c == diag_offset + i) diag = true;
     }
-    if (need_diag && i < n_cols && !diag) bad |= 1;
+    if (need_diag && !diag) bad |= 1;
     if (val)
       for (int64_t t = a * vpe; t < b * vpe; ++t)
         if (!std::isfinite(val[t])) nonfinite |= 1;
@@ -241,11 +241,11 @@ int mgi_bsr_to_dense(int64_t n, int bs, const int64_t *rp, const int64_t *col, c
   return 0;
 }
 
-int mgi_localize_columns(int64_t row_begin, int64_t row_end, const int64_t *rp, const int64_t *col,
+int mgi_localize_columns(int64_t n_rows, int64_t row_begin, int64_t row_end, const int64_t *rp, const int64_t *col,
                          int64_t *local_col, int64_t *ghosts, int64_t *n_ghost) {
   const int64_t n = row_end - row_begin;
-  if (n < 0) return MG_ERR_INVALID_ARG;
-  const int64_t nnz = rp[n];
+  if (n < 0 || n_rows < 0) return MG_ERR_INVALID_ARG;
+  const int64_t nnz = rp[n_rows];
   int64_t ng = 0;
   for (int64_t t = 0; t < nnz; ++t)
     if (col[t] < row_begin || col[t] >= row_end) ghosts[ng++] = col[t];
@@ -263,6 +263,23 @@ int mgi_localize_columns(int64_t row_begin, int64_t row_end, const int64_t *rp, 
 
 int mgi_owner(int64_t g, const int64_t *bounds, int nranks) {
   return int(std::upper_bound(bounds, bounds + nranks + 1, g) - bounds) - 1;
+}
+
+int mgi_assemble_routed_rows(int64_t m, const int64_t *J, const int64_t *i, const double *w, int wpe, int64_t r0,
+                             int64_t nr, int64_t *orp, int64_t *ocol, double *ow) {
+  std::fill(orp, orp + nr + 1, int64_t(0));
+  for (int64_t t = 0; t < m; ++t) {
+    if (J[t] < r0 || J[t] >= r0 + nr) return MG_ERR_STRUCTURE;
+    orp[J[t] - r0 + 1]++;
+  }
+  for (int64_t j = 0; j < nr; ++j) orp[j + 1] += orp[j];
+  std::vector<int64_t> next(orp, orp + nr);
+  for (int64_t t = 0; t < m; ++t) {
+    const int64_t d = next[J[t] - r0]++;
+    ocol[d] = i[t];
+    for (int q = 0; q < wpe; ++q) ow[d * wpe + q] = w[t * wpe + q];
+  }
+  return 0;
 }
 
 }  // extern "C"

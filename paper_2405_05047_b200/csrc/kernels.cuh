@@ -69,8 +69,16 @@ __device__ __forceinline__ void load_entry(const double *__restrict__ gval, int 
 // ---------------------------------------------------------------------------
 enum { OP_SPMV = 0, OP_RESID = 1, OP_SWEEP = 2 };
 
-template <int BS, int OP, bool STREAM>
+// HALO: columns >= n_own are ghosts (multi-GPU), read from xg[c - n_own].
+template <int BS, bool HALO>
+__device__ __forceinline__ const double *col_ptr(const double *x, const double *xg, int n_own, int c) {
+  if constexpr (HALO) return c < n_own ? x + int64_t(c) * BS : xg + int64_t(c - n_own) * BS;
+  else return x + int64_t(c) * BS;
+}
+
+template <int BS, int OP, bool STREAM, bool HALO>
 __global__ void __launch_bounds__(kCta) k_sell_apply(Sell A, const double *__restrict__ x,
+                                                     const double *__restrict__ xg, int n_own,
                                                      const double *__restrict__ b,
                                                      const double *__restrict__ dinv,
                                                      double *__restrict__ out, double alpha, double beta) {
@@ -88,7 +96,7 @@ __global__ void __launch_bounds__(kCta) k_sell_apply(Sell A, const double *__res
     const int c = ld_col<STREAM>(A.col + g + lane);
     double v[V];
     load_entry<V, STREAM>(A.val + g * V, lane, v);
-    const double *xc = x + int64_t(c) * BS;
+    const double *xc = col_ptr<BS, HALO>(x, xg, n_own, c);
     double xv[BS];
 #pragma unroll
     for (int q = 0; q < BS; ++q) xv[q] = __ldg(xc + q);
@@ -150,8 +158,9 @@ __global__ void __launch_bounds__(kCta) k_sweep0(int64_t n_slices, const int32_t
 // Transfer y = T x (ACCUM = 0) or y += T x (ACCUM = 1) with scalar weights
 // (WPE = 1) or per-component weights (WPE = BS): restriction R r (P:131,
 // P:337), prolongation x + P y, hanging interpolation H x.
-template <int BS, int WPE, bool ACCUM, bool STREAM>
+template <int BS, int WPE, bool ACCUM, bool STREAM, bool HALO>
 __global__ void __launch_bounds__(kCta) k_transfer(Sell T, const double *__restrict__ in,
+                                                   const double *__restrict__ ing, int n_own,
                                                    double *__restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int64_t s = (int64_t(blockIdx.x) * kCta + threadIdx.x) >> 5;
@@ -166,7 +175,7 @@ __global__ void __launch_bounds__(kCta) k_transfer(Sell T, const double *__restr
     const int c = ld_col<STREAM>(T.col + g + lane);
     double w[WPE];
     load_entry<WPE, STREAM>(T.val + g * WPE, lane, w);
-    const double *xc = in + int64_t(c) * BS;
+    const double *xc = col_ptr<BS, HALO>(in, ing, n_own, c);
 #pragma unroll
     for (int q = 0; q < BS; ++q) acc[q] = fma(w[WPE == 1 ? 0 : q], __ldg(xc + q), acc[q]);
   }
@@ -342,6 +351,25 @@ __global__ void k_update_x(int64_t n, int k, const double *__restrict__ y, const
     double v = x[i];
     for (int t = 0; t < k; ++t) v = fma(ys[t], __ldg(Z + int64_t(t) * n + i), v);
     x[i] = v;
+  }
+}
+
+// Halo pack: out[i] = v[idx[i]] (bs values per item).
+template <int BS>
+__global__ void k_pack(int64_t n, const int32_t *__restrict__ idx, const double *__restrict__ v,
+                       double *__restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t s = int64_t(idx[i]) * BS;
+#pragma unroll
+    for (int q = 0; q < BS; ++q) out[i * BS + q] = v[s + q];
+  }
+}
+
+__global__ void k_sqrt_copy(double *p, double *copy) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const double r = sqrt(*p);
+    *p = r;
+    if (copy) *copy = r;
   }
 }
 

@@ -1,7 +1,10 @@
 // libmgb200.so: the C ABI of include/mg.h.  Context and level state, device
 // upload of the SELL-32-sigma operators built by host.cpp, the V-cycle of
-// Alg. `gmg` with CUDA-graph capture, and the MG iteration /
-// MG-preconditioned GMRES drivers.
+// Alg. `gmg` with CUDA-graph capture, the MG iteration /
+// MG-preconditioned GMRES drivers, and the
+// row-partitioned multi-GPU variant (halo exchange before every A-pass and
+// transfer, all-reduced Krylov dots, agglomeration of replicated coarse
+// levels) over the transports of comm.h.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -10,43 +13,64 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <string>
 #include <tuple>
 #include <vector>
 
 #include "../../include/mg.h"
 #include "../../include/mg_internal.h"
+#include "comm.h"
 #include "kernels.cuh"
 
-#define MGB200_VERSION "mgb200 0.1 (sm_100a, fp64, SELL-32-sigma)"
+#define MGB200_VERSION "mgb200 0.2 (sm_100a, fp64, SELL-32-sigma, multi-GPU halo)"
 
 namespace {
 
 thread_local std::string g_err;
 thread_local int64_t g_tally = 0;  // kernel launches issued by this thread (bench accounting)
 
-mg_status fail(mg_status st, const char *fmt, ...) {
+mg_status vfail(mg_status st, const char *fmt, va_list ap) {
   char buf[512];
-  va_list ap;
-  va_start(ap, fmt);
   vsnprintf(buf, sizeof buf, fmt, ap);
-  va_end(ap);
   g_err = buf;
   return st;
 }
 
-#define CU(x)                                                                           \
-  do {                                                                                  \
-    cudaError_t e_ = (x);                                                               \
-    if (e_ != cudaSuccess) {                                                            \
+mg_status fail(mg_status st, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vfail(st, fmt, ap);
+  va_end(ap);
+  return st;
+}
+
+}  // namespace
+
+namespace mgc {
+mg_status comm_fail(mg_status st, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vfail(st, fmt, ap);
+  va_end(ap);
+  return st;
+}
+}  // namespace mgc
+
+namespace {
+
+#define CU(x)                                                                                \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess) {                                                                 \
       if (e_ == cudaErrorMemoryAllocation) return fail(MG_ERR_OOM, "%s: out of memory", #x); \
-      return fail(MG_ERR_CUDA, "%s: %s", #x, cudaGetErrorString(e_));                   \
-    }                                                                                   \
+      return fail(MG_ERR_CUDA, "%s: %s", #x, cudaGetErrorString(e_));                        \
+    }                                                                                        \
   } while (0)
-#define TRY(x)                   \
-  do {                           \
-    mg_status s_ = (x);          \
-    if (s_ != MG_OK) return s_;  \
+#define TRY(x)                  \
+  do {                          \
+    mg_status s_ = (x);         \
+    if (s_ != MG_OK) return s_; \
   } while (0)
 
 constexpr int kSigma = 4096;                       // sorting window of SELL-32-sigma
@@ -100,7 +124,7 @@ struct SellOp {
   mgk::Sell view() const { return mgk::Sell{slice_ptr.p, perm.p, col.p, val.p, n_slices}; }
 };
 
-// Build SELL-32-sigma on the host and upload it.
+// Build SELL-32-sigma on the host and upload it (col: LOCAL column indices).
 mg_status build_sell(SellOp &op, int64_t n, const int64_t *rp, const int64_t *col, const double *val, int vpe) {
   int64_t ns = 0, ne = 0;
   int st = mgi_sell_size(n, rp, kSigma, &ns, &ne);
@@ -136,18 +160,37 @@ mg_status fetch(std::vector<T> &dst, const T *src, size_t count, int mem) {
   return MG_OK;
 }
 
+// Ghost exchange of one vector kind (multi-GPU).  `active` is uniform over
+// ranks (set for every operator of a distributed level), so every rank takes
+// part in every exchange even when its own pattern is empty.
+struct Halo {
+  bool active = false;
+  mgc::Pattern pat;
+  DevArray<int32_t> send_idx;  // owned rows to pack, in send order
+  DevArray<double> sendbuf, ghost;
+  int64_t n_ghost = 0;
+};
+
 struct Level {
   bool declared = false;
   int64_t n_global = 0, row_begin = 0, row_end = 0, n = 0;
+  bool dist = false;             // rows partitioned over ranks
+  std::vector<int64_t> bounds;   // [nranks+1] row ranges of the ranks (distributed levels)
   SellOp A;
   int64_t nnzb = 0;
+  Halo hx;                        // ghosts of x for A-passes on this level
   std::vector<double> diag_host;  // diagonal blocks until D^-1 is built
   std::vector<double> dinv_host;  // user-supplied D^-1 (row-major blocks)
   std::vector<int64_t> rp0, col0;  // level-0 copy for the dense coarse inverse
   std::vector<double> val0;
-  DevArray<double> dinv;          // sliced D^-1 (chunked like a 1-entry slice)
+  DevArray<double> dinv;  // sliced D^-1 (chunked like a 1-entry slice)
   bool dinv_ready = false;
-  SellOp P, R;  // P_{l-1}: level l-1 -> l, R_{l-1} = P^T
+  SellOp P, R;  // P_{l-1}: level l-1 -> l (rows: owned fine rows), R_{l-1} = P^T (rows: r_row0 ...)
+  Halo hp;      // ghosts of the coarse vector y for P (coarse level distributed)
+  Halo hr;      // ghosts of the fine vector r for R (this level distributed)
+  int64_t r_row0 = 0, r_rows = 0;  // coarse rows produced by the local R
+  bool agglomerate = false;        // coarse level replicated: all-gather d after R
+  std::vector<int64_t> ag_counts, ag_displs;
   int wpe = 1;
   int64_t nnz_p = 0;
   double omega = 0.0;
@@ -175,8 +218,10 @@ struct mg_ctx_s {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int n_sm = 148;
+  std::unique_ptr<mgc::Transport> tr;  // null => single GPU
   std::vector<Level> lv;
   SellOp H;
+  Halo hh;
   DevArray<double> cinv;  // dense A_0^-1, row stride cld
   int64_t cN = 0, cld = 0;
   DevArray<double> red_part, scal;
@@ -187,7 +232,7 @@ struct mg_ctx_s {
   // GMRES workspace
   int gm_m = 0;
   DevArray<double> gm_V, gm_Z, gm_state;
-  double *gm_host = nullptr;  // pinned [8]
+  double *gm_host = nullptr;  // pinned
   mgk::GmresDev gm{};
   ~mg_ctx_s() {
     for (auto &kv : graphs) cudaGraphExecDestroy(kv.second.exec);
@@ -201,6 +246,9 @@ struct mg_ctx_s {
   }
   int bs() const { return cfg.block_size; }
   int L() const { return cfg.n_levels - 1; }
+  int nranks() const { return tr ? tr->nranks : 1; }
+  int rank() const { return tr ? tr->rank : 0; }
+  bool use_graphs() const { return cfg.use_graphs && (!tr || tr->graph_safe()); }
 };
 
 namespace {
@@ -227,26 +275,42 @@ mg_status check_launch(const char *what = "kernel") {
   return MG_OK;
 }
 
-// --- dispatch over block size / op / cache hint ---------------------------
-template <int BS, int OP>
-void launch_apply_t(const SellOp &A, const double *x, const double *b, const double *dinv, double *out, double alpha,
+// Input vector of an operator: owned part x, ghost part xg (HALO when xg != 0)
+struct In {
+  const double *x;
+  const double *xg;
+  int n_own;
+};
+
+// --- dispatch over block size / op / cache hint / halo -------------------------
+template <int BS, int OP, bool HALO>
+void launch_apply_h(const SellOp &A, In in, const double *b, const double *dinv, double *out, double alpha,
                     double beta, cudaStream_t st) {
-  if (A.n_slices == 0) return;
   const unsigned g = grid_for_slices(A.n_slices);
   if (A.stream)
-    ++g_tally, mgk::k_sell_apply<BS, OP, true><<<g, mgk::kCta, 0, st>>>(A.view(), x, b, dinv, out, alpha, beta);
+    ++g_tally, mgk::k_sell_apply<BS, OP, true, HALO>
+                   <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
   else
-    ++g_tally, mgk::k_sell_apply<BS, OP, false><<<g, mgk::kCta, 0, st>>>(A.view(), x, b, dinv, out, alpha, beta);
+    ++g_tally, mgk::k_sell_apply<BS, OP, false, HALO>
+                   <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+}
+
+template <int BS, int OP>
+void launch_apply_t(const SellOp &A, In in, const double *b, const double *dinv, double *out, double alpha,
+                    double beta, cudaStream_t st) {
+  if (A.n_slices == 0) return;
+  if (in.xg) launch_apply_h<BS, OP, true>(A, in, b, dinv, out, alpha, beta, st);
+  else launch_apply_h<BS, OP, false>(A, in, b, dinv, out, alpha, beta, st);
 }
 
 template <int OP>
-mg_status launch_apply(int bs, const SellOp &A, const double *x, const double *b, const double *dinv, double *out,
+mg_status launch_apply(int bs, const SellOp &A, In in, const double *b, const double *dinv, double *out,
                        double alpha, double beta, cudaStream_t st) {
   switch (bs) {
-    case 1: launch_apply_t<1, OP>(A, x, b, dinv, out, alpha, beta, st); break;
-    case 2: launch_apply_t<2, OP>(A, x, b, dinv, out, alpha, beta, st); break;
-    case 3: launch_apply_t<3, OP>(A, x, b, dinv, out, alpha, beta, st); break;
-    case 4: launch_apply_t<4, OP>(A, x, b, dinv, out, alpha, beta, st); break;
+    case 1: launch_apply_t<1, OP>(A, in, b, dinv, out, alpha, beta, st); break;
+    case 2: launch_apply_t<2, OP>(A, in, b, dinv, out, alpha, beta, st); break;
+    case 3: launch_apply_t<3, OP>(A, in, b, dinv, out, alpha, beta, st); break;
+    case 4: launch_apply_t<4, OP>(A, in, b, dinv, out, alpha, beta, st); break;
     default: return fail(MG_ERR_INVALID_ARG, "block size %d not supported", bs);
   }
   return check_launch(OP == mgk::OP_SWEEP ? "sweep" : OP == mgk::OP_RESID ? "residual" : "spmv");
@@ -255,7 +319,8 @@ mg_status launch_apply(int bs, const SellOp &A, const double *x, const double *b
 template <int BS>
 void launch_sweep0_t(const SellOp &A, const double *dinv, const double *b, double *x, double omega, cudaStream_t st) {
   if (A.n_slices == 0) return;
-  ++g_tally, mgk::k_sweep0<BS><<<grid_for_slices(A.n_slices), mgk::kCta, 0, st>>>(A.n_slices, A.perm.p, dinv, b, x, omega);
+  ++g_tally,
+      mgk::k_sweep0<BS><<<grid_for_slices(A.n_slices), mgk::kCta, 0, st>>>(A.n_slices, A.perm.p, dinv, b, x, omega);
 }
 
 mg_status launch_sweep0(int bs, const SellOp &A, const double *dinv, const double *b, double *x, double omega,
@@ -270,23 +335,30 @@ mg_status launch_sweep0(int bs, const SellOp &A, const double *dinv, const doubl
   return check_launch("sweep0");
 }
 
-template <int BS, int WPE, bool ACC>
-void launch_transfer_t(const SellOp &T, const double *in, double *out, cudaStream_t st) {
-  if (T.n_slices == 0) return;
+template <int BS, int WPE, bool ACC, bool HALO>
+void launch_transfer_h(const SellOp &T, In in, double *out, cudaStream_t st) {
   const unsigned g = grid_for_slices(T.n_slices);
   if (T.stream)
-    ++g_tally, mgk::k_transfer<BS, WPE, ACC, true><<<g, mgk::kCta, 0, st>>>(T.view(), in, out);
+    ++g_tally, mgk::k_transfer<BS, WPE, ACC, true, HALO><<<g, mgk::kCta, 0, st>>>(T.view(), in.x, in.xg, in.n_own, out);
   else
-    ++g_tally, mgk::k_transfer<BS, WPE, ACC, false><<<g, mgk::kCta, 0, st>>>(T.view(), in, out);
+    ++g_tally,
+        mgk::k_transfer<BS, WPE, ACC, false, HALO><<<g, mgk::kCta, 0, st>>>(T.view(), in.x, in.xg, in.n_own, out);
+}
+
+template <int BS, int WPE, bool ACC>
+void launch_transfer_t(const SellOp &T, In in, double *out, cudaStream_t st) {
+  if (T.n_slices == 0) return;
+  if (in.xg) launch_transfer_h<BS, WPE, ACC, true>(T, in, out, st);
+  else launch_transfer_h<BS, WPE, ACC, false>(T, in, out, st);
 }
 
 template <int BS, bool ACC>
-void launch_transfer_bs(const SellOp &T, const double *in, double *out, cudaStream_t st) {
+void launch_transfer_bs(const SellOp &T, In in, double *out, cudaStream_t st) {
   if (T.vpe == 1 || BS == 1) launch_transfer_t<BS, 1, ACC>(T, in, out, st);
   else launch_transfer_t<BS, BS, ACC>(T, in, out, st);
 }
 
-mg_status launch_transfer(int bs, bool acc, const SellOp &T, const double *in, double *out, cudaStream_t st) {
+mg_status launch_transfer(int bs, bool acc, const SellOp &T, In in, double *out, cudaStream_t st) {
   switch (bs) {
     case 1: acc ? launch_transfer_bs<1, true>(T, in, out, st) : launch_transfer_bs<1, false>(T, in, out, st); break;
     case 2: acc ? launch_transfer_bs<2, true>(T, in, out, st) : launch_transfer_bs<2, false>(T, in, out, st); break;
@@ -297,35 +369,131 @@ mg_status launch_transfer(int bs, bool acc, const SellOp &T, const double *in, d
   return check_launch(acc ? "prolong-add" : "transfer");
 }
 
-// --- reductions --------------------------------------------------------------
+// --- halo exchange: pack owned rows, transport into the ghost buffer ----------
+mg_status halo_exchange(mg_ctx_s *c, Halo &h, const double *v) {
+  if (!h.active) return MG_OK;
+  const int bs = c->bs();
+  const int64_t ns = h.pat.n_send;
+  if (ns > 0) {
+    const unsigned g = unsigned(std::min<int64_t>((ns + 255) / 256, 4 * c->n_sm));
+    switch (bs) {
+      case 1: ++g_tally, mgk::k_pack<1><<<g, 256, 0, c->stream>>>(ns, h.send_idx.p, v, h.sendbuf.p); break;
+      case 2: ++g_tally, mgk::k_pack<2><<<g, 256, 0, c->stream>>>(ns, h.send_idx.p, v, h.sendbuf.p); break;
+      case 3: ++g_tally, mgk::k_pack<3><<<g, 256, 0, c->stream>>>(ns, h.send_idx.p, v, h.sendbuf.p); break;
+      default: ++g_tally, mgk::k_pack<4><<<g, 256, 0, c->stream>>>(ns, h.send_idx.p, v, h.sendbuf.p); break;
+    }
+    TRY(check_launch("halo pack"));
+  }
+  return c->tr->exchange(h.pat, bs, h.sendbuf.p, h.ghost.p, c->stream);
+}
+
+// Build a halo from sorted unique ghost global rows of a level with ranges
+// `bounds`; my owned rows there start at `row_begin`.  Collective.
+mg_status build_halo(mg_ctx_s *c, Halo &h, const std::vector<int64_t> &ghosts, const std::vector<int64_t> &bounds,
+                     int64_t row_begin, int64_t row_end) {
+  const int P = c->nranks(), me = c->rank();
+  h = Halo();
+  h.active = true;
+  h.n_ghost = int64_t(ghosts.size());
+  std::vector<std::vector<char>> out(P), in;
+  std::vector<std::vector<int64_t>> req(P);
+  for (int64_t g : ghosts) {
+    const int o = mgi_owner(g, bounds.data(), P);
+    if (o < 0 || o >= P || o == me) return fail(MG_ERR_STRUCTURE, "ghost %lld has no owner", (long long)g);
+    req[o].push_back(g);
+  }
+  int64_t off = 0;
+  for (int r = 0; r < P; ++r) {
+    if (req[r].empty()) continue;
+    h.pat.recv_rank.push_back(r);
+    h.pat.recv_off.push_back(off);
+    h.pat.recv_cnt.push_back(int64_t(req[r].size()));
+    off += int64_t(req[r].size());
+    out[r].resize(req[r].size() * sizeof(int64_t));
+    std::memcpy(out[r].data(), req[r].data(), out[r].size());
+  }
+  h.pat.n_recv = off;
+  TRY(c->tr->alltoallv_host(out, in));
+  std::vector<int32_t> idx;
+  for (int r = 0; r < P; ++r) {
+    const int64_t cnt = int64_t(in[r].size() / sizeof(int64_t));
+    if (!cnt) continue;
+    const int64_t *g = reinterpret_cast<const int64_t *>(in[r].data());
+    h.pat.send_rank.push_back(r);
+    h.pat.send_off.push_back(int64_t(idx.size()));
+    h.pat.send_cnt.push_back(cnt);
+    for (int64_t k = 0; k < cnt; ++k) {
+      if (g[k] < row_begin || g[k] >= row_end) return fail(MG_ERR_STRUCTURE, "halo request for a row not owned");
+      idx.push_back(int32_t(g[k] - row_begin));
+    }
+  }
+  h.pat.n_send = int64_t(idx.size());
+  TRY(h.send_idx.upload(idx.data(), idx.size()));
+  TRY(h.sendbuf.alloc(size_t(std::max<int64_t>(1, h.pat.n_send)) * c->bs()));
+  TRY(h.ghost.alloc(size_t(std::max<int64_t>(1, h.n_ghost)) * c->bs()));
+  return MG_OK;
+}
+
+// Renumber the global columns of a local operator (rows: rp.size()-1) whose
+// column space is a level owned here as [rb, re) into owned + ghost (sorted).
+mg_status localize(int64_t rb, int64_t re, const std::vector<int64_t> &rp, std::vector<int64_t> &col,
+                   std::vector<int64_t> &ghosts) {
+  const int64_t nnz = int64_t(col.size());
+  std::vector<int64_t> loc(std::max<int64_t>(1, nnz)), gh(std::max<int64_t>(1, nnz));
+  int64_t ng = 0;
+  mgi_localize_columns(int64_t(rp.size()) - 1, rb, re, rp.data(), col.data(), loc.data(), gh.data(), &ng);
+  loc.resize(nnz);
+  ghosts.assign(gh.begin(), gh.begin() + ng);
+  col.swap(loc);
+  return MG_OK;
+}
+
+// --- reductions (deterministic; all-reduced over ranks on distributed levels) ---
 unsigned red_grid(const mg_ctx_s *c, int64_t n) {
   const int64_t want = (n + mgk::kRedThreads * 4 - 1) / (mgk::kRedThreads * 4);
   return unsigned(std::max<int64_t>(1, std::min<int64_t>(want, 2 * c->n_sm)));
 }
 
-// res (device) = (a, b)
-mg_status dev_dot(mg_ctx_s *c, int64_t n, const double *a, const double *b, double *res, bool sqrt_) {
-  const unsigned g = red_grid(c, n);
-  if (sqrt_)
-    ++g_tally, mgk::k_reduce<0, true><<<g, mgk::kRedThreads, 0, c->stream>>>(n, const_cast<double *>(a), b, nullptr, nullptr,
-                                                                   c->red_part.p, c->ticket.p, res, nullptr);
-  else
-    ++g_tally, mgk::k_reduce<0, false><<<g, mgk::kRedThreads, 0, c->stream>>>(n, const_cast<double *>(a), b, nullptr, nullptr,
-                                                                    c->red_part.p, c->ticket.p, res, nullptr);
-  return check_launch("dot");
+mg_status finish_reduce(mg_ctx_s *c, bool dist, double *res, bool sqrt_, double *copy = nullptr) {
+  if (!dist) {
+    if (copy) CU(cudaMemcpyAsync(copy, res, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    return MG_OK;
+  }
+  TRY(c->tr->allreduce_sum(res, 1, c->stream));
+  if (sqrt_) {
+    ++g_tally, mgk::k_sqrt_copy<<<1, 32, 0, c->stream>>>(res, copy);
+    return check_launch("sqrt");
+  }
+  if (copy) CU(cudaMemcpyAsync(copy, res, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  return MG_OK;
 }
 
-// MGS step: a -= (*h) v ; res = (a, u) or ||a|| (u == nullptr; also -> res2)
-mg_status dev_axpy_dot(mg_ctx_s *c, int64_t n, double *a, const double *v, const double *h, const double *u,
-                       double *res) {
+// res (device) = (a, b) [sqrt] over the level's rows (all ranks if dist)
+mg_status dev_dot(mg_ctx_s *c, bool dist, int64_t n, const double *a, const double *b, double *res, bool sqrt_) {
   const unsigned g = red_grid(c, n);
-  if (u)
-    ++g_tally, mgk::k_reduce<1, false><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, u, v, h, c->red_part.p, c->ticket.p, res,
-                                                                    nullptr);
+  double *A = const_cast<double *>(a);
+  if (sqrt_ && !dist)
+    ++g_tally, mgk::k_reduce<0, true><<<g, mgk::kRedThreads, 0, c->stream>>>(n, A, b, nullptr, nullptr, c->red_part.p,
+                                                                               c->ticket.p, res, nullptr);
   else
-    ++g_tally, mgk::k_reduce<1, true><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, nullptr, v, h, c->red_part.p, c->ticket.p,
-                                                                   res, nullptr);
-  return check_launch("axpy-dot");
+    ++g_tally, mgk::k_reduce<0, false><<<g, mgk::kRedThreads, 0, c->stream>>>(n, A, b, nullptr, nullptr, c->red_part.p,
+                                                                                c->ticket.p, res, nullptr);
+  TRY(check_launch("dot"));
+  return finish_reduce(c, dist, res, sqrt_);
+}
+
+// MGS step: a -= (*h) v ; res = (a, u), or ||a|| when u == nullptr
+mg_status dev_axpy_dot(mg_ctx_s *c, bool dist, int64_t n, double *a, const double *v, const double *h,
+                       const double *u, double *res) {
+  const unsigned g = red_grid(c, n);
+  if (u || dist)
+    ++g_tally, mgk::k_reduce<1, false><<<g, mgk::kRedThreads, 0, c->stream>>>(
+                   n, a, u, v, h, c->red_part.p, c->ticket.p, res, nullptr);
+  else
+    ++g_tally, mgk::k_reduce<1, true><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, nullptr, v, h, c->red_part.p,
+                                                                               c->ticket.p, res, nullptr);
+  TRY(check_launch("axpy-dot"));
+  return finish_reduce(c, dist, res, u == nullptr);
 }
 
 // --- dense coarse inverse on the device (in-place Gauss-Jordan, partial pivoting)
@@ -336,7 +504,10 @@ __global__ void k_gj_pivot(int64_t N, int64_t ld, double *a, int64_t k, int64_t 
   int64_t bidx = k;
   for (int64_t r = k + threadIdx.x; r < N; r += blockDim.x) {
     const double v = fabs(a[r * ld + k]);
-    if (v > best) { best = v; bidx = r; }
+    if (v > best) {
+      best = v;
+      bidx = r;
+    }
   }
   bv[threadIdx.x] = best;
   bi[threadIdx.x] = bidx;
@@ -372,7 +543,10 @@ __global__ void k_gj_pivot(int64_t N, int64_t ld, double *a, int64_t k, int64_t 
   __syncthreads();
   for (int64_t c = threadIdx.x; c < N; c += blockDim.x) a[k * ld + c] /= d;
   for (int64_t r = threadIdx.x; r < N; r += blockDim.x) {
-    if (r == k) { f[r] = 0.0; continue; }
+    if (r == k) {
+      f[r] = 0.0;
+      continue;
+    }
     f[r] = a[r * ld + k];
     a[r * ld + k] = 0.0;
   }
@@ -425,7 +599,7 @@ mg_status build_coarse_inverse(mg_ctx_s *c) {
     k_gj_eliminate<<<dim3(gx, unsigned(N)), 256, 0, c->stream>>>(N, ld, c->cinv.p, k, f.p);
   }
   k_gj_unswap<<<unsigned((N + 255) / 256), 256, 0, c->stream>>>(N, ld, c->cinv.p, piv.p);
-  TRY(check_launch());
+  TRY(check_launch("coarse inverse"));
   int s = 0;
   CU(cudaMemcpyAsync(&s, sing.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
@@ -470,6 +644,11 @@ mg_status finalize(mg_ctx_s *c) {
     if (!L.A.set) return fail(MG_ERR_STATE, "level %d has no matrix (mg_set_matrix)", l);
     if (l > 0 && !L.P.set) return fail(MG_ERR_STATE, "level %d has no transfer (mg_set_transfer)", l);
   }
+  if (c->cfg.coarse_mode == MG_COARSE_DIRECT && c->lv[0].dist)
+    return fail(MG_ERR_INVALID_ARG, "direct coarse solve needs a replicated level 0");
+  for (int l = 0; l < c->L(); ++l)
+    if (c->lv[l].dist && !c->lv[l + 1].dist)
+      return fail(MG_ERR_INVALID_ARG, "level %d is distributed below replicated level %d", l, l + 1);
   for (int l = 0; l <= c->L(); ++l) {
     Level &L = c->lv[l];
     if (!L.dinv_ready) {
@@ -478,7 +657,6 @@ mg_status finalize(mg_ctx_s *c) {
       } else {
         const int V = bs * bs;
         std::vector<double> inv(size_t(L.n) * V);
-        // identity row pointers over the stored diagonal blocks
         std::vector<int64_t> rp(L.n + 1), cl(L.n);
         for (int64_t i = 0; i <= L.n; ++i) rp[i] = i;
         for (int64_t i = 0; i < L.n; ++i) cl[i] = i;
@@ -489,7 +667,7 @@ mg_status finalize(mg_ctx_s *c) {
       }
       std::vector<double>().swap(L.diag_host);
     }
-    const size_t nv = size_t(L.n) * bs;
+    const size_t nv = size_t(std::max<int64_t>(1, L.n)) * bs;
     if (L.w.n < nv) TRY(L.w.alloc(nv));
     if (l < c->L()) {
       if (L.x.n < nv) TRY(L.x.alloc(nv));
@@ -507,7 +685,48 @@ mg_status finalize(mg_ctx_s *c) {
   return MG_OK;
 }
 
-// --- V-cycle pieces (stream-ordered, capturable) -----------------------------
+// --- V-cycle pieces (stream-ordered; capturable with NCCL / single GPU) ---------
+In in_of(Level &L, Halo &h, const double *v) {
+  return In{v, h.active ? h.ghost.p : nullptr, int(L.n)};
+}
+
+mg_status a_pass_sweep(mg_ctx_s *c, int l, const double *src, const double *b, double *dst) {
+  Level &L = c->lv[l];
+  TRY(halo_exchange(c, L.hx, src));
+  return launch_apply<mgk::OP_SWEEP>(c->bs(), L.A, in_of(L, L.hx, src), b, L.dinv.p, dst, lv_omega(c, L), 0.0,
+                                     c->stream);
+}
+
+mg_status a_pass_resid(mg_ctx_s *c, int l, const double *x, const double *b, double *r) {
+  Level &L = c->lv[l];
+  TRY(halo_exchange(c, L.hx, x));
+  return launch_apply<mgk::OP_RESID>(c->bs(), L.A, in_of(L, L.hx, x), b, nullptr, r, 1.0, 0.0, c->stream);
+}
+
+mg_status a_pass_spmv(mg_ctx_s *c, int l, double alpha, const double *x, double beta, double *y) {
+  Level &L = c->lv[l];
+  TRY(halo_exchange(c, L.hx, x));
+  return launch_apply<mgk::OP_SPMV>(c->bs(), L.A, in_of(L, L.hx, x), nullptr, nullptr, y, alpha, beta, c->stream);
+}
+
+// d_coarse = R r_fine (all coarse rows on every rank if the coarse level is replicated)
+mg_status do_restrict(mg_ctx_s *c, int l, const double *r, double *d) {
+  Level &L = c->lv[l];
+  const int bs = c->bs();
+  TRY(halo_exchange(c, L.hr, r));
+  TRY(launch_transfer(bs, false, L.R, in_of(L, L.hr, r), d + L.r_row0 * bs, c->stream));
+  if (L.agglomerate) TRY(c->tr->allgatherv(d + L.r_row0 * bs, d, L.ag_counts, L.ag_displs, c->stream));
+  return MG_OK;
+}
+
+// x_fine += P y_coarse
+mg_status do_prolong(mg_ctx_s *c, int l, const double *y, double *x) {
+  Level &L = c->lv[l];
+  Level &C = c->lv[l - 1];
+  TRY(halo_exchange(c, L.hp, y));
+  return launch_transfer(c->bs(), true, L.P, In{y, L.hp.active ? L.hp.ghost.p : nullptr, int(C.n)}, x, c->stream);
+}
+
 mg_status smooth(mg_ctx_s *c, int l, double *x, const double *b, int k, bool zero) {
   Level &L = c->lv[l];
   const int bs = c->bs();
@@ -522,7 +741,7 @@ mg_status smooth(mg_ctx_s *c, int l, double *x, const double *b, int k, bool zer
   }
   double *src = x, *dst = L.w.p;
   for (int i = 0; i < k; ++i) {
-    TRY(launch_apply<mgk::OP_SWEEP>(bs, L.A, src, b, L.dinv.p, dst, om, 0.0, c->stream));
+    TRY(a_pass_sweep(c, l, src, b, dst));
     std::swap(src, dst);
   }
   if (src != x) CU(cudaMemcpyAsync(x, src, size_t(L.n) * bs * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
@@ -533,7 +752,7 @@ mg_status coarse_solve(mg_ctx_s *c, const double *b, double *x) {
   if (c->cfg.coarse_mode == MG_COARSE_DIRECT) {
     const unsigned g = unsigned((c->cN + mgk::kWarpsPerCta - 1) / mgk::kWarpsPerCta);
     ++g_tally, mgk::k_dense_gemv<<<g, mgk::kCta, 0, c->stream>>>(c->cN, c->cld, c->cinv.p, b, x);
-    return check_launch();
+    return check_launch("coarse gemv");
   }
   return smooth(c, 0, x, b, std::max(1, c->cfg.coarse_sweeps), true);
 }
@@ -543,17 +762,16 @@ mg_status vcycle_rec(mg_ctx_s *c, int l, double *x, const double *b, bool zero) 
   if (l == 0) return coarse_solve(c, b, x);  // Step 0; ignores x (Z21)
   Level &L = c->lv[l];
   Level &C = c->lv[l - 1];
-  const int bs = c->bs();
-  TRY(smooth(c, l, x, b, lv_nu_pre(c, L), zero));                                             // Step 1
-  TRY(launch_apply<mgk::OP_RESID>(bs, L.A, x, b, nullptr, L.w.p, 1.0, 0.0, c->stream));       // Step 2
-  TRY(launch_transfer(bs, false, L.R, L.w.p, C.b.p, c->stream));                                //  d = R r
-  TRY(vcycle_rec(c, l - 1, C.x.p, C.b.p, true));                                               // Step 3
-  TRY(launch_transfer(bs, true, L.P, C.x.p, x, c->stream));                                    // Step 4
-  return smooth(c, l, x, b, lv_nu_post(c, L), false);                                          // Step 5
+  TRY(smooth(c, l, x, b, lv_nu_pre(c, L), zero));    // Step 1
+  TRY(a_pass_resid(c, l, x, b, L.w.p));              // Step 2: r = b - A x
+  TRY(do_restrict(c, l, L.w.p, C.b.p));              //         d = R r
+  TRY(vcycle_rec(c, l - 1, C.x.p, C.b.p, true));     // Step 3
+  TRY(do_prolong(c, l, C.x.p, x));                   // Step 4
+  return smooth(c, l, x, b, lv_nu_post(c, L), false);  // Step 5
 }
 
 mg_status run_vcycle(mg_ctx_s *c, double *x, const double *b, bool zero) {
-  if (!c->cfg.use_graphs) return vcycle_rec(c, c->L(), x, b, zero);
+  if (!c->use_graphs()) return vcycle_rec(c, c->L(), x, b, zero);
   const GraphKey key{x, b, zero ? 1 : 0};
   auto it = c->graphs.find(key);
   if (it == c->graphs.end()) {
@@ -608,8 +826,8 @@ mg_status check_level(mg_ctx_s *c, int level) {
 mg_status ensure_gmres(mg_ctx_s *c, int m) {
   const int64_t N = c->lv[c->L()].n * c->bs();
   if (c->gm_m >= m && c->gm_V.p) return MG_OK;
-  TRY(c->gm_V.alloc(size_t(m + 1) * N));
-  TRY(c->gm_Z.alloc(size_t(m) * N));
+  TRY(c->gm_V.alloc(size_t(m + 1) * std::max<int64_t>(N, 1)));
+  TRY(c->gm_Z.alloc(size_t(m) * std::max<int64_t>(N, 1)));
   const size_t ns = size_t(m + 1) * m + 6 * size_t(m + 1) + 16;
   TRY(c->gm_state.alloc(ns));
   CU(cudaMemset(c->gm_state.p, 0, ns * sizeof(double)));
@@ -617,16 +835,41 @@ mg_status ensure_gmres(mg_ctx_s *c, int m) {
   double *p = c->gm_state.p;
   mgk::GmresDev &g = c->gm;
   g.m = m;
-  g.H = p; p += size_t(m + 1) * m;
-  g.cs = p; p += m + 1;
-  g.sn = p; p += m + 1;
-  g.g = p; p += m + 1;
-  g.y = p; p += m + 1;
-  g.hn = p; p += m + 1;
-  g.beta = p; p += 1;
-  g.beta0 = p; p += 1;
-  g.out = p; p += 4;
+  g.H = p;
+  p += size_t(m + 1) * m;
+  g.cs = p;
+  p += m + 1;
+  g.sn = p;
+  p += m + 1;
+  g.g = p;
+  p += m + 1;
+  g.y = p;
+  p += m + 1;
+  g.hn = p;
+  p += m + 1;
+  g.beta = p;
+  p += 1;
+  g.beta0 = p;
+  p += 1;
+  g.out = p;
   c->gm_m = m;
+  return MG_OK;
+}
+
+// validated host copies of a CSR/BSR input
+mg_status fetch_csr(mg_ctx_s *c, int64_t n, int64_t n_cols, const int64_t *row_ptr, const int64_t *col,
+                    const double *vals, int64_t nnz, int vpe, int mem, bool need_diag, int64_t diag_offset,
+                    std::vector<int64_t> &rp, std::vector<int64_t> &cl, std::vector<double> &v, const char *what) {
+  (void)c;
+  if (nnz < 0) return fail(MG_ERR_DIMENSION, "%s: nnz < 0", what);
+  TRY(fetch(rp, row_ptr, size_t(n + 1), mem));
+  if (rp[n] != nnz)
+    return fail(MG_ERR_DIMENSION, "%s: row_ptr[n] = %lld != nnz = %lld", what, (long long)rp[n], (long long)nnz);
+  TRY(fetch(cl, col, size_t(nnz), mem));
+  TRY(fetch(v, vals, size_t(nnz) * vpe, mem));
+  const int st = mgi_validate_csr(n, n_cols, rp.data(), cl.data(), v.data(), vpe, need_diag ? 1 : 0, diag_offset);
+  if (st == MG_ERR_NONFINITE) return fail(MG_ERR_NONFINITE, "%s: non-finite value", what);
+  if (st) return fail(MG_ERR_STRUCTURE, "%s: invalid CSR structure (row_ptr / columns / diagonal)", what);
   return MG_OK;
 }
 
@@ -640,6 +883,11 @@ extern "C" {
 const char *mg_last_error(void) { return g_err.c_str(); }
 const char *mg_version(void) { return MGB200_VERSION; }
 
+mg_status mg_get_unique_id(unsigned char out[128]) {
+  if (!out) return fail(MG_ERR_INVALID_ARG, "NULL argument");
+  return mgc::nccl_unique_id(out);
+}
+
 mg_status mg_create(mg_ctx *out, const mg_config *cfg, int device, void *cuda_stream, const mg_comm *comm) {
   if (!out || !cfg) return fail(MG_ERR_INVALID_ARG, "NULL argument");
   *out = nullptr;
@@ -649,14 +897,17 @@ mg_status mg_create(mg_ctx *out, const mg_config *cfg, int device, void *cuda_st
   if (!(cfg->omega > 0.0) || !std::isfinite(cfg->omega)) return fail(MG_ERR_INVALID_ARG, "omega must be > 0");
   if (cfg->coarse_mode != MG_COARSE_DIRECT && cfg->coarse_mode != MG_COARSE_SMOOTH)
     return fail(MG_ERR_INVALID_ARG, "bad coarse_mode");
-  if (comm && comm->nranks > 1) return fail(MG_ERR_INVALID_ARG, "multi-GPU contexts are not built into this library");
   DeviceGuard dg(device);
   int ndev = 0;
   CU(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) return fail(MG_ERR_INVALID_ARG, "device %d out of range", device);
+  CU(cudaSetDevice(device));
+  std::unique_ptr<mgc::Transport> tr;
+  TRY(mgc::make_transport(comm, device, tr));
   auto *c = new mg_ctx_s();
   c->cfg = *cfg;
   c->device = device;
+  c->tr = std::move(tr);
   cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device);
   if (cuda_stream) {
     c->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -685,14 +936,45 @@ mg_status mg_create_level(mg_ctx c, int level, int64_t n_rows_global, int64_t ro
   if (level < 0 || level > c->L()) return fail(MG_ERR_INVALID_ARG, "level %d out of range", level);
   if (n_rows_global < 1 || n_rows_global >= (int64_t(1) << 31))
     return fail(MG_ERR_DIMENSION, "n_rows_global must be in [1, 2^31)");
-  if (row_begin != 0 || row_end != n_rows_global)
-    return fail(MG_ERR_INVALID_ARG, "single-GPU context: a level must own all rows");
+  if (row_begin < 0 || row_end < row_begin || row_end > n_rows_global)
+    return fail(MG_ERR_INVALID_ARG, "bad row range [%lld, %lld)", (long long)row_begin, (long long)row_end);
+  DeviceGuard dg(c->device);
   Level &L = c->lv[level];
+  const int P = c->nranks();
+  bool dist = false;
+  std::vector<int64_t> bounds;
+  if (P > 1) {
+    int64_t mine[3] = {n_rows_global, row_begin, row_end};
+    std::vector<int64_t> allv(3 * size_t(P));
+    TRY(c->tr->allgather_host(mine, sizeof mine, allv.data()));
+    bool repl = true, tiled = true;
+    for (int r = 0; r < P; ++r) {
+      if (allv[3 * r] != n_rows_global) return fail(MG_ERR_DIMENSION, "ranks disagree on level %d size", level);
+      repl = repl && allv[3 * r + 1] == 0 && allv[3 * r + 2] == n_rows_global;
+      tiled = tiled && allv[3 * r + 1] == (r == 0 ? 0 : allv[3 * (r - 1) + 2]);
+    }
+    tiled = tiled && allv[3 * (P - 1) + 2] == n_rows_global;
+    if (!repl && !tiled)
+      return fail(MG_ERR_INVALID_ARG, "level %d: row ranges must tile [0, n) in rank order or all be [0, n)", level);
+    dist = !repl;
+    if (dist) {
+      bounds.resize(P + 1);
+      for (int r = 0; r < P; ++r) bounds[r] = allv[3 * r + 1];
+      bounds[P] = n_rows_global;
+    }
+  } else if (row_begin != 0 || row_end != n_rows_global) {
+    return fail(MG_ERR_INVALID_ARG, "single-GPU context: a level must own all rows");
+  }
+  if (dist && level < c->L() && c->lv[level + 1].declared && !c->lv[level + 1].dist)
+    return fail(MG_ERR_INVALID_ARG, "level %d distributed below a replicated level", level);
+  L = Level();
   L.declared = true;
   L.n_global = n_rows_global;
   L.row_begin = row_begin;
   L.row_end = row_end;
   L.n = row_end - row_begin;
+  L.dist = dist;
+  L.bounds = bounds;
   c->invalidate();
   return MG_OK;
 }
@@ -703,24 +985,22 @@ mg_status mg_set_matrix(mg_ctx c, int level, const int64_t *row_ptr, const int64
   DeviceGuard dg(c->device);
   Level &L = c->lv[level];
   const int bs = c->bs(), V = bs * bs;
-  if (nnzb < 0) return fail(MG_ERR_DIMENSION, "nnzb < 0");
   std::vector<int64_t> rp, cl;
   std::vector<double> v;
-  TRY(fetch(rp, row_ptr, size_t(L.n + 1), mem));
-  if (rp[L.n] != nnzb) return fail(MG_ERR_DIMENSION, "row_ptr[n] = %lld != nnzb = %lld", (long long)rp[L.n], (long long)nnzb);
-  TRY(fetch(cl, col, size_t(nnzb), mem));
-  TRY(fetch(v, vals, size_t(nnzb) * V, mem));
-  const int st = mgi_validate_csr(L.n, L.n_global, rp.data(), cl.data(), v.data(), V, 1);
-  if (st == MG_ERR_NONFINITE) return fail(MG_ERR_NONFINITE, "level %d: non-finite matrix value", level);
-  if (st) return fail(MG_ERR_STRUCTURE, "level %d: invalid BSR structure (row_ptr/cols/diagonal)", level);
-  TRY(build_sell(L.A, L.n, rp.data(), cl.data(), v.data(), V));
-  L.nnzb = nnzb;
+  TRY(fetch_csr(c, L.n, L.n_global, row_ptr, col, vals, nnzb, V, mem, true, L.row_begin, rp, cl, v, "matrix"));
   L.diag_host.assign(size_t(L.n) * V, 0.0);
   for (int64_t i = 0; i < L.n; ++i)
     for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
-      if (cl[k] == i) std::memcpy(&L.diag_host[size_t(i) * V], &v[size_t(k) * V], V * sizeof(double));
+      if (cl[k] == L.row_begin + i) std::memcpy(&L.diag_host[size_t(i) * V], &v[size_t(k) * V], V * sizeof(double));
+  if (L.dist) {
+    std::vector<int64_t> ghosts;
+    TRY(localize(L.row_begin, L.row_end, rp, cl, ghosts));
+    TRY(build_halo(c, L.hx, ghosts, L.bounds, L.row_begin, L.row_end));
+  }
+  TRY(build_sell(L.A, L.n, rp.data(), cl.data(), v.data(), V));
+  L.nnzb = nnzb;
   L.dinv_ready = false;  // (re)built at finalize; a user D^-1 is re-sliced with the new permutation
-  if (level == 0) {
+  if (level == 0 && !L.dist) {
     L.rp0.swap(rp);
     L.col0.swap(cl);
     L.val0.swap(v);
@@ -737,23 +1017,96 @@ mg_status mg_set_transfer(mg_ctx c, int fine_level, const int64_t *row_ptr, cons
   if (!c->lv[fine_level - 1].declared) return fail(MG_ERR_STATE, "level %d not created", fine_level - 1);
   DeviceGuard dg(c->device);
   Level &L = c->lv[fine_level];
-  const int64_t nc = c->lv[fine_level - 1].n;
+  Level &C = c->lv[fine_level - 1];
   const int wpe = weights_per_entry;
+  const int P = c->nranks(), me = c->rank();
   if (wpe != 1 && wpe != c->bs()) return fail(MG_ERR_INVALID_ARG, "weights_per_entry must be 1 or bs");
+  if (!L.dist && C.dist) return fail(MG_ERR_INVALID_ARG, "replicated level above a distributed one");
   std::vector<int64_t> rp, cl;
   std::vector<double> v;
-  TRY(fetch(rp, row_ptr, size_t(L.n + 1), mem));
-  if (rp[L.n] != nnz) return fail(MG_ERR_DIMENSION, "row_ptr[n] != nnz");
-  TRY(fetch(cl, col, size_t(nnz), mem));
-  TRY(fetch(v, w, size_t(nnz) * wpe, mem));
-  const int st = mgi_validate_csr(L.n, nc, rp.data(), cl.data(), v.data(), wpe, 0);
-  if (st == MG_ERR_NONFINITE) return fail(MG_ERR_NONFINITE, "transfer %d: non-finite weight", fine_level);
-  if (st) return fail(MG_ERR_STRUCTURE, "transfer %d: invalid CSR structure", fine_level);
+  TRY(fetch_csr(c, L.n, C.n_global, row_ptr, col, w, nnz, wpe, mem, false, 0, rp, cl, v, "transfer"));
+  // ---- R = P^T -------------------------------------------------------
+  std::vector<int64_t> rrp, rcl;
+  std::vector<double> rv;
+  if (!L.dist) {
+    rrp.resize(C.n + 1);
+    rcl.resize(nnz);
+    rv.resize(size_t(nnz) * wpe);
+    mgi_csr_transpose(L.n, C.n, rp.data(), cl.data(), v.data(), wpe, rrp.data(), rcl.data(), rv.data());
+    L.r_row0 = 0;
+    L.r_rows = C.n;
+    L.agglomerate = false;
+    L.hr = Halo();
+  } else {
+    // rows of R computed here: my coarse rows (coarse distributed) or an even
+    // share of the replicated coarse level, all-gathered afterwards
+    std::vector<int64_t> rb(P + 1);
+    if (C.dist) {
+      rb = C.bounds;
+    } else {
+      for (int r = 0; r <= P; ++r) rb[r] = C.n_global * r / P;
+    }
+    // route every P entry (i_fine, J) to the rank computing R row J
+    std::vector<std::vector<char>> out(P), in;
+    const size_t rec = sizeof(int64_t) * 2 + sizeof(double) * wpe;
+    std::vector<int64_t> cnt(P, 0);
+    for (int64_t t = 0; t < nnz; ++t) cnt[mgi_owner(cl[t], rb.data(), P)]++;
+    for (int r = 0; r < P; ++r) out[r].resize(size_t(cnt[r]) * rec);
+    std::vector<size_t> pos(P, 0);
+    for (int64_t i = 0; i < L.n; ++i)
+      for (int64_t t = rp[i]; t < rp[i + 1]; ++t) {
+        const int o = mgi_owner(cl[t], rb.data(), P);
+        char *dst = out[o].data() + pos[o];
+        const int64_t gi = L.row_begin + i;
+        std::memcpy(dst, &cl[t], 8);
+        std::memcpy(dst + 8, &gi, 8);
+        std::memcpy(dst + 16, &v[size_t(t) * wpe], sizeof(double) * wpe);
+        pos[o] += rec;
+      }
+    TRY(c->tr->alltoallv_host(out, in));
+    std::vector<int64_t> J, I;
+    std::vector<double> W;
+    for (int r = 0; r < P; ++r)
+      for (size_t off = 0; off < in[r].size(); off += rec) {
+        int64_t j, i;
+        std::memcpy(&j, in[r].data() + off, 8);
+        std::memcpy(&i, in[r].data() + off + 8, 8);
+        J.push_back(j);
+        I.push_back(i);
+        const double *ww = reinterpret_cast<const double *>(in[r].data() + off + 16);
+        W.insert(W.end(), ww, ww + wpe);
+      }
+    // output offset into the coarse vector: local rows start at 0 on a
+    // distributed coarse level; the full vector is addressed when replicated
+    L.r_row0 = C.dist ? 0 : rb[me];
+    L.r_rows = rb[me + 1] - rb[me];
+    rrp.resize(L.r_rows + 1);
+    rcl.resize(J.size());
+    rv.resize(J.size() * wpe);
+    const int st = mgi_assemble_routed_rows(int64_t(J.size()), J.data(), I.data(), W.data(), wpe, rb[me], L.r_rows,
+                                            rrp.data(), rcl.data(), rv.data());
+    if (st) return fail(MG_ERR_STRUCTURE, "restriction routing failed");
+    std::vector<int64_t> ghosts;
+    TRY(localize(L.row_begin, L.row_end, rrp, rcl, ghosts));
+    TRY(build_halo(c, L.hr, ghosts, L.bounds, L.row_begin, L.row_end));
+    L.agglomerate = !C.dist;
+    L.ag_counts.assign(P, 0);
+    L.ag_displs.assign(P, 0);
+    for (int r = 0; r < P; ++r) {
+      L.ag_counts[r] = (rb[r + 1] - rb[r]) * c->bs();
+      L.ag_displs[r] = rb[r] * c->bs();
+    }
+  }
+  TRY(build_sell(L.R, L.r_rows, rrp.data(), rcl.data(), rv.data(), wpe));
+  // ---- P: columns are coarse rows ------------------------------------------
+  if (C.dist) {
+    std::vector<int64_t> ghosts;
+    TRY(localize(C.row_begin, C.row_end, rp, cl, ghosts));
+    TRY(build_halo(c, L.hp, ghosts, C.bounds, C.row_begin, C.row_end));
+  } else {
+    L.hp = Halo();
+  }
   TRY(build_sell(L.P, L.n, rp.data(), cl.data(), v.data(), wpe));
-  std::vector<int64_t> rrp(nc + 1), rcl(nnz);
-  std::vector<double> rv(size_t(nnz) * wpe);
-  mgi_csr_transpose(L.n, nc, rp.data(), cl.data(), v.data(), wpe, rrp.data(), rcl.data(), rv.data());
-  TRY(build_sell(L.R, nc, rrp.data(), rcl.data(), rv.data(), wpe));
   L.wpe = wpe;
   L.nnz_p = nnz;
   c->invalidate();
@@ -784,17 +1137,18 @@ mg_status mg_set_constraints(mg_ctx c, const int64_t *H_row_ptr, const int64_t *
   TRY(check_ctx(c));
   TRY(check_level(c, c->L()));
   DeviceGuard dg(c->device);
-  const int64_t n = c->lv[c->L()].n;
+  Level &F = c->lv[c->L()];
   std::vector<int64_t> rp, cl;
   std::vector<double> v;
-  TRY(fetch(rp, H_row_ptr, size_t(n + 1), mem));
-  if (rp[n] != nnz) return fail(MG_ERR_DIMENSION, "H row_ptr[n] != nnz");
-  TRY(fetch(cl, H_col, size_t(nnz), mem));
-  TRY(fetch(v, H_w, size_t(nnz), mem));
-  const int st = mgi_validate_csr(n, n, rp.data(), cl.data(), v.data(), 1, 0);
-  if (st == MG_ERR_NONFINITE) return fail(MG_ERR_NONFINITE, "H: non-finite weight");
-  if (st) return fail(MG_ERR_STRUCTURE, "H: invalid CSR structure");
-  TRY(build_sell(c->H, n, rp.data(), cl.data(), v.data(), 1));
+  TRY(fetch_csr(c, F.n, F.n_global, H_row_ptr, H_col, H_w, nnz, 1, mem, false, 0, rp, cl, v, "H"));
+  if (F.dist) {
+    std::vector<int64_t> ghosts;
+    TRY(localize(F.row_begin, F.row_end, rp, cl, ghosts));
+    TRY(build_halo(c, c->hh, ghosts, F.bounds, F.row_begin, F.row_end));
+  } else {
+    c->hh = Halo();
+  }
+  TRY(build_sell(c->H, F.n, rp.data(), cl.data(), v.data(), 1));
   return MG_OK;
 }
 
@@ -828,7 +1182,7 @@ mg_status mg_spmv(mg_ctx c, int level, double alpha, const double *x, double bet
   if (!c->lv[level].A.set) return fail(MG_ERR_STATE, "level %d has no matrix", level);
   DeviceGuard dg(c->device);
   Tally tally(c);
-  return launch_apply<mgk::OP_SPMV>(c->bs(), c->lv[level].A, x, nullptr, nullptr, y, alpha, beta, c->stream);
+  return a_pass_spmv(c, level, alpha, x, beta, y);
 }
 
 mg_status mg_sweep(mg_ctx c, int level, const double *x, const double *b, double *x_out) {
@@ -837,8 +1191,7 @@ mg_status mg_sweep(mg_ctx c, int level, const double *x, const double *b, double
   DeviceGuard dg(c->device);
   Tally tally(c);
   TRY(finalize(c));
-  Level &L = c->lv[level];
-  return launch_apply<mgk::OP_SWEEP>(c->bs(), L.A, x, b, L.dinv.p, x_out, lv_omega(c, L), 0.0, c->stream);
+  return a_pass_sweep(c, level, x, b, x_out);
 }
 
 mg_status mg_residual(mg_ctx c, int level, const double *x, const double *b, double *r) {
@@ -847,7 +1200,7 @@ mg_status mg_residual(mg_ctx c, int level, const double *x, const double *b, dou
   if (!c->lv[level].A.set) return fail(MG_ERR_STATE, "level %d has no matrix", level);
   DeviceGuard dg(c->device);
   Tally tally(c);
-  return launch_apply<mgk::OP_RESID>(c->bs(), c->lv[level].A, x, b, nullptr, r, 1.0, 0.0, c->stream);
+  return a_pass_resid(c, level, x, b, r);
 }
 
 mg_status mg_smooth(mg_ctx c, int level, double *x, const double *b, int sweeps) {
@@ -866,7 +1219,7 @@ mg_status mg_restrict(mg_ctx c, int fine_level, const double *r_fine, double *d_
   if (!r_fine || !d_coarse) return fail(MG_ERR_INVALID_ARG, "NULL vector");
   DeviceGuard dg(c->device);
   Tally tally(c);
-  return launch_transfer(c->bs(), false, c->lv[fine_level].R, r_fine, d_coarse, c->stream);
+  return do_restrict(c, fine_level, r_fine, d_coarse);
 }
 
 mg_status mg_prolong_add(mg_ctx c, int fine_level, const double *y_coarse, double *x_fine) {
@@ -875,7 +1228,7 @@ mg_status mg_prolong_add(mg_ctx c, int fine_level, const double *y_coarse, doubl
   if (!y_coarse || !x_fine) return fail(MG_ERR_INVALID_ARG, "NULL vector");
   DeviceGuard dg(c->device);
   Tally tally(c);
-  return launch_transfer(c->bs(), true, c->lv[fine_level].P, y_coarse, x_fine, c->stream);
+  return do_prolong(c, fine_level, y_coarse, x_fine);
 }
 
 mg_status mg_coarse_solve(mg_ctx c, const double *d, double *y) {
@@ -895,8 +1248,10 @@ mg_status mg_apply_constraints(mg_ctx c, double *x) {
   Tally tally(c);
   TRY(finalize(c));
   Level &F = c->lv[c->L()];
-  TRY(launch_transfer(c->bs(), false, c->H, x, F.w.p, c->stream));
-  CU(cudaMemcpyAsync(x, F.w.p, size_t(F.n) * c->bs() * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  TRY(halo_exchange(c, c->hh, x));
+  TRY(launch_transfer(c->bs(), false, c->H, In{x, c->hh.active ? c->hh.ghost.p : nullptr, int(F.n)}, F.w.p,
+                      c->stream));
+  if (F.n) CU(cudaMemcpyAsync(x, F.w.p, size_t(F.n) * c->bs() * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   return MG_OK;
 }
 
@@ -906,7 +1261,7 @@ mg_status mg_dot(mg_ctx c, int level, const double *a, const double *b, double *
   DeviceGuard dg(c->device);
   Tally tally(c);
   TRY(finalize(c));
-  TRY(dev_dot(c, c->lv[level].n * c->bs(), a, b, c->scal.p, false));
+  TRY(dev_dot(c, c->lv[level].dist, c->lv[level].n * c->bs(), a, b, c->scal.p, false));
   CU(cudaMemcpyAsync(out_host, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   return MG_OK;
@@ -927,11 +1282,6 @@ int mgi_level_info(mgi_ctx c, int level, int64_t *n, int64_t *nnzb, int64_t *sel
   return 0;
 }
 
-mg_status mg_get_unique_id(unsigned char out[128]) {
-  if (!out) return fail(MG_ERR_INVALID_ARG, "NULL argument");
-  return fail(MG_ERR_NCCL, "multi-GPU support is not built into this library");
-}
-
 mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *opts, mg_solve_info *info) {
   TRY(check_ctx(c));
   if (!x || !b || !opts || x == b) return fail(MG_ERR_INVALID_ARG, "bad arguments");
@@ -939,20 +1289,21 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
   DeviceGuard dg(c->device);
   Tally tally(c);
   TRY(finalize(c));
-  Level &F = c->lv[c->L()];
+  const int Lf = c->L();
+  Level &F = c->lv[Lf];
+  const bool dist = F.dist;
   const int bs = c->bs();
   const int64_t N = F.n * bs;
   const double rtol = opts->rtol;
   int its = 0;
   double rel = 0.0;
   bool conv = false;
-  double *hst = nullptr;
   if (!c->gm_host) CU(cudaMallocHost(&c->gm_host, 16 * sizeof(double)));
-  hst = c->gm_host;
+  double *hst = c->gm_host;
 
   if (opts->method == MG_RICHARDSON) {
-    TRY(launch_apply<mgk::OP_RESID>(bs, F.A, x, b, nullptr, F.w.p, 1.0, 0.0, c->stream));
-    TRY(dev_dot(c, N, F.w.p, F.w.p, c->scal.p, true));
+    TRY(a_pass_resid(c, Lf, x, b, F.w.p));
+    TRY(dev_dot(c, dist, N, F.w.p, F.w.p, c->scal.p, true));
     CU(cudaMemcpyAsync(hst, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     const double r0 = hst[0];
@@ -961,8 +1312,8 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
     while (!conv && its < opts->max_iter) {
       TRY(run_vcycle(c, x, b, false));
       ++its;
-      TRY(launch_apply<mgk::OP_RESID>(bs, F.A, x, b, nullptr, F.w.p, 1.0, 0.0, c->stream));
-      TRY(dev_dot(c, N, F.w.p, F.w.p, c->scal.p, true));
+      TRY(a_pass_resid(c, Lf, x, b, F.w.p));
+      TRY(dev_dot(c, dist, N, F.w.p, F.w.p, c->scal.p, true));
       CU(cudaMemcpyAsync(hst, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CU(cudaStreamSynchronize(c->stream));
       if (!std::isfinite(hst[0])) return fail(MG_ERR_NONFINITE, "non-finite residual at iteration %d", its);
@@ -973,36 +1324,37 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
     const int m = std::max(1, std::min(opts->restart > 0 ? opts->restart : 30, 64));
     TRY(ensure_gmres(c, m));
     mgk::GmresDev g = c->gm;
+    const int ld = g.m + 1;  // leading dimension of the allocated Hessenberg
     double *V = c->gm_V.p, *Z = c->gm_Z.p;
-    TRY(launch_apply<mgk::OP_RESID>(bs, F.A, x, b, nullptr, V, 1.0, 0.0, c->stream));
-    TRY(dev_dot(c, N, V, V, g.beta0, true));
+    TRY(a_pass_resid(c, Lf, x, b, V));
+    TRY(dev_dot(c, dist, N, V, V, g.beta0, true));
     CU(cudaMemcpyAsync(g.beta, g.beta0, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     CU(cudaMemcpyAsync(hst, g.beta0, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     const double beta0 = hst[0];
     if (!std::isfinite(beta0)) return fail(MG_ERR_NONFINITE, "non-finite initial residual");
     if (beta0 == 0.0) conv = true;
-    const unsigned eg = unsigned(std::min<int64_t>((N + 255) / 256, 8 * c->n_sm));
+    const unsigned eg = unsigned(std::min<int64_t>(std::max<int64_t>(1, (N + 255) / 256), 8 * c->n_sm));
     while (!conv && its < opts->max_iter) {
       const int mm = std::min(m, opts->max_iter - its);
       ++g_tally, mgk::k_gmres_start<<<1, 32, 0, c->stream>>>(g);
       ++g_tally, mgk::k_scale_div<<<eg, 256, 0, c->stream>>>(N, V, g.beta, V);
-      TRY(check_launch());
+      TRY(check_launch("gmres start"));
       int k = 0;
       bool done = false;
       for (int j = 0; j < mm; ++j) {
         double *vj = V + size_t(j) * N, *zj = Z + size_t(j) * N, *w = V + size_t(j + 1) * N;
         TRY(run_vcycle(c, zj, vj, true));  // z_j = GMG(L, 0, v_j)
         ++its;
-        TRY(launch_apply<mgk::OP_SPMV>(bs, F.A, zj, nullptr, nullptr, w, 1.0, 0.0, c->stream));  // w = A z_j
-        double *hcol = g.H + size_t(j) * (g.m + 1);  // leading dimension of the allocated state
-        TRY(dev_dot(c, N, w, V, hcol + 0, false));  // h_0j = (w, v_0)
-        for (int i = 0; i < j; ++i)                 // w -= h_ij v_i ; h_{i+1,j} = (w, v_{i+1})
-          TRY(dev_axpy_dot(c, N, w, V + size_t(i) * N, hcol + i, V + size_t(i + 1) * N, hcol + i + 1));
-        TRY(dev_axpy_dot(c, N, w, vj, hcol + j, nullptr, hcol + j + 1));  // w -= h_jj v_j ; h_{j+1,j} = ||w||
+        TRY(a_pass_spmv(c, Lf, 1.0, zj, 0.0, w));  // w = A z_j
+        double *hcol = g.H + size_t(j) * ld;
+        TRY(dev_dot(c, dist, N, w, V, hcol + 0, false));  // h_0j = (w, v_0)
+        for (int i = 0; i < j; ++i)                       // w -= h_ij v_i ; h_{i+1,j} = (w, v_{i+1})
+          TRY(dev_axpy_dot(c, dist, N, w, V + size_t(i) * N, hcol + i, V + size_t(i + 1) * N, hcol + i + 1));
+        TRY(dev_axpy_dot(c, dist, N, w, vj, hcol + j, nullptr, hcol + j + 1));  // w -= h_jj v_j ; ||w||
         ++g_tally, mgk::k_givens<<<1, 32, 0, c->stream>>>(g, j, rtol);
         ++g_tally, mgk::k_scale_div<<<eg, 256, 0, c->stream>>>(N, w, g.hn + j, w);  // v_{j+1} = w / h_{j+1,j}
-        TRY(check_launch());
+        TRY(check_launch("givens"));
         CU(cudaMemcpyAsync(hst, g.out, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         CU(cudaStreamSynchronize(c->stream));
         k = j + 1;
@@ -1014,9 +1366,9 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
       }
       ++g_tally, mgk::k_backsolve<<<1, 32, 0, c->stream>>>(g, k);
       ++g_tally, mgk::k_update_x<<<eg, 256, 0, c->stream>>>(N, k, g.y, Z, x);
-      TRY(check_launch());
-      TRY(launch_apply<mgk::OP_RESID>(bs, F.A, x, b, nullptr, V, 1.0, 0.0, c->stream));
-      TRY(dev_dot(c, N, V, V, g.beta, true));
+      TRY(check_launch("gmres update"));
+      TRY(a_pass_resid(c, Lf, x, b, V));
+      TRY(dev_dot(c, dist, N, V, V, g.beta, true));
       CU(cudaMemcpyAsync(hst, g.beta, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CU(cudaStreamSynchronize(c->stream));
       rel = hst[0] / beta0;

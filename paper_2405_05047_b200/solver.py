@@ -11,18 +11,23 @@ class Multigrid:
     """levels: coarse -> fine sequence of objects with attributes
     n, row_ptr, col, val (BSR, val shaped (nnzb, bs, bs) or flat), and for
     l >= 1 P = (row_ptr, col, w) (n_l x n_{l-1}) and wpe.  H (optional):
-    (row_ptr, col, w) hanging matrix of the finest level."""
+    (row_ptr, col, w) hanging matrix of the finest level.
+    Multi-GPU: comm = (nranks, rank, id_bytes, transport) and levels carrying
+    n_global, row_begin, row_end (this rank's rows; columns global), e.g. from
+    problems.partition."""
 
     def __init__(self, levels, bs, *, omega=0.8, nu_pre=2, nu_post=2, coarse_mode=MG_COARSE_DIRECT,
-                 coarse_sweeps=20, use_graphs=True, device=0, stream=None, H=None, omegas=None):
+                 coarse_sweeps=20, use_graphs=True, device=0, stream=None, H=None, omegas=None, comm=None):
         self.bs = bs
         self.n = [int(L.n) for L in levels]
         self.ctx = mg_create(len(levels), bs, nu_pre=nu_pre, nu_post=nu_post, omega=omega,
                              coarse_mode=coarse_mode, coarse_sweeps=coarse_sweeps, use_graphs=use_graphs,
-                             device=device, stream=stream)
+                             device=device, stream=stream, comm=comm)
         try:
             for l, L in enumerate(levels):
-                mg_create_level(self.ctx, l, int(L.n))
+                ng = int(getattr(L, "n_global", L.n))
+                rb = int(getattr(L, "row_begin", 0))
+                mg_create_level(self.ctx, l, ng, rb, rb + int(L.n))
             for l, L in enumerate(levels):
                 val = L.val.reshape(-1) if hasattr(L.val, "reshape") else L.val
                 mg_set_matrix(self.ctx, l, L.row_ptr, L.col, val)

@@ -30,6 +30,7 @@ class LevelData:
     H: tuple                     # (rp, col, w) hanging matrix, n x n
     P: tuple | None = None       # (rp, col, w) prolongation from level-1, n x n_{l-1}
     wpe: int = 1                 # weights per P entry (1 or bs)
+    keys: np.ndarray | None = None  # (n,) sorted Morton keys at the finest lattice level (partitioning)
     mesh: M.Mesh | None = None
     nodes: M.NodeSet | None = None
 
@@ -125,7 +126,7 @@ def make_problem(name, root, box, steps, op: F.Operator, *, seed_index=0, omega=
         bnd = M.boundary_nodes(lm, nodes)
         cmask = np.repeat((nodes.hanging | bnd)[:, None], bs, axis=1)
         rp, col, val = F.assemble(lm, nodes, op, box, H)
-        lvl = LevelData(n, bs, rp, col, val, cmask, H, mesh=lm if keep_geometry else None,
+        lvl = LevelData(n, bs, rp, col, val, cmask, H, keys=nodes.keys, mesh=lm if keep_geometry else None,
                         nodes=nodes if keep_geometry else None)
         lvl._bnd = bnd
         lvl._nodes = nodes

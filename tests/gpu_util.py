@@ -21,10 +21,10 @@ def host(t):
 
 
 def build_gpu(levels, bs, *, omega=0.8, nu=(2, 2), coarse_mode=0, coarse_sweeps=20, use_graphs=True, H=None,
-              omegas=None):
+              omegas=None, **kw):
     from paper_2405_05047_b200 import Multigrid
     return Multigrid(levels, bs, omega=omega, nu_pre=nu[0], nu_post=nu[1], coarse_mode=coarse_mode,
-                     coarse_sweeps=coarse_sweeps, use_graphs=use_graphs, H=H, omegas=omegas)
+                     coarse_sweeps=coarse_sweeps, use_graphs=use_graphs, H=H, omegas=omegas, **kw)
 
 
 def build_oracle(levels, *, omega=0.8, nu=(2, 2), coarse="direct", coarse_sweeps=20, H=None):

@@ -195,22 +195,22 @@ def test_dense_inverse_vs_numpy():
 
 def test_validate_csr_errors():
     L = _lib()
-    L.mgi_validate_csr.argtypes = [ctypes.c_int64, ctypes.c_int64] + [ctypes.c_void_p] * 3 + [ctypes.c_int64,
-                                                                                               ctypes.c_int]
+    L.mgi_validate_csr.argtypes = [ctypes.c_int64, ctypes.c_int64] + [ctypes.c_void_p] * 3 + [
+        ctypes.c_int64, ctypes.c_int, ctypes.c_int64]
     rp = np.array([0, 2, 3], np.int64)
     col = np.array([0, 1, 1], np.int64)
     val = np.ones(3)
-    assert L.mgi_validate_csr(2, 2, _p(rp), _p(col), _p(val), 1, 1) == 0
+    assert L.mgi_validate_csr(2, 2, _p(rp), _p(col), _p(val), 1, 1, 0) == 0
     bad = np.array([1, 0, 1], np.int64)                       # unsorted
-    assert L.mgi_validate_csr(2, 2, _p(rp), _p(bad), _p(val), 1, 0) == -3
+    assert L.mgi_validate_csr(2, 2, _p(rp), _p(bad), _p(val), 1, 0, 0) == -3
     oob = np.array([0, 2, 1], np.int64)                       # out of range
-    assert L.mgi_validate_csr(2, 2, _p(rp), _p(oob), _p(val), 1, 0) == -3
+    assert L.mgi_validate_csr(2, 2, _p(rp), _p(oob), _p(val), 1, 0, 0) == -3
     nod = np.array([0, 1, 0], np.int64)                       # row 1 lacks its diagonal
-    assert L.mgi_validate_csr(2, 2, _p(rp), _p(nod), _p(val), 1, 1) == -3
+    assert L.mgi_validate_csr(2, 2, _p(rp), _p(nod), _p(val), 1, 1, 0) == -3
     rpb = np.array([0, 3, 2], np.int64)                       # decreasing row_ptr
-    assert L.mgi_validate_csr(2, 2, _p(rpb), _p(col), _p(val), 1, 0) == -3
+    assert L.mgi_validate_csr(2, 2, _p(rpb), _p(col), _p(val), 1, 0, 0) == -3
     nan = np.array([1.0, np.nan, 1.0])
-    assert L.mgi_validate_csr(2, 2, _p(rp), _p(col), _p(nan), 1, 1) == -4
+    assert L.mgi_validate_csr(2, 2, _p(rp), _p(col), _p(nan), 1, 1, 0) == -4
 
 
 def test_localize_columns_bruteforce():
@@ -218,14 +218,14 @@ def test_localize_columns_bruteforce():
     P = problem("c2_small")
     lv = P.levels[-1]
     n = lv.n
-    L.mgi_localize_columns.argtypes = [ctypes.c_int64, ctypes.c_int64] + [ctypes.c_void_p] * 5
+    L.mgi_localize_columns.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64] + [ctypes.c_void_p] * 5
     for r0, r1 in [(0, n // 3), (n // 3, 2 * n // 3), (2 * n // 3, n)]:
         rp = lv.row_ptr[r0:r1 + 1] - lv.row_ptr[r0]
         col = np.ascontiguousarray(lv.col[lv.row_ptr[r0]:lv.row_ptr[r1]])
         loc = np.zeros(len(col), np.int64)
         gh = np.zeros(len(col), np.int64)
         ng = ctypes.c_int64()
-        assert L.mgi_localize_columns(r0, r1, _p(np.ascontiguousarray(rp)), _p(col), _p(loc), _p(gh),
+        assert L.mgi_localize_columns(r1 - r0, r0, r1, _p(np.ascontiguousarray(rp)), _p(col), _p(loc), _p(gh),
                                       ctypes.byref(ng)) == 0
         ghosts = sorted({int(c) for c in col if c < r0 or c >= r1})
         assert list(gh[:ng.value]) == ghosts
