@@ -195,6 +195,8 @@ def run_ours(args):
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # host threads per rank for the generator's OpenMP helper
+        os.environ["OMP_NUM_THREADS"] = str(max(1, cpu_cores() // ws))
     dev = local
     torch.cuda.set_device(dev)
     import paper_2405_05047_b200 as mg
@@ -203,15 +205,34 @@ def run_ours(args):
     bs = P.bs
     stream = torch.cuda.current_stream()
     t = time.time()
-    solver = mg.Multigrid(P.levels, bs, omega=P.omega, nu_pre=P.nu_pre, nu_post=P.nu_post, H=P.fine.H,
-                          device=dev, stream=stream)
+    if ws > 1:
+        # row partition: nnz-balanced Morton splitters on every
+        # level; levels with < 16k rows per rank are replicated (agglomerated)
+        from problems.partition import partition
+        parts, extras, ranges = partition(P, ws, min_rows_per_rank=args.min_rows_per_rank, only_rank=rank)
+        uid = [mg.mg_get_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(uid, src=0)
+        levels, (b_np, H) = parts[rank], extras[rank]
+        del parts, extras
+        solver = mg.Multigrid(levels, bs, omega=P.omega, nu_pre=P.nu_pre, nu_post=P.nu_post, H=H, device=dev,
+                              stream=stream, use_graphs=not args.no_graphs,
+                              comm=(ws, rank, uid[0], mg.MG_TRANSPORT_NCCL))
+        n_global = P.n_dof
+        level_kinds = ["replicated" if all(r == (0, P.levels[l].n) for r in ranges[l]) else "distributed"
+                       for l in range(len(P.levels))]
+    else:
+        solver = mg.Multigrid(P.levels, bs, omega=P.omega, nu_pre=P.nu_pre, nu_post=P.nu_post, H=P.fine.H,
+                              device=dev, stream=stream, use_graphs=not args.no_graphs)
+        b_np = P.b
+        n_global = P.n_dof
+        level_kinds = ["single"] * len(P.levels)
     torch.cuda.synchronize()
     log(f"[bench] rank {rank}: library setup {time.time() - t:.1f}s")
     ctx = solver.ctx
     L = len(P.levels) - 1
     infos = [mg.level_info(ctx, l) for l in range(L + 1)]
-    N = P.n_dof
-    b_host = torch.from_numpy(P.b).pin_memory()
+    N = infos[L]["n"] * bs                      # this rank's fine DOFs
+    b_host = torch.from_numpy(np.ascontiguousarray(b_np)).pin_memory()
     b = b_host.cuda()
     x = torch.zeros(N, dtype=torch.float64, device="cuda")
     opts = dict(restart=30, max_iter=200, rtol=args.rtol)
@@ -251,14 +272,14 @@ def run_ours(args):
     launches = mg.launch_count(ctx) - l0
     clocks = sampler.stop()
     if ws > 1:
-        tt = torch.tensor([t_ms, float(total_its)], dtype=torch.float64, device="cuda")
-        tmax = tt.clone()
-        torch.distributed.all_reduce(tmax[:1], op=torch.distributed.ReduceOp.MAX)
+        tt = torch.tensor([t_ms, float(launches)], dtype=torch.float64, device="cuda")
+        tmax = tt[:1].clone()
+        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
         torch.distributed.all_reduce(tt[1:], op=torch.distributed.ReduceOp.SUM)
-        t_ms, total_its_all = float(tmax[0]), int(tt[1])
-    else:
-        total_its_all = total_its
-    value = total_its_all / (t_ms / 1e3)
+        t_ms, launches = float(tmax[0]), int(tt[1])
+    # every rank takes part in the same global V-cycles (strong scaling):
+    # units = global V-cycles of the whole job
+    value = total_its / (t_ms / 1e3)
 
     # ---------------- e2e: host buffers through the public API -----------------
     x_host = torch.empty(N, dtype=torch.float64).pin_memory()
@@ -279,7 +300,7 @@ def run_ours(args):
         tt = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(tt[0])
-    e2e_val = e2e_its * ws / (e2e_ms / 1e3)
+    e2e_val = e2e_its / (e2e_ms / 1e3)
 
     # ---------------- pure V-cycle rate (graph replay of mg_vcycle_zero) -------
     z = torch.zeros_like(x)
@@ -330,14 +351,17 @@ def run_ours(args):
         line = {
             "metric": "V-cycles/s", "value": value, "unit": "V-cycles/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.config], "n_dof": N, "n_dof_per_gpu": N,
-                       "levels": len(P.levels), "level_rows": [i["n"] for i in infos],
-                       "nnzb_fine": infos[L]["nnzb"], "parallelism": f"replicas{ws}" if ws > 1 else "single",
+            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config], "n_dof": n_global, "n_dof_per_gpu": N,
+                       "levels": len(P.levels), "level_rows_rank0": [i["n"] for i in infos],
+                       "level_kinds": level_kinds,
+                       "nnzb_fine_rank0": infos[L]["nnzb"],
+                       "parallelism": f"row-partition x{ws} (NCCL halos, allreduce dots, agglomeration)"
+                       if ws > 1 else "single GPU",
                        "solver": "GMRES(30) + V(2,2) block-Jacobi, rtol 1e-10, x0 = 0, then x <- Hx",
                        "l2": "operator 7 GB >> L2 126 MB (no flush needed)",
                        "iterations_per_solve": total_its // args.steps},
-            "dof_cycles_per_s": value * N,
+            "dof_cycles_per_s": value * n_global,
             "solve_ms": t_ms / args.steps,
             "vcycle_only": {"ms": vc_ms, "per_s": 1e3 / vc_ms, "alg_bytes": vc_bytes,
                             "alg_gbs": vc_bytes / (vc_ms / 1e3) / 1e9,
@@ -346,8 +370,8 @@ def run_ours(args):
                          "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "alg_bytes_per_launch": sweep_b, "avg_launch_ms": sw_ms},
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_val, "unit": "V-cycles/s", "h2d_bytes_per_step": 8 * N,
-                    "d2h_bytes_per_step": 8 * N},
+            "e2e": {"value": e2e_val, "unit": "V-cycles/s", "h2d_bytes_per_step": 8 * n_global,
+                    "d2h_bytes_per_step": 8 * n_global},
             "gpu_launches": launches,
             "clocks": clocks,
         }
@@ -366,6 +390,9 @@ def main():
     ap.add_argument("--config", choices=sorted(WORKLOADS), default="c3")
     ap.add_argument("--rtol", type=float, default=1e-10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--min-rows-per-rank", type=int, default=16384,
+                    help="multi-GPU: levels with fewer rows per rank are replicated (agglomerated)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("[bench] warmup raised to 3 (timing rules)")

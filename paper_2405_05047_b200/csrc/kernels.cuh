@@ -76,36 +76,66 @@ __device__ __forceinline__ const double *col_ptr(const double *x, const double *
   else return x + int64_t(c) * BS;
 }
 
-template <int BS, int OP, bool STREAM, bool HALO>
+// KS warps per slice ("split-k", for levels with few slices): warp `sub` of a
+// slice accumulates entries k = sub, sub + KS, ...; the partial sums are added
+// in shared memory in sub order.  KS = 1 keeps the CSR summation order.
+template <int BS, int KS>
+__device__ __forceinline__ bool combine_split(double (&acc)[BS], int wid, int sub, int lane) {
+  if constexpr (KS > 1) {
+    __shared__ double part[kWarpsPerCta][BS][32];
+    if (sub) {
+#pragma unroll
+      for (int r = 0; r < BS; ++r) part[wid][r][lane] = acc[r];
+    }
+    __syncthreads();
+    if (sub) return false;
+#pragma unroll
+    for (int k = 1; k < KS; ++k)
+#pragma unroll
+      for (int r = 0; r < BS; ++r) acc[r] += part[wid + k][r][lane];
+  }
+  return true;
+}
+
+template <int BS, int OP, bool STREAM, bool HALO, int KS>
 __global__ void __launch_bounds__(kCta) k_sell_apply(Sell A, const double *__restrict__ x,
                                                      const double *__restrict__ xg, int n_own,
                                                      const double *__restrict__ b,
                                                      const double *__restrict__ dinv,
                                                      double *__restrict__ out, double alpha, double beta) {
   constexpr int V = BS * BS;
-  const int lane = threadIdx.x & 31;
-  const int64_t s = (int64_t(blockIdx.x) * kCta + threadIdx.x) >> 5;
-  if (s >= A.n_slices) return;
-  const int64_t e0 = A.slice_ptr[s], e1 = A.slice_ptr[s + 1];
-  const int row = A.perm[s * 32 + lane];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int sub = KS == 1 ? 0 : wid % KS;
+  const int64_t s = int64_t(blockIdx.x) * (kWarpsPerCta / KS) + wid / KS;
+  const bool live = s < A.n_slices;
+  if (KS == 1 && !live) return;
   double acc[BS];
 #pragma unroll
   for (int r = 0; r < BS; ++r) acc[r] = 0.0;
+  int row = -1;
+  if (live) {
+    const int64_t e0 = A.slice_ptr[s], e1 = A.slice_ptr[s + 1];
+    row = A.perm[s * 32 + lane];
+    int64_t g = e0 + 32 * sub;
+    int cn = g < e1 ? ld_col<STREAM>(A.col + g + lane) : 0;  // column of the next entry (prefetched)
 #pragma unroll 4
-  for (int64_t g = e0; g < e1; g += 32) {
-    const int c = ld_col<STREAM>(A.col + g + lane);
-    double v[V];
-    load_entry<V, STREAM>(A.val + g * V, lane, v);
-    const double *xc = col_ptr<BS, HALO>(x, xg, n_own, c);
-    double xv[BS];
+    for (; g < e1; g += 32 * KS) {
+      const int c = cn;
+      if (g + 32 * KS < e1) cn = ld_col<STREAM>(A.col + g + 32 * KS + lane);
+      double v[V];
+      load_entry<V, STREAM>(A.val + g * V, lane, v);
+      const double *xc = col_ptr<BS, HALO>(x, xg, n_own, c);
+      double xv[BS];
 #pragma unroll
-    for (int q = 0; q < BS; ++q) xv[q] = __ldg(xc + q);
+      for (int q = 0; q < BS; ++q) xv[q] = __ldg(xc + q);
 #pragma unroll
-    for (int r = 0; r < BS; ++r)
+      for (int r = 0; r < BS; ++r)
 #pragma unroll
-      for (int q = 0; q < BS; ++q) acc[r] = fma(v[r * BS + q], xv[q], acc[r]);
+        for (int q = 0; q < BS; ++q) acc[r] = fma(v[r * BS + q], xv[q], acc[r]);
+    }
   }
-  if (row < 0) return;
+  if (!combine_split<BS, KS>(acc, wid, sub, lane)) return;
+  if (!live || row < 0) return;
   const int64_t o = int64_t(row) * BS;
   if constexpr (OP == OP_SPMV) {
 #pragma unroll
@@ -158,28 +188,37 @@ __global__ void __launch_bounds__(kCta) k_sweep0(int64_t n_slices, const int32_t
 // Transfer y = T x (ACCUM = 0) or y += T x (ACCUM = 1) with scalar weights
 // (WPE = 1) or per-component weights (WPE = BS): restriction R r (P:131,
 // P:337), prolongation x + P y, hanging interpolation H x.
-template <int BS, int WPE, bool ACCUM, bool STREAM, bool HALO>
+template <int BS, int WPE, bool ACCUM, bool STREAM, bool HALO, int KS>
 __global__ void __launch_bounds__(kCta) k_transfer(Sell T, const double *__restrict__ in,
                                                    const double *__restrict__ ing, int n_own,
                                                    double *__restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t s = (int64_t(blockIdx.x) * kCta + threadIdx.x) >> 5;
-  if (s >= T.n_slices) return;
-  const int64_t e0 = T.slice_ptr[s], e1 = T.slice_ptr[s + 1];
-  const int row = T.perm[s * 32 + lane];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int sub = KS == 1 ? 0 : wid % KS;
+  const int64_t s = int64_t(blockIdx.x) * (kWarpsPerCta / KS) + wid / KS;
+  const bool live = s < T.n_slices;
+  if (KS == 1 && !live) return;
   double acc[BS];
 #pragma unroll
   for (int q = 0; q < BS; ++q) acc[q] = 0.0;
+  int row = -1;
+  if (live) {
+    const int64_t e0 = T.slice_ptr[s], e1 = T.slice_ptr[s + 1];
+    row = T.perm[s * 32 + lane];
+    int64_t g = e0 + 32 * sub;
+    int cn = g < e1 ? ld_col<STREAM>(T.col + g + lane) : 0;
 #pragma unroll 4
-  for (int64_t g = e0; g < e1; g += 32) {
-    const int c = ld_col<STREAM>(T.col + g + lane);
-    double w[WPE];
-    load_entry<WPE, STREAM>(T.val + g * WPE, lane, w);
-    const double *xc = col_ptr<BS, HALO>(in, ing, n_own, c);
+    for (; g < e1; g += 32 * KS) {
+      const int c = cn;
+      if (g + 32 * KS < e1) cn = ld_col<STREAM>(T.col + g + 32 * KS + lane);
+      double w[WPE];
+      load_entry<WPE, STREAM>(T.val + g * WPE, lane, w);
+      const double *xc = col_ptr<BS, HALO>(in, ing, n_own, c);
 #pragma unroll
-    for (int q = 0; q < BS; ++q) acc[q] = fma(w[WPE == 1 ? 0 : q], __ldg(xc + q), acc[q]);
+      for (int q = 0; q < BS; ++q) acc[q] = fma(w[WPE == 1 ? 0 : q], __ldg(xc + q), acc[q]);
+    }
   }
-  if (row < 0) return;
+  if (!combine_split<BS, KS>(acc, wid, sub, lane)) return;
+  if (!live || row < 0) return;
   const int64_t o = int64_t(row) * BS;
 #pragma unroll
   for (int q = 0; q < BS; ++q) out[o + q] = ACCUM ? out[o + q] + acc[q] : acc[q];
@@ -252,20 +291,48 @@ __device__ __forceinline__ void grid_finish(double blocksum, double *part, unsig
 }
 
 // MODE 0: res = (a, b).  MODE 1 (MGS step): a -= (*h) * c; res = (a_new, b)
-// (b == nullptr => res = ||a_new||_2, written also to *res2).
-template <int MODE, bool SQRT>
+// (b == nullptr => res = ||a_new||_2 with SQRT).  VEC: all pointers 16-byte
+// aligned -> double2 loads/stores over the even part, the odd tail in thread 0.
+template <int MODE, bool SQRT, bool VEC>
 __global__ void __launch_bounds__(kRedThreads) k_reduce(int64_t n, double *__restrict__ a, const double *__restrict__ b,
                                                         const double *__restrict__ c, const double *__restrict__ h,
                                                         double *part, unsigned *ticket, double *res, double *res2) {
   __shared__ double sh[32];
   const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  double s = 0.0;
-  if constexpr (MODE == 0) {
-    for (int64_t i = tid; i < n; i += stride) s = fma(__ldg(a + i), __ldg(b + i), s);
-  } else {
-    const double hv = *h;
-    for (int64_t i = tid; i < n; i += stride) {
+  double s = 0.0, s2 = 0.0;
+  const double hv = MODE == 1 ? *h : 0.0;
+  int64_t i0 = 0;
+  if constexpr (VEC) {
+    const int64_t n2 = n / 2;
+    double2 *a2 = reinterpret_cast<double2 *>(a);
+    const double2 *b2 = reinterpret_cast<const double2 *>(b);
+    const double2 *c2 = reinterpret_cast<const double2 *>(c);
+#pragma unroll 2
+    for (int64_t i = tid; i < n2; i += stride) {
+      if constexpr (MODE == 0) {
+        const double2 x = __ldg(a2 + i), y = __ldg(b2 + i);
+        s = fma(x.x, y.x, s);
+        s2 = fma(x.y, y.y, s2);
+      } else {
+        double2 x = a2[i];
+        const double2 v = __ldg(c2 + i);
+        x.x = fma(-hv, v.x, x.x);
+        x.y = fma(-hv, v.y, x.y);
+        a2[i] = x;
+        const double2 y = b ? __ldg(b2 + i) : x;
+        s = fma(x.x, y.x, s);
+        s2 = fma(x.y, y.y, s2);
+      }
+    }
+    i0 = 2 * n2;
+    s += s2;
+    if (tid != 0) i0 = n;  // the odd tail element (if any) goes to thread 0
+  }
+  for (int64_t i = i0 + (VEC ? 0 : tid); i < n; i += (VEC ? 1 : stride)) {
+    if constexpr (MODE == 0) {
+      s = fma(__ldg(a + i), __ldg(b + i), s);
+    } else {
       const double v = fma(-hv, __ldg(c + i), a[i]);
       a[i] = v;
       s = fma(v, b ? __ldg(b + i) : v, s);
@@ -297,11 +364,19 @@ __global__ void k_gmres_start(GmresDev st) {
   }
 }
 
+// out = in / *den (in-place allowed); 16-byte aligned pointers, odd tail in thread 0
 __global__ void k_scale_div(int64_t n, const double *in, const double *den, double *out) {
   const double d = *den;
   if (d == 0.0) return;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
-    out[i] = in[i] / d;
+  const int64_t n2 = n / 2;
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int64_t i = tid; i < n2; i += int64_t(gridDim.x) * blockDim.x) {
+    double2 v = reinterpret_cast<const double2 *>(in)[i];
+    v.x /= d;
+    v.y /= d;
+    reinterpret_cast<double2 *>(out)[i] = v;
+  }
+  if (tid == 0 && (n & 1)) out[n - 1] = in[n - 1] / d;
 }
 
 // Apply the previous rotations to column j, form the new one, update g and
@@ -341,15 +416,15 @@ __global__ void k_backsolve(GmresDev st, int k) {
   }
 }
 
-// x += sum_{t<k} y_t Z_t  (Z: k vectors of length n, contiguous).
-__global__ void k_update_x(int64_t n, int k, const double *__restrict__ y, const double *__restrict__ Z,
+// x += sum_{t<k} y_t Z_t  (Z: k vectors of length n at stride ldz).
+__global__ void k_update_x(int64_t n, int k, const double *__restrict__ y, const double *__restrict__ Z, int64_t ldz,
                            double *__restrict__ x) {
   __shared__ double ys[64];
   if (threadIdx.x < k) ys[threadIdx.x] = y[threadIdx.x];
   __syncthreads();
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     double v = x[i];
-    for (int t = 0; t < k; ++t) v = fma(ys[t], __ldg(Z + int64_t(t) * n + i), v);
+    for (int t = 0; t < k; ++t) v = fma(ys[t], __ldg(Z + int64_t(t) * ldz + i), v);
     x[i] = v;
   }
 }

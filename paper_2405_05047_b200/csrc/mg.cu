@@ -119,6 +119,7 @@ struct SellOp {
   std::vector<int32_t> perm_host;
   int64_t n_rows = 0, n_slices = 0, n_entries = 0;
   int vpe = 0;
+  int ks = 1;  // warps per slice (split-k for small levels / long transfer rows)
   bool stream = false;
   bool set = false;
   mgk::Sell view() const { return mgk::Sell{slice_ptr.p, perm.p, col.p, val.p, n_slices}; }
@@ -228,6 +229,7 @@ struct mg_ctx_s {
   DevArray<unsigned> ticket;
   bool finalized = false;
   std::map<GraphKey, GraphExec> graphs;
+  std::map<std::tuple<int, double, int>, GraphExec> iter_graphs;  // GMRES iteration j (j, rtol, m)
   int64_t launches = 0;
   // GMRES workspace
   int gm_m = 0;
@@ -235,13 +237,18 @@ struct mg_ctx_s {
   double *gm_host = nullptr;  // pinned
   mgk::GmresDev gm{};
   ~mg_ctx_s() {
-    for (auto &kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+    clear_graphs();
     if (gm_host) cudaFreeHost(gm_host);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
-  void invalidate() {
+  void clear_graphs() {
     for (auto &kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+    for (auto &kv : iter_graphs) cudaGraphExecDestroy(kv.second.exec);
     graphs.clear();
+    iter_graphs.clear();
+  }
+  void invalidate() {
+    clear_graphs();
     finalized = false;
   }
   int bs() const { return cfg.block_size; }
@@ -265,8 +272,16 @@ struct DeviceGuard {
   }
 };
 
-inline unsigned grid_for_slices(int64_t n_slices) {
-  return unsigned((n_slices + mgk::kWarpsPerCta - 1) / mgk::kWarpsPerCta);
+inline unsigned grid_for_slices(int64_t n_slices, int ks = 1) {
+  const int per = mgk::kWarpsPerCta / ks;
+  return unsigned((n_slices + per - 1) / per);
+}
+
+// split-k factor of an A operator, decided on the GLOBAL level size so every
+// rank of a distributed solve (and the single-GPU solve) sums identically
+int ks_for_level(int64_t n_global) {
+  const int64_t slices = (n_global + 31) / 32;
+  return slices < 4096 ? 4 : slices < 32768 ? 2 : 1;
 }
 
 mg_status check_launch(const char *what = "kernel") {
@@ -286,12 +301,18 @@ struct In {
 template <int BS, int OP, bool HALO>
 void launch_apply_h(const SellOp &A, In in, const double *b, const double *dinv, double *out, double alpha,
                     double beta, cudaStream_t st) {
-  const unsigned g = grid_for_slices(A.n_slices);
-  if (A.stream)
-    ++g_tally, mgk::k_sell_apply<BS, OP, true, HALO>
+  const unsigned g = grid_for_slices(A.n_slices, A.ks);
+  if (A.ks == 4)
+    ++g_tally, mgk::k_sell_apply<BS, OP, false, HALO, 4>
+                   <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+  else if (A.ks == 2)
+    ++g_tally, mgk::k_sell_apply<BS, OP, true, HALO, 2>
+                   <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+  else if (A.stream)
+    ++g_tally, mgk::k_sell_apply<BS, OP, true, HALO, 1>
                    <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
   else
-    ++g_tally, mgk::k_sell_apply<BS, OP, false, HALO>
+    ++g_tally, mgk::k_sell_apply<BS, OP, false, HALO, 1>
                    <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
 }
 
@@ -337,12 +358,16 @@ mg_status launch_sweep0(int bs, const SellOp &A, const double *dinv, const doubl
 
 template <int BS, int WPE, bool ACC, bool HALO>
 void launch_transfer_h(const SellOp &T, In in, double *out, cudaStream_t st) {
-  const unsigned g = grid_for_slices(T.n_slices);
-  if (T.stream)
-    ++g_tally, mgk::k_transfer<BS, WPE, ACC, true, HALO><<<g, mgk::kCta, 0, st>>>(T.view(), in.x, in.xg, in.n_own, out);
+  const unsigned g = grid_for_slices(T.n_slices, T.ks);
+  if (T.ks > 1)
+    ++g_tally,
+        mgk::k_transfer<BS, WPE, ACC, true, HALO, 4><<<g, mgk::kCta, 0, st>>>(T.view(), in.x, in.xg, in.n_own, out);
+  else if (T.stream)
+    ++g_tally,
+        mgk::k_transfer<BS, WPE, ACC, true, HALO, 1><<<g, mgk::kCta, 0, st>>>(T.view(), in.x, in.xg, in.n_own, out);
   else
     ++g_tally,
-        mgk::k_transfer<BS, WPE, ACC, false, HALO><<<g, mgk::kCta, 0, st>>>(T.view(), in.x, in.xg, in.n_own, out);
+        mgk::k_transfer<BS, WPE, ACC, false, HALO, 1><<<g, mgk::kCta, 0, st>>>(T.view(), in.x, in.xg, in.n_own, out);
 }
 
 template <int BS, int WPE, bool ACC>
@@ -468,16 +493,24 @@ mg_status finish_reduce(mg_ctx_s *c, bool dist, double *res, bool sqrt_, double 
   return MG_OK;
 }
 
+inline bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <int MODE>
+void launch_reduce(mg_ctx_s *c, bool sq, bool vec, int64_t n, double *a, const double *b, const double *v,
+                   const double *h, double *res) {
+  const unsigned g = red_grid(c, n);
+  auto *P = c->red_part.p;
+  auto *T = c->ticket.p;
+  if (sq && vec) ++g_tally, mgk::k_reduce<MODE, true, true><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, b, v, h, P, T, res, nullptr);
+  else if (sq) ++g_tally, mgk::k_reduce<MODE, true, false><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, b, v, h, P, T, res, nullptr);
+  else if (vec) ++g_tally, mgk::k_reduce<MODE, false, true><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, b, v, h, P, T, res, nullptr);
+  else ++g_tally, mgk::k_reduce<MODE, false, false><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, b, v, h, P, T, res, nullptr);
+}
+
 // res (device) = (a, b) [sqrt] over the level's rows (all ranks if dist)
 mg_status dev_dot(mg_ctx_s *c, bool dist, int64_t n, const double *a, const double *b, double *res, bool sqrt_) {
-  const unsigned g = red_grid(c, n);
-  double *A = const_cast<double *>(a);
-  if (sqrt_ && !dist)
-    ++g_tally, mgk::k_reduce<0, true><<<g, mgk::kRedThreads, 0, c->stream>>>(n, A, b, nullptr, nullptr, c->red_part.p,
-                                                                               c->ticket.p, res, nullptr);
-  else
-    ++g_tally, mgk::k_reduce<0, false><<<g, mgk::kRedThreads, 0, c->stream>>>(n, A, b, nullptr, nullptr, c->red_part.p,
-                                                                                c->ticket.p, res, nullptr);
+  const bool vec = al16(a) && al16(b);
+  launch_reduce<0>(c, sqrt_ && !dist, vec, n, const_cast<double *>(a), b, nullptr, nullptr, res);
   TRY(check_launch("dot"));
   return finish_reduce(c, dist, res, sqrt_);
 }
@@ -485,13 +518,8 @@ mg_status dev_dot(mg_ctx_s *c, bool dist, int64_t n, const double *a, const doub
 // MGS step: a -= (*h) v ; res = (a, u), or ||a|| when u == nullptr
 mg_status dev_axpy_dot(mg_ctx_s *c, bool dist, int64_t n, double *a, const double *v, const double *h,
                        const double *u, double *res) {
-  const unsigned g = red_grid(c, n);
-  if (u || dist)
-    ++g_tally, mgk::k_reduce<1, false><<<g, mgk::kRedThreads, 0, c->stream>>>(
-                   n, a, u, v, h, c->red_part.p, c->ticket.p, res, nullptr);
-  else
-    ++g_tally, mgk::k_reduce<1, true><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, nullptr, v, h, c->red_part.p,
-                                                                               c->ticket.p, res, nullptr);
+  const bool vec = al16(a) && al16(v) && (!u || al16(u));
+  launch_reduce<1>(c, u == nullptr && !dist, vec, n, a, u, v, h, res);
   TRY(check_launch("axpy-dot"));
   return finish_reduce(c, dist, res, u == nullptr);
 }
@@ -770,36 +798,49 @@ mg_status vcycle_rec(mg_ctx_s *c, int l, double *x, const double *b, bool zero) 
   return smooth(c, l, x, b, lv_nu_post(c, L), false);  // Step 5
 }
 
+// Capture everything `body` enqueues on the context stream into a graph.
+template <class F>
+mg_status capture(mg_ctx_s *c, F &&body, GraphExec &out) {
+  cudaGraph_t graph = nullptr;
+  const int64_t t0 = g_tally;
+  CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  const mg_status st = body();
+  const int64_t captured = g_tally - t0;
+  g_tally = t0;
+  const cudaError_t ee = cudaStreamEndCapture(c->stream, &graph);
+  if (st != MG_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (ee != cudaSuccess) return fail(MG_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ee));
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) return fail(MG_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ie));
+  out = GraphExec{exec, captured};
+  return MG_OK;
+}
+
+mg_status launch_graph(mg_ctx_s *c, const GraphExec &g) {
+  CU(cudaGraphLaunch(g.exec, c->stream));
+  g_tally += g.kernels;
+  return MG_OK;
+}
+
 mg_status run_vcycle(mg_ctx_s *c, double *x, const double *b, bool zero) {
   if (!c->use_graphs()) return vcycle_rec(c, c->L(), x, b, zero);
   const GraphKey key{x, b, zero ? 1 : 0};
   auto it = c->graphs.find(key);
   if (it == c->graphs.end()) {
-    cudaGraph_t graph = nullptr;
-    const int64_t t0 = g_tally;
-    CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    const mg_status st = vcycle_rec(c, c->L(), x, b, zero);
-    const int64_t captured = g_tally - t0;
-    g_tally = t0;
-    const cudaError_t ee = cudaStreamEndCapture(c->stream, &graph);
-    if (st != MG_OK) {
-      if (graph) cudaGraphDestroy(graph);
-      return st;
-    }
-    if (ee != cudaSuccess) return fail(MG_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ee));
-    cudaGraphExec_t exec = nullptr;
-    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (ie != cudaSuccess) return fail(MG_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ie));
+    GraphExec ge;
+    TRY(capture(c, [&] { return vcycle_rec(c, c->L(), x, b, zero); }, ge));
     if (c->graphs.size() > 256) {
       for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
       c->graphs.clear();
     }
-    it = c->graphs.emplace(key, GraphExec{exec, captured}).first;
+    it = c->graphs.emplace(key, ge).first;
   }
-  CU(cudaGraphLaunch(it->second.exec, c->stream));
-  g_tally += it->second.kernels;
-  return MG_OK;
+  return launch_graph(c, it->second);
 }
 
 struct Tally {
@@ -823,11 +864,14 @@ mg_status check_level(mg_ctx_s *c, int level) {
   return MG_OK;
 }
 
+int64_t gm_stride(int64_t N) { return std::max<int64_t>(2, (N + 1) & ~int64_t(1)); }  // 16-byte aligned vectors
+
 mg_status ensure_gmres(mg_ctx_s *c, int m) {
   const int64_t N = c->lv[c->L()].n * c->bs();
   if (c->gm_m >= m && c->gm_V.p) return MG_OK;
-  TRY(c->gm_V.alloc(size_t(m + 1) * std::max<int64_t>(N, 1)));
-  TRY(c->gm_Z.alloc(size_t(m) * std::max<int64_t>(N, 1)));
+  c->clear_graphs();  // iteration graphs hold basis pointers
+  TRY(c->gm_V.alloc(size_t(m + 1) * gm_stride(N)));
+  TRY(c->gm_Z.alloc(size_t(m) * gm_stride(N)));
   const size_t ns = size_t(m + 1) * m + 6 * size_t(m + 1) + 16;
   TRY(c->gm_state.alloc(ns));
   CU(cudaMemset(c->gm_state.p, 0, ns * sizeof(double)));
@@ -998,6 +1042,7 @@ mg_status mg_set_matrix(mg_ctx c, int level, const int64_t *row_ptr, const int64
     TRY(build_halo(c, L.hx, ghosts, L.bounds, L.row_begin, L.row_end));
   }
   TRY(build_sell(L.A, L.n, rp.data(), cl.data(), v.data(), V));
+  L.A.ks = ks_for_level(L.n_global);
   L.nnzb = nnzb;
   L.dinv_ready = false;  // (re)built at finalize; a user D^-1 is re-sliced with the new permutation
   if (level == 0 && !L.dist) {
@@ -1098,6 +1143,7 @@ mg_status mg_set_transfer(mg_ctx c, int fine_level, const int64_t *row_ptr, cons
     }
   }
   TRY(build_sell(L.R, L.r_rows, rrp.data(), rcl.data(), rv.data(), wpe));
+  L.R.ks = 4;  // R rows gather 9-27+ fine entries: split them over 4 warps
   // ---- P: columns are coarse rows ------------------------------------------
   if (C.dist) {
     std::vector<int64_t> ghosts;
@@ -1326,6 +1372,7 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
     mgk::GmresDev g = c->gm;
     const int ld = g.m + 1;  // leading dimension of the allocated Hessenberg
     double *V = c->gm_V.p, *Z = c->gm_Z.p;
+    const int64_t NS = gm_stride(N);
     TRY(a_pass_resid(c, Lf, x, b, V));
     TRY(dev_dot(c, dist, N, V, V, g.beta0, true));
     CU(cudaMemcpyAsync(g.beta, g.beta0, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
@@ -1343,19 +1390,36 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
       int k = 0;
       bool done = false;
       for (int j = 0; j < mm; ++j) {
-        double *vj = V + size_t(j) * N, *zj = Z + size_t(j) * N, *w = V + size_t(j + 1) * N;
-        TRY(run_vcycle(c, zj, vj, true));  // z_j = GMG(L, 0, v_j)
+        // one Arnoldi step: a single CUDA graph per j (V-cycle, SpMV, MGS,
+        // Givens, scaling, flag copy-out), then one host sync
+        auto step = [&]() -> mg_status {
+          double *vj = V + size_t(j) * NS, *zj = Z + size_t(j) * NS, *w = V + size_t(j + 1) * NS;
+          TRY(vcycle_rec(c, Lf, zj, vj, true));      // z_j = GMG(L, 0, v_j)
+          TRY(a_pass_spmv(c, Lf, 1.0, zj, 0.0, w));  // w = A z_j
+          double *hcol = g.H + size_t(j) * ld;
+          TRY(dev_dot(c, dist, N, w, V, hcol + 0, false));  // h_0j = (w, v_0)
+          for (int i = 0; i < j; ++i)                       // w -= h_ij v_i ; h_{i+1,j} = (w, v_{i+1})
+            TRY(dev_axpy_dot(c, dist, N, w, V + size_t(i) * NS, hcol + i, V + size_t(i + 1) * NS, hcol + i + 1));
+          TRY(dev_axpy_dot(c, dist, N, w, vj, hcol + j, nullptr, hcol + j + 1));  // w -= h_jj v_j ; ||w||
+          ++g_tally, mgk::k_givens<<<1, 32, 0, c->stream>>>(g, j, rtol);
+          ++g_tally, mgk::k_scale_div<<<eg, 256, 0, c->stream>>>(N, w, g.hn + j, w);  // v_{j+1} = w / h_{j+1,j}
+          TRY(check_launch("givens"));
+          CU(cudaMemcpyAsync(hst, g.out, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+          return MG_OK;
+        };
+        if (c->use_graphs()) {
+          const auto key = std::make_tuple(j, rtol, g.m);
+          auto it = c->iter_graphs.find(key);
+          if (it == c->iter_graphs.end()) {
+            GraphExec ge;
+            TRY(capture(c, step, ge));
+            it = c->iter_graphs.emplace(key, ge).first;
+          }
+          TRY(launch_graph(c, it->second));
+        } else {
+          TRY(step());
+        }
         ++its;
-        TRY(a_pass_spmv(c, Lf, 1.0, zj, 0.0, w));  // w = A z_j
-        double *hcol = g.H + size_t(j) * ld;
-        TRY(dev_dot(c, dist, N, w, V, hcol + 0, false));  // h_0j = (w, v_0)
-        for (int i = 0; i < j; ++i)                       // w -= h_ij v_i ; h_{i+1,j} = (w, v_{i+1})
-          TRY(dev_axpy_dot(c, dist, N, w, V + size_t(i) * N, hcol + i, V + size_t(i + 1) * N, hcol + i + 1));
-        TRY(dev_axpy_dot(c, dist, N, w, vj, hcol + j, nullptr, hcol + j + 1));  // w -= h_jj v_j ; ||w||
-        ++g_tally, mgk::k_givens<<<1, 32, 0, c->stream>>>(g, j, rtol);
-        ++g_tally, mgk::k_scale_div<<<eg, 256, 0, c->stream>>>(N, w, g.hn + j, w);  // v_{j+1} = w / h_{j+1,j}
-        TRY(check_launch("givens"));
-        CU(cudaMemcpyAsync(hst, g.out, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         CU(cudaStreamSynchronize(c->stream));
         k = j + 1;
         if (!std::isfinite(hst[0])) return fail(MG_ERR_NONFINITE, "non-finite GMRES residual estimate");
@@ -1365,7 +1429,7 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
         }
       }
       ++g_tally, mgk::k_backsolve<<<1, 32, 0, c->stream>>>(g, k);
-      ++g_tally, mgk::k_update_x<<<eg, 256, 0, c->stream>>>(N, k, g.y, Z, x);
+      ++g_tally, mgk::k_update_x<<<eg, 256, 0, c->stream>>>(N, k, g.y, Z, NS, x);
       TRY(check_launch("gmres update"));
       TRY(a_pass_resid(c, Lf, x, b, V));
       TRY(dev_dot(c, dist, N, V, V, g.beta, true));

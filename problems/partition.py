@@ -67,13 +67,18 @@ def splitters(problem, nranks, min_rows_per_rank=64, replicate_level0=True):
     return out[::-1]
 
 
-def partition(problem, nranks, min_rows_per_rank=64, replicate_level0=True):
-    """Returns (per-rank list of RankLevel lists, per-rank (b_local, H_local), ranges)."""
+def partition(problem, nranks, min_rows_per_rank=64, replicate_level0=True, only_rank=None):
+    """Returns (per-rank list of RankLevel lists, per-rank (b_local, H_local), ranges).
+    only_rank: build the data of that rank only (the other entries are None)."""
     ranges = splitters(problem, nranks, min_rows_per_rank, replicate_level0)
     bs = problem.bs
     ranks = []
     extras = []
     for r in range(nranks):
+        if only_rank is not None and r != only_rank:
+            ranks.append(None)
+            extras.append(None)
+            continue
         lv = []
         for l, L in enumerate(problem.levels):
             r0, r1 = ranges[l][r]
