@@ -117,6 +117,7 @@ def make_problem(name, root, box, steps, op: F.Operator, *, seed_index=0, omega=
     meshes = M.hierarchy(fine_mesh)
     R = fine_mesh.max_level
     bs = op.bs
+    vel_only = op.name == "stokes"      # Dirichlet on velocity only (reading Z23)
     levels = []
     prev = None
     for lm in meshes:
@@ -125,15 +126,28 @@ def make_problem(name, root, box, steps, op: F.Operator, *, seed_index=0, omega=
         n = len(nodes.keys)
         bnd = M.boundary_nodes(lm, nodes)
         cmask = np.repeat((nodes.hanging | bnd)[:, None], bs, axis=1)
+        if vel_only:
+            cmask[:, 0] = nodes.hanging
         rp, col, val = F.assemble(lm, nodes, op, box, H)
         lvl = LevelData(n, bs, rp, col, val, cmask, H, keys=nodes.keys, mesh=lm if keep_geometry else None,
                         nodes=nodes if keep_geometry else None)
         lvl._bnd = bnd
         lvl._nodes = nodes
         lvl._mesh = lm
-        if prev is not None:
+        if prev is not None and not vel_only:
             lvl.P = F.prolongation(prev._mesh, prev._nodes, prev.H, ~prev.cmask[:, 0],
                                    lm, nodes, ~cmask[:, 0])
+        elif prev is not None:
+            # per-component Pi: weights_per_entry = bs (pressure free at the boundary)
+            prp, pcol, pw = F.prolongation(prev._mesh, prev._nodes, prev.H, ~prev._nodes.hanging,
+                                           lm, nodes, ~nodes.hanging)
+            rows = F.row_of(prp)
+            wc = pw[:, None] * (~cmask[rows]) * (~prev.cmask[pcol])
+            keep = np.any(wc != 0.0, axis=1)
+            rp2 = np.zeros(n + 1, np.int64)
+            np.add.at(rp2, rows[keep] + 1, 1)
+            lvl.P = (np.cumsum(rp2), pcol[keep], np.ascontiguousarray(wc[keep]).reshape(-1))
+            lvl.wpe = bs
         levels.append(lvl)
         prev = lvl
     # constraints on every level: identity rows at hanging/Dirichlet DOFs
@@ -169,6 +183,18 @@ def make_problem(name, root, box, steps, op: F.Operator, *, seed_index=0, omega=
 # --------------------------------------------------------------------------
 
 TD = dict(lam=0.01, b=(0.0, -1.0), dt=0.02)
+STOKES2 = dict(nu=1e-3, dt=1e-2, eps=1e-2, alpha=1.0)          # reading Z23 (C4)
+STOKES3 = dict(nu=1e-3, dt=1e-4, eps=1e-2, alpha=1.0)          # P:595, reading Z23 (C5)
+
+
+def lid(dim, bs):
+    """Cavity velocity Dirichlet data: u_1 = 1 on the moving lid x_{d-1} = 0
+    (the face the band rule refines toward), 0 elsewhere; pressure free."""
+    def g(xyz):
+        out = np.zeros((len(xyz), bs))
+        out[:, 1] = (xyz[:, dim - 1] == 0.0).astype(float)
+        return out
+    return g
 ELAST = dict(lam=8e4, mu=2e4, dt=0.025)                         # P:439, P:480
 
 
@@ -195,6 +221,22 @@ CONFIGS = {
 }
 
 
+CONFIGS.update({
+    # C4: 2D NS-shaped generalised Stokes, 3x3 blocks (p, u, v), lid cavity, band toward the lid
+    "c4": ((32, 32), (1.0, 1.0), [("band", [1], 20)] * 6, F.Operator("stokes", 3, False, STOKES2), 0.8, 3),
+    "c4_small": ((8, 8), (1.0, 1.0), [("band", [1], 2)] * 3, F.Operator("stokes", 3, False, STOKES2), 0.8, 3),
+    # C5: 3D NS-shaped, 4x4 blocks (p, u, v, w) on (0,1)x(0,1)x(0,2), root (4,4,8), uniform refinement
+    # omega: 0.8 diverges on the adaptive 3D case (rho ~ 1.2); 0.6 gives h-independent
+    # GMRES counts (25-27 at 1.4k..70.8k nodes), tests/test_oracle_stokes.py
+    "c5": ((4, 4, 8), (1.0, 1.0, 2.0), [("uniform",)] * 5, F.Operator("stokes", 4, False, STOKES3), 0.6, 4),
+    "c5_small": ((2, 2, 4), (1.0, 1.0, 2.0), [("uniform",)] * 2, F.Operator("stokes", 4, False, STOKES3), 0.6, 4),
+    "c5_mid": ((2, 2, 4), (1.0, 1.0, 2.0), [("band", [2], 1)] * 2 + [("uniform",)],
+               F.Operator("stokes", 4, False, STOKES3), 0.6, 4),
+})
+
+
 def build(name: str, **kw) -> Problem:
     root, box, steps, op, omega, si = CONFIGS[name]
+    if op.name == "stokes" and "g_fun" not in kw:
+        kw["g_fun"] = lid(len(root), op.bs)
     return make_problem(name, root, box, steps, op, seed_index=si, omega=omega, **kw)

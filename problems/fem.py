@@ -149,6 +149,37 @@ def element_terms(op: Operator, dim: int, h: np.ndarray):
                     T2.append(_sym(T[ia] + T[ib]))
                 S2.append(S[ia])
         T, S = T2, S2
+    elif op.name == "stokes":
+        # Generalised Stokes, equal-order Q1, unknowns (p, u_1..u_d) node-major
+        # (P:108), PSPG stabilisation + pressure-mass regularisation (reading Z23):
+        #   (u/dt, v) + nu (grad u, grad v) - (p, div v) + (div u, q)
+        #   + sum_T delta_T (grad p, grad q)_T + eps (p, q),
+        #   delta_T = alpha (1/dt + nu/h_T^2)^-1.
+        bs = dim + 1
+        nu, dt = p["nu"], p["dt"]
+        eps, alpha = p.get("eps", 1e-2), p.get("alpha", 1.0)
+        hT = h.max(axis=1)
+        delta = alpha / (1.0 / dt + nu / hT ** 2)
+
+        def blk(A, r, c):
+            Tb = np.zeros((nloc, bs, nloc, bs))
+            Tb[:, r, :, c] = A
+            return Tb.reshape(nloc * bs, nloc * bs)
+
+        T.append(sum(blk(Mref, c, c) for c in range(1, bs)))
+        S.append(vol / dt)
+        for a in range(dim):
+            T.append(sum(blk(G[a, a], c, c) for c in range(1, bs)))
+            S.append(nu * vol / h[:, a] ** 2)
+            T.append(blk(G[a, a], 0, 0))
+            S.append(delta * vol / h[:, a] ** 2)
+        T.append(blk(Mref, 0, 0))
+        S.append(eps * vol)
+        for a in range(dim):
+            # velocity row (i, 1+a), pressure col j: -int phi_j d_a phi_i ;
+            # pressure row i, velocity col (j, 1+a): +int phi_i d_a phi_j
+            T.append(blk(-C[a].T, 1 + a, 0) + blk(C[a], 0, 1 + a))
+            S.append(vol / h[:, a])
     else:
         raise ValueError(op.name)
     return np.ascontiguousarray(np.stack(T)), np.ascontiguousarray(np.stack(S, axis=1))

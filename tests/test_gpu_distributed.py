@@ -61,7 +61,7 @@ def gather(vals, ranges_fine, bs):
     return np.concatenate([v.reshape(-1, bs) for v in vals]).reshape(-1)
 
 
-CASES = [("c3_small", 2), ("c3_small", 3), ("c2_small", 2), ("c3_mid", 4)]
+CASES = [("c3_small", 2), ("c3_small", 3), ("c2_small", 2), ("c3_mid", 4), ("c4_small", 2), ("c5_mid", 3)]
 
 
 @pytest.mark.parametrize("name,P", CASES)
@@ -112,7 +112,7 @@ def test_distributed_vcycle_bitwise_equals_single_gpu(name, P):
         g.close()
 
 
-@pytest.mark.parametrize("name,P", [("c3_small", 2), ("c2_small", 3)])
+@pytest.mark.parametrize("name,P", [("c3_small", 2), ("c2_small", 3), ("c4_small", 2)])
 def test_distributed_per_op(name, P):
     import paper_2405_05047_b200 as m
     Pr, parts, extras, ranges, mgs = dist_mg(name, P)
@@ -179,7 +179,7 @@ def test_distributed_per_op(name, P):
     assert np.array_equal(np.concatenate([o["H"] for o in out]), host(hx))
 
 
-@pytest.mark.parametrize("name,P", [("c3_small", 2), ("c3_mid", 4), ("c2_small", 3)])
+@pytest.mark.parametrize("name,P", [("c3_small", 2), ("c3_mid", 4), ("c2_small", 3), ("c5_mid", 2)])
 def test_distributed_gmres_matches(name, P):
     import paper_2405_05047_b200 as m
     Pr, parts, extras, ranges, mgs = dist_mg(name, P)
