@@ -107,22 +107,23 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def level_bytes(info, bs, zero):
-    """Algorithmic bytes of one V(2,2) on one level; info from mgi_level_info."""
+def level_bytes(info, bs, zero, vb=8):
+    """Algorithmic bytes of one V(2,2) on one level; info from mgi_level_info.
+    vb: bytes per stored matrix value (8 fp64, 4 in the mixed-precision V-cycle)."""
     n, z = info["n"], info["nnzb"]
-    a_stream = z * (8 * bs * bs + 4) + 8 * (n + 1)
+    a_stream = z * (vb * bs * bs + 4) + 8 * (n + 1)
     sweep = a_stream + 8 * bs * n * 3 + 8 * bs * bs * n
     sweep0 = 16 * bs * n + 8 * bs * bs * n
     resid = a_stream + 24 * bs * n
     return sweep, sweep0, resid
 
 
-def vcycle_bytes(infos, bs, nu=(2, 2), zero=True, coarse_direct=True):
+def vcycle_bytes(infos, bs, nu=(2, 2), zero=True, coarse_direct=True, vb=8):
     """Algorithmic bytes of one V-cycle (fine level from zero guess if zero)."""
     total = 0
     L = len(infos) - 1
     for l in range(L, 0, -1):
-        sweep, sweep0, resid = level_bytes(infos[l], bs, zero)
+        sweep, sweep0, resid = level_bytes(infos[l], bs, zero, vb)
         first_zero = zero or l < L
         total += (sweep0 + (nu[0] - 1) * sweep) if first_zero else nu[0] * sweep
         total += resid + nu[1] * sweep
@@ -207,6 +208,8 @@ def run_ours(args):
 
     P = build_problem(args.config)
     bs = P.bs
+    prec = mg.MG_PREC_MIXED if args.precision == "mixed" else mg.MG_PREC_FP64
+    vb = 4 if args.precision == "mixed" else 8
     stream = torch.cuda.current_stream()
     t = time.time()
     if ws > 1:
@@ -219,14 +222,14 @@ def run_ours(args):
         levels, (b_np, H) = parts[rank], extras[rank]
         del parts, extras
         solver = mg.Multigrid(levels, bs, omega=P.omega, nu_pre=P.nu_pre, nu_post=P.nu_post, H=H, device=dev,
-                              stream=stream, use_graphs=not args.no_graphs,
+                              stream=stream, use_graphs=not args.no_graphs, precision=prec,
                               comm=(ws, rank, uid[0], mg.MG_TRANSPORT_NCCL))
         n_global = P.n_dof
         level_kinds = ["replicated" if all(r == (0, P.levels[l].n) for r in ranges[l]) else "distributed"
                        for l in range(len(P.levels))]
     else:
         solver = mg.Multigrid(P.levels, bs, omega=P.omega, nu_pre=P.nu_pre, nu_post=P.nu_post, H=P.fine.H,
-                              device=dev, stream=stream, use_graphs=not args.no_graphs)
+                              device=dev, stream=stream, use_graphs=not args.no_graphs, precision=prec)
         b_np = P.b
         n_global = P.n_dof
         level_kinds = ["single"] * len(P.levels)
@@ -318,7 +321,7 @@ def run_ours(args):
     e1.record(stream)
     torch.cuda.synchronize()
     vc_ms = e0.elapsed_time(e1) / nv
-    vc_bytes = vcycle_bytes(infos, bs, (P.nu_pre, P.nu_post), zero=True)
+    vc_bytes = vcycle_bytes(infos, bs, (P.nu_pre, P.nu_post), zero=True, vb=vb)
 
     # ---------------- dominant kernel: fine-level fused block-Jacobi sweep -----
     peak, peak_src = measured_peaks()
@@ -335,7 +338,7 @@ def run_ours(args):
         c.record(stream)
     torch.cuda.synchronize()
     sw_ms = sum(a.elapsed_time(c) for a, c in evs) / ns
-    sweep_b, _, _ = level_bytes(infos[L], bs, False)
+    sweep_b, _, _ = level_bytes(infos[L], bs, False, vb)
     achieved = sweep_b / (sw_ms / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -363,6 +366,9 @@ def run_ours(args):
                        "parallelism": f"row-partition x{ws} (NCCL halos, allreduce dots, agglomeration)"
                        if ws > 1 else "single GPU",
                        "solver": "GMRES(30) + V(2,2) block-Jacobi, rtol 1e-10, x0 = 0, then x <- Hx",
+                       "precision": ("fp64" if vb == 8 else
+                                     "mixed: V-cycle A_l stored fp32 (fp64 vectors/accumulation/D^-1/transfers), "
+                                     "fp64 GMRES operator; true fp64 residual 1e-10"),
                        "l2": (f"finest operator {infos[L]['nnzb'] * (8 * bs * bs + 4) / 1e9:.2f} GB vs L2 126 MB: "
                               + ("no flush needed" if infos[L]["nnzb"] * (8 * bs * bs + 4) > 1e9
                                  else "partly L2-resident (small config)")),
@@ -398,6 +404,8 @@ def main():
     ap.add_argument("--rtol", type=float, default=1e-10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--precision", choices=["fp64", "mixed"], default="fp64",
+                    help="mixed: fp32-stored V-cycle operators inside fp64 GMRES (SURVEY N1)")
     ap.add_argument("--min-rows-per-rank", type=int, default=16384,
                     help="multi-GPU: levels with fewer rows per rank are replicated (agglomerated)")
     args = ap.parse_args()

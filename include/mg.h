@@ -79,13 +79,22 @@ enum { MG_MEM_HOST = 0, MG_MEM_DEVICE = 1 };
 enum { MG_TRANSPORT_NCCL = 0, MG_TRANSPORT_LOCAL = 1 };
 enum { MG_COARSE_DIRECT = 0, MG_COARSE_SMOOTH = 1 };
 enum { MG_GMRES = 0, MG_RICHARDSON = 1 };
+enum { MG_PREC_FP64 = 0, MG_PREC_MIXED = 1 };
 
 /* Global multigrid configuration (SPEC MgConfig; readings Z1-Z3).
  * omega: damping of the block-Jacobi smoother ("a damping factor");
  * nu_pre / nu_post: smoothing steps (Alg. gmg Steps 1 and 5);
  * coarse_mode: MG_COARSE_DIRECT = exact A_0^{-1} applied as a dense
  *   inverse, MG_COARSE_SMOOTH = coarse_sweeps smoothing steps from 0;
- * use_graphs: capture V-cycles into CUDA graphs (1) or launch eagerly (0). */
+ * use_graphs: capture V-cycles into CUDA graphs (1) or launch eagerly (0);
+ * precision: MG_PREC_FP64 (everything fp64), or MG_PREC_MIXED -- the
+ *   V-cycle's operators A_l are stored rounded to fp32 (fp64 vectors, fp64
+ *   accumulation, fp64 D^-1 / transfers / coarse inverse) while the finest
+ *   level also keeps its fp64 A for the Krylov operator, residuals and
+ *   mg_spmv / mg_residual ("single precision ... effectively
+ *   doubles the arithmetic intensity").  MG iteration then runs as defect
+ *   correction x += GMG(L, 0, b - A x) so both methods converge to the fp64
+ *   solution. */
 typedef struct {
   int n_levels;
   int block_size;
@@ -95,6 +104,7 @@ typedef struct {
   int coarse_mode;
   int coarse_sweeps;
   int use_graphs;
+  int precision;
 } mg_config;
 
 /* Multi-GPU communicator description: NULL (or nranks == 1) => single GPU.

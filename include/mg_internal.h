@@ -45,6 +45,14 @@ int mgi_sell_fill(int64_t n, const int64_t *row_ptr, const int64_t *col_in, cons
                   int vpe, int sigma, int64_t *slice_ptr, int32_t *perm, int32_t *col,
                   double *val);
 
+/* Same layout with fp32 values (mixed-precision V-cycle operators):
+ * 4-float chunks -- element 4j+t (j < vpe/4) at (e - lane)*vpe + 128*j + 4*lane + t
+ * -- then the vpe % 4 remaining elements as planes at (e - lane)*vpe + 128*(vpe/4)
+ * + 32*k + lane.  Values are rounded to nearest fp32. */
+int mgi_sell_fill_f32(int64_t n, const int64_t *row_ptr, const int64_t *col_in, const double *val_in,
+                      int vpe, int sigma, int64_t *slice_ptr, int32_t *perm, int32_t *col,
+                      float *val);
+
 /* Stable counting-sort transpose (R = P^T): out_row_ptr[n_cols+1],
  * out_col[nnz], out_w[nnz*wpe]; entries of each output row in ascending
  * input-row order. */

@@ -127,13 +127,16 @@ def richardson(h: MgHierarchy, b, x0=None, rtol=1e-10, max_iter=100):
     return x, max_iter, hist
 
 
-def gmres(h: MgHierarchy, b, x0=None, rtol=1e-10, restart=30, max_iter=200, precondition=True):
+def gmres(h: MgHierarchy, b, x0=None, rtol=1e-10, restart=30, max_iter=200, precondition=True, op=None):
     """Right-preconditioned GMRES(m) with modified Gram-Schmidt and Givens
     rotations (Saad §6.5.3 as cited at P:346; stored-Z form, reading O8/Z5).
     The iteration count is the number of preconditioner applications.
+    op: optional outer operator (an MgLevel-like object with n, bs, rp, col,
+    val) when the preconditioning hierarchy h approximates it (mixed-precision
+    V-cycle); default the finest level of h.
     Returns x, iterations, history of |g_{j+1}| / beta_0 estimates, true rel. residual."""
     Lf = len(h.levels) - 1
-    F = h.levels[-1]
+    F = h.levels[-1] if op is None else op
     N = F.n * F.bs
     x = np.zeros(N) if x0 is None else np.array(x0, np.float64)
     r = residual(F.n, F.bs, F.rp, F.col, F.val, x, b)
@@ -158,7 +161,7 @@ def gmres(h: MgHierarchy, b, x0=None, rtol=1e-10, restart=30, max_iter=200, prec
         for j in range(m):
             Z[j] = vcycle(h, Lf, np.zeros(N), V[j]) if precondition else V[j]
             its += 1
-            w = h.A(Lf, Z[j])
+            w = spmv(F.n, F.bs, F.rp, F.col, F.val, Z[j])
             for i in range(j + 1):                       # modified Gram-Schmidt
                 Hh[i, j] = dot(w, V[i])
                 w = w - Hh[i, j] * V[i]

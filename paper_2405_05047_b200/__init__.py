@@ -31,6 +31,7 @@ MG_MEM_HOST, MG_MEM_DEVICE = 0, 1
 MG_COARSE_DIRECT, MG_COARSE_SMOOTH = 0, 1
 MG_GMRES, MG_RICHARDSON = 0, 1
 MG_TRANSPORT_NCCL, MG_TRANSPORT_LOCAL = 0, 1
+MG_PREC_FP64, MG_PREC_MIXED = 0, 1
 
 STATUS_NAMES = {0: "MG_OK", 1: "MG_NOT_CONVERGED", -1: "MG_ERR_INVALID_ARG", -2: "MG_ERR_DIMENSION",
                 -3: "MG_ERR_STRUCTURE", -4: "MG_ERR_NONFINITE", -5: "MG_ERR_SINGULAR", -6: "MG_ERR_STATE",
@@ -40,7 +41,7 @@ STATUS_NAMES = {0: "MG_OK", 1: "MG_NOT_CONVERGED", -1: "MG_ERR_INVALID_ARG", -2:
 class mg_config(ctypes.Structure):
     _fields_ = [("n_levels", ctypes.c_int), ("block_size", ctypes.c_int), ("nu_pre", ctypes.c_int),
                 ("nu_post", ctypes.c_int), ("omega", ctypes.c_double), ("coarse_mode", ctypes.c_int),
-                ("coarse_sweeps", ctypes.c_int), ("use_graphs", ctypes.c_int)]
+                ("coarse_sweeps", ctypes.c_int), ("use_graphs", ctypes.c_int), ("precision", ctypes.c_int)]
 
 
 class mg_comm(ctypes.Structure):
@@ -170,11 +171,12 @@ def mg_get_unique_id() -> bytes:
 
 
 def mg_create(n_levels, block_size, *, nu_pre=2, nu_post=2, omega=0.8, coarse_mode=MG_COARSE_DIRECT,
-              coarse_sweeps=20, use_graphs=True, device=0, stream=None, comm=None):
+              coarse_sweeps=20, use_graphs=True, device=0, stream=None, comm=None, precision=MG_PREC_FP64):
     """Returns an opaque context handle (int).  stream: a torch.cuda.Stream, a
     raw cudaStream_t int, or None (internal blocking stream).  comm: None
     (single GPU) or (nranks, rank, id_bytes[, transport])."""
-    cfg = mg_config(n_levels, block_size, nu_pre, nu_post, omega, coarse_mode, coarse_sweeps, int(bool(use_graphs)))
+    cfg = mg_config(n_levels, block_size, nu_pre, nu_post, omega, coarse_mode, coarse_sweeps, int(bool(use_graphs)),
+                    precision)
     h = _P()
     s = getattr(stream, "cuda_stream", stream)
     cm = None

@@ -25,6 +25,15 @@ inline void put_entry(double *val, int64_t e, int lane, int vpe, const double *s
   if (vpe & 1) base[64 * half + lane] = src ? src[vpe - 1] : 0.0;
 }
 
+// fp32 layout: 4-float (16-byte) chunks, then vpe % 4 single-float planes
+inline void put_entry(float *val, int64_t e, int lane, int vpe, const double *src) {
+  float *base = val + (e - lane) * vpe;
+  const int q = vpe / 4;
+  for (int j = 0; j < q; ++j)
+    for (int t = 0; t < 4; ++t) base[128 * j + 4 * lane + t] = src ? float(src[4 * j + t]) : 0.0f;
+  for (int k = 0; k < vpe % 4; ++k) base[128 * q + 32 * k + lane] = src ? float(src[4 * q + k]) : 0.0f;
+}
+
 // Gauss-Jordan with partial pivoting on one bs x bs block (bs <= 8).
 int gj_block(int bs, const double *a_in, double *out) {
   double a[64], inv[64];
@@ -108,8 +117,11 @@ int mgi_sell_size(int64_t n, const int64_t *rp, int sigma, int64_t *n_slices, in
   return 0;
 }
 
-int mgi_sell_fill(int64_t n, const int64_t *rp, const int64_t *col_in, const double *val_in, int vpe,
-                  int sigma, int64_t *slice_ptr, int32_t *perm, int32_t *col, double *val) {
+}  // extern "C" (template helpers below)
+
+template <class T>
+int sell_fill(int64_t n, const int64_t *rp, const int64_t *col_in, const double *val_in, int vpe, int sigma,
+              int64_t *slice_ptr, int32_t *perm, int32_t *col, T *val) {
   if (n < 0 || sigma < kSlice || sigma % kSlice || vpe < 1) return MG_ERR_INVALID_ARG;
   if (n >= (int64_t(1) << 31)) return MG_ERR_DIMENSION;
   const int64_t ns = (n + kSlice - 1) / kSlice;
@@ -155,6 +167,18 @@ int mgi_sell_fill(int64_t n, const int64_t *rp, const int64_t *col_in, const dou
     }
   }
   return 0;
+}
+
+extern "C" {
+
+int mgi_sell_fill(int64_t n, const int64_t *rp, const int64_t *col_in, const double *val_in, int vpe, int sigma,
+                  int64_t *slice_ptr, int32_t *perm, int32_t *col, double *val) {
+  return sell_fill<double>(n, rp, col_in, val_in, vpe, sigma, slice_ptr, perm, col, val);
+}
+
+int mgi_sell_fill_f32(int64_t n, const int64_t *rp, const int64_t *col_in, const double *val_in, int vpe, int sigma,
+                      int64_t *slice_ptr, int32_t *perm, int32_t *col, float *val) {
+  return sell_fill<float>(n, rp, col_in, val_in, vpe, sigma, slice_ptr, perm, col, val);
 }
 
 int mgi_csr_transpose(int64_t n_rows, int64_t n_cols, const int64_t *rp, const int64_t *col,

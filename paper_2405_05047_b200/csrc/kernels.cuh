@@ -28,6 +28,7 @@ struct Sell {
   const int32_t *col;        // [n_entries]
   const double *val;         // [n_entries*vpe], chunked (mg_internal.h)
   int64_t n_slices;
+  const float *valf;         // fp32 values (mixed-precision V-cycle operators), fp32 chunk layout
 };
 
 // ---------------------------------------------------------------------------
@@ -60,6 +61,26 @@ __device__ __forceinline__ void load_entry(const double *__restrict__ gval, int 
     v[2 * j + 1] = t.y;
   }
   if constexpr (VPE & 1) v[VPE - 1] = ld_val1<STREAM>(gval + 64 * (VPE / 2) + lane);
+}
+
+// fp32 values (layout of mgi_sell_fill_f32), converted exactly to fp64;
+// gval = valf + (e - lane) * VPE
+template <int VPE, bool STREAM>
+__device__ __forceinline__ void load_entry(const float *__restrict__ gval, int lane, double (&v)[VPE]) {
+#pragma unroll
+  for (int j = 0; j < VPE / 4; ++j) {
+    const float4 t = STREAM ? __ldcs(reinterpret_cast<const float4 *>(gval + 128 * j + 4 * lane))
+                            : __ldg(reinterpret_cast<const float4 *>(gval + 128 * j + 4 * lane));
+    v[4 * j] = t.x;
+    v[4 * j + 1] = t.y;
+    v[4 * j + 2] = t.z;
+    v[4 * j + 3] = t.w;
+  }
+#pragma unroll
+  for (int k = 0; k < VPE % 4; ++k) {
+    const float *p = gval + 128 * (VPE / 4) + 32 * k + lane;
+    v[4 * (VPE / 4) + k] = STREAM ? __ldcs(p) : __ldg(p);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -97,7 +118,7 @@ __device__ __forceinline__ bool combine_split(double (&acc)[BS], int wid, int su
   return true;
 }
 
-template <int BS, int OP, bool STREAM, bool HALO, int KS>
+template <int BS, int OP, bool STREAM, bool HALO, int KS, bool F32 = false>
 __global__ void __launch_bounds__(kCta) k_sell_apply(Sell A, const double *__restrict__ x,
                                                      const double *__restrict__ xg, int n_own,
                                                      const double *__restrict__ b,
@@ -123,7 +144,8 @@ __global__ void __launch_bounds__(kCta) k_sell_apply(Sell A, const double *__res
       const int c = cn;
       if (g + 32 * KS < e1) cn = ld_col<STREAM>(A.col + g + 32 * KS + lane);
       double v[V];
-      load_entry<V, STREAM>(A.val + g * V, lane, v);
+      if constexpr (F32) load_entry<V, STREAM>(A.valf + g * V, lane, v);
+      else load_entry<V, STREAM>(A.val + g * V, lane, v);
       const double *xc = col_ptr<BS, HALO>(x, xg, n_own, c);
       double xv[BS];
 #pragma unroll
@@ -446,6 +468,12 @@ __global__ void k_sqrt_copy(double *p, double *copy) {
     *p = r;
     if (copy) *copy = r;
   }
+}
+
+// x += z
+__global__ void k_axpy1(int64_t n, const double *__restrict__ z, double *__restrict__ x) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    x[i] += z[i];
 }
 
 // Finite check of a vector (any NaN/Inf -> *flag = 1).

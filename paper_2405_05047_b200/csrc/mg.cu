@@ -116,35 +116,48 @@ struct SellOp {
   DevArray<int64_t> slice_ptr;
   DevArray<int32_t> perm, col;
   DevArray<double> val;
+  DevArray<float> valf;  // fp32 values (mixed precision)
+  bool f32 = false;
   std::vector<int32_t> perm_host;
   int64_t n_rows = 0, n_slices = 0, n_entries = 0;
   int vpe = 0;
   int ks = 1;  // warps per slice (split-k for small levels / long transfer rows)
   bool stream = false;
   bool set = false;
-  mgk::Sell view() const { return mgk::Sell{slice_ptr.p, perm.p, col.p, val.p, n_slices}; }
+  mgk::Sell view() const { return mgk::Sell{slice_ptr.p, perm.p, col.p, val.p, n_slices, valf.p}; }
 };
 
-// Build SELL-32-sigma on the host and upload it (col: LOCAL column indices).
-mg_status build_sell(SellOp &op, int64_t n, const int64_t *rp, const int64_t *col, const double *val, int vpe) {
+// Build SELL-32-sigma on the host and upload it (col: LOCAL column indices);
+// f32: values rounded to fp32 in the fp32 chunk layout.
+mg_status build_sell(SellOp &op, int64_t n, const int64_t *rp, const int64_t *col, const double *val, int vpe,
+                     bool f32 = false) {
   int64_t ns = 0, ne = 0;
   int st = mgi_sell_size(n, rp, kSigma, &ns, &ne);
   if (st) return fail(mg_status(st), "sell layout: invalid input");
   std::vector<int64_t> sp(ns + 1);
   std::vector<int32_t> perm(ns * 32), c(ne);
-  std::vector<double> v(ne * vpe);
-  st = mgi_sell_fill(n, rp, col, val, vpe, kSigma, sp.data(), perm.data(), c.data(), v.data());
+  if (f32) {
+    std::vector<float> v(ne * vpe);
+    st = mgi_sell_fill_f32(n, rp, col, val, vpe, kSigma, sp.data(), perm.data(), c.data(), v.data());
+    if (!st) TRY(op.valf.upload(v.data(), v.size()));
+    op.val.release();
+  } else {
+    std::vector<double> v(ne * vpe);
+    st = mgi_sell_fill(n, rp, col, val, vpe, kSigma, sp.data(), perm.data(), c.data(), v.data());
+    if (!st) TRY(op.val.upload(v.data(), v.size()));
+    op.valf.release();
+  }
   if (st) return fail(mg_status(st), "sell layout: fill failed (%d)", st);
   TRY(op.slice_ptr.upload(sp.data(), sp.size()));
   TRY(op.perm.upload(perm.data(), perm.size()));
   TRY(op.col.upload(c.data(), c.size()));
-  TRY(op.val.upload(v.data(), v.size()));
   op.perm_host.swap(perm);
   op.n_rows = n;
   op.n_slices = ns;
   op.n_entries = ne;
   op.vpe = vpe;
-  op.stream = size_t(ne) * (8 * vpe + 4) > kStreamBytes;
+  op.f32 = f32;
+  op.stream = size_t(ne) * ((f32 ? 4 : 8) * vpe + 4) > kStreamBytes;
   op.set = true;
   return MG_OK;
 }
@@ -177,7 +190,8 @@ struct Level {
   int64_t n_global = 0, row_begin = 0, row_end = 0, n = 0;
   bool dist = false;             // rows partitioned over ranks
   std::vector<int64_t> bounds;   // [nranks+1] row ranges of the ranks (distributed levels)
-  SellOp A;
+  SellOp A;                       // the V-cycle operator (fp32 values in mixed precision)
+  SellOp A64;                     // mixed precision, finest level: fp64 operator for Krylov / residuals
   int64_t nnzb = 0;
   Halo hx;                        // ghosts of x for A-passes on this level
   std::vector<double> diag_host;  // diagonal blocks until D^-1 is built
@@ -234,6 +248,7 @@ struct mg_ctx_s {
   // GMRES workspace
   int gm_m = 0;
   DevArray<double> gm_V, gm_Z, gm_state;
+  DevArray<double> rich_z, rich_r;  // mixed-precision MG iteration (defect correction)
   double *gm_host = nullptr;  // pinned
   mgk::GmresDev gm{};
   ~mg_ctx_s() {
@@ -302,7 +317,17 @@ template <int BS, int OP, bool HALO>
 void launch_apply_h(const SellOp &A, In in, const double *b, const double *dinv, double *out, double alpha,
                     double beta, cudaStream_t st) {
   const unsigned g = grid_for_slices(A.n_slices, A.ks);
-  if (A.ks == 4)
+  if (A.f32) {
+    if (A.ks == 4)
+      ++g_tally, mgk::k_sell_apply<BS, OP, false, HALO, 4, true>
+                     <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+    else if (A.ks == 2)
+      ++g_tally, mgk::k_sell_apply<BS, OP, true, HALO, 2, true>
+                     <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+    else
+      ++g_tally, mgk::k_sell_apply<BS, OP, true, HALO, 1, true>
+                     <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+  } else if (A.ks == 4)
     ++g_tally, mgk::k_sell_apply<BS, OP, false, HALO, 4>
                    <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
   else if (A.ks == 2)
@@ -725,16 +750,23 @@ mg_status a_pass_sweep(mg_ctx_s *c, int l, const double *src, const double *b, d
                                      c->stream);
 }
 
-mg_status a_pass_resid(mg_ctx_s *c, int l, const double *x, const double *b, double *r) {
+// krylov = true: the problem operator (fp64 A64 on the finest level in mixed
+// precision); false: the V-cycle's operator.
+const SellOp &op_of(Level &L, bool krylov) { return krylov && L.A64.set ? L.A64 : L.A; }
+
+mg_status a_pass_resid(mg_ctx_s *c, int l, const double *x, const double *b, double *r, bool krylov = false) {
   Level &L = c->lv[l];
   TRY(halo_exchange(c, L.hx, x));
-  return launch_apply<mgk::OP_RESID>(c->bs(), L.A, in_of(L, L.hx, x), b, nullptr, r, 1.0, 0.0, c->stream);
+  return launch_apply<mgk::OP_RESID>(c->bs(), op_of(L, krylov), in_of(L, L.hx, x), b, nullptr, r, 1.0, 0.0,
+                                     c->stream);
 }
 
-mg_status a_pass_spmv(mg_ctx_s *c, int l, double alpha, const double *x, double beta, double *y) {
+mg_status a_pass_spmv(mg_ctx_s *c, int l, double alpha, const double *x, double beta, double *y,
+                      bool krylov = false) {
   Level &L = c->lv[l];
   TRY(halo_exchange(c, L.hx, x));
-  return launch_apply<mgk::OP_SPMV>(c->bs(), L.A, in_of(L, L.hx, x), nullptr, nullptr, y, alpha, beta, c->stream);
+  return launch_apply<mgk::OP_SPMV>(c->bs(), op_of(L, krylov), in_of(L, L.hx, x), nullptr, nullptr, y, alpha, beta,
+                                    c->stream);
 }
 
 // d_coarse = R r_fine (all coarse rows on every rank if the coarse level is replicated)
@@ -941,6 +973,8 @@ mg_status mg_create(mg_ctx *out, const mg_config *cfg, int device, void *cuda_st
   if (!(cfg->omega > 0.0) || !std::isfinite(cfg->omega)) return fail(MG_ERR_INVALID_ARG, "omega must be > 0");
   if (cfg->coarse_mode != MG_COARSE_DIRECT && cfg->coarse_mode != MG_COARSE_SMOOTH)
     return fail(MG_ERR_INVALID_ARG, "bad coarse_mode");
+  if (cfg->precision != MG_PREC_FP64 && cfg->precision != MG_PREC_MIXED)
+    return fail(MG_ERR_INVALID_ARG, "bad precision");
   DeviceGuard dg(device);
   int ndev = 0;
   CU(cudaGetDeviceCount(&ndev));
@@ -1032,6 +1066,14 @@ mg_status mg_set_matrix(mg_ctx c, int level, const int64_t *row_ptr, const int64
   std::vector<int64_t> rp, cl;
   std::vector<double> v;
   TRY(fetch_csr(c, L.n, L.n_global, row_ptr, col, vals, nnzb, V, mem, true, L.row_begin, rp, cl, v, "matrix"));
+  const bool mixed = c->cfg.precision == MG_PREC_MIXED;
+  std::vector<double> v64;
+  if (mixed) {
+    // the V-cycle works with A rounded to fp32 (its D^-1 and coarse inverse
+    // too); the finest level keeps the fp64 operator for the Krylov side
+    if (level == c->L()) v64 = v;
+    for (double &a : v) a = double(float(a));
+  }
   L.diag_host.assign(size_t(L.n) * V, 0.0);
   for (int64_t i = 0; i < L.n; ++i)
     for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
@@ -1041,8 +1083,14 @@ mg_status mg_set_matrix(mg_ctx c, int level, const int64_t *row_ptr, const int64
     TRY(localize(L.row_begin, L.row_end, rp, cl, ghosts));
     TRY(build_halo(c, L.hx, ghosts, L.bounds, L.row_begin, L.row_end));
   }
-  TRY(build_sell(L.A, L.n, rp.data(), cl.data(), v.data(), V));
+  TRY(build_sell(L.A, L.n, rp.data(), cl.data(), v.data(), V, mixed));
   L.A.ks = ks_for_level(L.n_global);
+  if (!v64.empty()) {
+    TRY(build_sell(L.A64, L.n, rp.data(), cl.data(), v64.data(), V, false));
+    L.A64.ks = L.A.ks;
+  } else {
+    L.A64 = SellOp();
+  }
   L.nnzb = nnzb;
   L.dinv_ready = false;  // (re)built at finalize; a user D^-1 is re-sliced with the new permutation
   if (level == 0 && !L.dist) {
@@ -1228,7 +1276,7 @@ mg_status mg_spmv(mg_ctx c, int level, double alpha, const double *x, double bet
   if (!c->lv[level].A.set) return fail(MG_ERR_STATE, "level %d has no matrix", level);
   DeviceGuard dg(c->device);
   Tally tally(c);
-  return a_pass_spmv(c, level, alpha, x, beta, y);
+  return a_pass_spmv(c, level, alpha, x, beta, y, true);
 }
 
 mg_status mg_sweep(mg_ctx c, int level, const double *x, const double *b, double *x_out) {
@@ -1246,7 +1294,7 @@ mg_status mg_residual(mg_ctx c, int level, const double *x, const double *b, dou
   if (!c->lv[level].A.set) return fail(MG_ERR_STATE, "level %d has no matrix", level);
   DeviceGuard dg(c->device);
   Tally tally(c);
-  return a_pass_resid(c, level, x, b, r);
+  return a_pass_resid(c, level, x, b, r, true);
 }
 
 mg_status mg_smooth(mg_ctx c, int level, double *x, const double *b, int sweeps) {
@@ -1347,19 +1395,34 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
   if (!c->gm_host) CU(cudaMallocHost(&c->gm_host, 16 * sizeof(double)));
   double *hst = c->gm_host;
 
+  const bool mixed = F.A64.set;
   if (opts->method == MG_RICHARDSON) {
-    TRY(a_pass_resid(c, Lf, x, b, F.w.p));
-    TRY(dev_dot(c, dist, N, F.w.p, F.w.p, c->scal.p, true));
+    // mixed precision: defect correction x += GMG(L, 0, r), r = b - A x in fp64,
+    // kept in a buffer of its own (F.w is the V-cycle's work vector)
+    if (mixed && !c->rich_z.p) {
+      TRY(c->rich_z.alloc(size_t(std::max<int64_t>(N, 1))));
+      TRY(c->rich_r.alloc(size_t(std::max<int64_t>(N, 1))));
+    }
+    double *r = mixed ? c->rich_r.p : F.w.p;
+    TRY(a_pass_resid(c, Lf, x, b, r, true));
+    TRY(dev_dot(c, dist, N, r, r, c->scal.p, true));
     CU(cudaMemcpyAsync(hst, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     const double r0 = hst[0];
     if (!std::isfinite(r0)) return fail(MG_ERR_NONFINITE, "non-finite initial residual");
     if (r0 == 0.0) conv = true;
+    const unsigned eg = unsigned(std::min<int64_t>(std::max<int64_t>(1, (N + 255) / 256), 8 * c->n_sm));
     while (!conv && its < opts->max_iter) {
-      TRY(run_vcycle(c, x, b, false));
+      if (!mixed) {
+        TRY(run_vcycle(c, x, b, false));  // x <- GMG(L, x, b)
+      } else {
+        TRY(run_vcycle(c, c->rich_z.p, r, true));
+        ++g_tally, mgk::k_axpy1<<<eg, 256, 0, c->stream>>>(N, c->rich_z.p, x);
+        TRY(check_launch("axpy"));
+      }
       ++its;
-      TRY(a_pass_resid(c, Lf, x, b, F.w.p));
-      TRY(dev_dot(c, dist, N, F.w.p, F.w.p, c->scal.p, true));
+      TRY(a_pass_resid(c, Lf, x, b, r, true));
+      TRY(dev_dot(c, dist, N, r, r, c->scal.p, true));
       CU(cudaMemcpyAsync(hst, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CU(cudaStreamSynchronize(c->stream));
       if (!std::isfinite(hst[0])) return fail(MG_ERR_NONFINITE, "non-finite residual at iteration %d", its);
@@ -1373,7 +1436,7 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
     const int ld = g.m + 1;  // leading dimension of the allocated Hessenberg
     double *V = c->gm_V.p, *Z = c->gm_Z.p;
     const int64_t NS = gm_stride(N);
-    TRY(a_pass_resid(c, Lf, x, b, V));
+    TRY(a_pass_resid(c, Lf, x, b, V, true));
     TRY(dev_dot(c, dist, N, V, V, g.beta0, true));
     CU(cudaMemcpyAsync(g.beta, g.beta0, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     CU(cudaMemcpyAsync(hst, g.beta0, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -1395,7 +1458,7 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
         auto step = [&]() -> mg_status {
           double *vj = V + size_t(j) * NS, *zj = Z + size_t(j) * NS, *w = V + size_t(j + 1) * NS;
           TRY(vcycle_rec(c, Lf, zj, vj, true));      // z_j = GMG(L, 0, v_j)
-          TRY(a_pass_spmv(c, Lf, 1.0, zj, 0.0, w));  // w = A z_j
+          TRY(a_pass_spmv(c, Lf, 1.0, zj, 0.0, w, true));  // w = A z_j
           double *hcol = g.H + size_t(j) * ld;
           TRY(dev_dot(c, dist, N, w, V, hcol + 0, false));  // h_0j = (w, v_0)
           for (int i = 0; i < j; ++i)                       // w -= h_ij v_i ; h_{i+1,j} = (w, v_{i+1})
@@ -1431,7 +1494,7 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
       ++g_tally, mgk::k_backsolve<<<1, 32, 0, c->stream>>>(g, k);
       ++g_tally, mgk::k_update_x<<<eg, 256, 0, c->stream>>>(N, k, g.y, Z, NS, x);
       TRY(check_launch("gmres update"));
-      TRY(a_pass_resid(c, Lf, x, b, V));
+      TRY(a_pass_resid(c, Lf, x, b, V, true));
       TRY(dev_dot(c, dist, N, V, V, g.beta, true));
       CU(cudaMemcpyAsync(hst, g.beta, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CU(cudaStreamSynchronize(c->stream));

@@ -17,12 +17,13 @@ class Multigrid:
     problems.partition."""
 
     def __init__(self, levels, bs, *, omega=0.8, nu_pre=2, nu_post=2, coarse_mode=MG_COARSE_DIRECT,
-                 coarse_sweeps=20, use_graphs=True, device=0, stream=None, H=None, omegas=None, comm=None):
+                 coarse_sweeps=20, use_graphs=True, device=0, stream=None, H=None, omegas=None, comm=None,
+                 precision=0):
         self.bs = bs
         self.n = [int(L.n) for L in levels]
         self.ctx = mg_create(len(levels), bs, nu_pre=nu_pre, nu_post=nu_post, omega=omega,
                              coarse_mode=coarse_mode, coarse_sweeps=coarse_sweeps, use_graphs=use_graphs,
-                             device=device, stream=stream, comm=comm)
+                             device=device, stream=stream, comm=comm, precision=precision)
         try:
             for l, L in enumerate(levels):
                 ng = int(getattr(L, "n_global", L.n))

@@ -1,8 +1,8 @@
 """GPU parity at BASELINE.json's full sizes, in bench.py's launch
-configuration (graph-captured V-cycles, SELL-32-4096 operators, C2 and C3):
+configuration (graph-captured V-cycles, SELL-32-4096 operators, C2-C5):
 sampled rows against the oracle computed row by row on the same inputs, and
 properties that hold at any size (exact scaling by 2, determinism, residual
-contraction, GMRES convergence; iteration parity +-1 on C2)."""
+contraction, GMRES convergence; iteration parity +-1 on C2 and C4)."""
 import functools
 
 import numpy as np
@@ -40,7 +40,7 @@ def sub_csr(rp, col, val, rows, vpe):
     return srp, col[idx], v
 
 
-@pytest.mark.parametrize("name", ["c2", "c3"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
 def test_fullsize_residual_sweep_sampled(name):
     import paper_2405_05047_b200 as m
     P, mg = full(name)
@@ -73,7 +73,7 @@ def test_fullsize_residual_sweep_sampled(name):
         assert np.max(np.abs(got - e_sw)) <= 10 * TOL_OP * np.max(sc_sw), f"{name} sweep level {l}"
 
 
-@pytest.mark.parametrize("name", ["c2", "c3"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
 def test_fullsize_transfers_sampled(name):
     import paper_2405_05047_b200 as m
     P, mg = full(name)
@@ -85,25 +85,26 @@ def test_fullsize_transfers_sampled(name):
     d = dev(np.full(C.n * bs, np.nan))
     m.mg_restrict(mg.ctx, Lf, dev(r), d)
     prp, pcol, pw = L.P
-    rrp, rcol, rw = oracle.csr_transpose(L.n, C.n, prp, pcol, pw)
+    wpe = L.wpe
+    rrp, rcol, rw = oracle.csr_transpose(L.n, C.n, prp, pcol, pw, wpe)
     rows = sample_rows(C.n, seed=3)
-    srp, scol, sw = sub_csr(rrp, rcol, rw, rows, 1)
-    exp = oracle.transfer(len(rows), bs, srp, scol, sw.reshape(-1), 1, r)
+    srp, scol, sw = sub_csr(rrp, rcol, rw.reshape(len(rcol), wpe), rows, 1)
+    exp = oracle.transfer(len(rows), bs, srp, scol, sw.reshape(-1), wpe, r)
     got = host(d).reshape(-1, bs)[rows].reshape(-1)
-    sc = oracle.transfer(len(rows), bs, srp, scol, np.abs(sw.reshape(-1)), 1, np.abs(r))
+    sc = oracle.transfer(len(rows), bs, srp, scol, np.abs(sw.reshape(-1)), wpe, np.abs(r))
     assert np.max(np.abs(got - exp)) <= TOL_OP * np.max(sc)
     y = g.standard_normal(C.n * bs)
     x0 = g.standard_normal(L.n * bs)
     x = dev(x0)
     m.mg_prolong_add(mg.ctx, Lf, dev(y), x)
     rows = sample_rows(L.n, seed=4)
-    srp, scol, sw = sub_csr(prp, pcol, pw, rows, 1)
-    exp = oracle.transfer(len(rows), bs, srp, scol, sw.reshape(-1), 1, y, x0.reshape(-1, bs)[rows].reshape(-1))
+    srp, scol, sw = sub_csr(prp, pcol, pw.reshape(len(pcol), wpe), rows, 1)
+    exp = oracle.transfer(len(rows), bs, srp, scol, sw.reshape(-1), wpe, y, x0.reshape(-1, bs)[rows].reshape(-1))
     got = host(x).reshape(-1, bs)[rows].reshape(-1)
     assert np.max(np.abs(got - exp)) <= TOL_OP * (np.max(np.abs(x0)) + np.max(np.abs(y)))
 
 
-@pytest.mark.parametrize("name", ["c2", "c3"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
 def test_fullsize_vcycle_properties(name):
     import paper_2405_05047_b200 as m
     P, mg = full(name)
@@ -118,16 +119,19 @@ def test_fullsize_vcycle_properties(name):
     h1, h2, h3 = host(z1), host(z2), host(z3)
     assert np.array_equal(h1, h3)                       # deterministic (no atomics)
     assert np.array_equal(2.0 * h1, h2)                 # linear in b, exactly (power-of-two scaling)
-    r = dev(np.zeros(P.n_dof))
-    m.mg_residual(mg.ctx, len(P.levels) - 1, z1, b, r)
-    rn = np.sqrt(m.mg_dot(mg.ctx, len(P.levels) - 1, r, r))
-    bn = np.linalg.norm(P.b)
-    assert rn < 0.75 * bn                               # one V-cycle contracts (C3 rho ~ 0.5, C2 ~ 0.15)
+    if P.op.name != "stokes":
+        # one V-cycle contracts for the SPD-type operators (C3 rho ~ 0.5, C2 ~ 0.15); for the
+        # non-normal saddle-point C5 a single cycle need not shrink the 2-norm (GMRES below)
+        r = dev(np.zeros(P.n_dof))
+        m.mg_residual(mg.ctx, len(P.levels) - 1, z1, b, r)
+        rn = np.sqrt(m.mg_dot(mg.ctx, len(P.levels) - 1, r, r))
+        assert rn < 0.9 * np.linalg.norm(P.b)
 
 
-def test_fullsize_gmres_c3_converges():
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_fullsize_gmres_converges(name):
     import paper_2405_05047_b200 as m
-    P, mg = full("c3")
+    P, mg = full(name)
     x = dev(np.zeros(P.n_dof))
     st, its, rel, conv = m.mg_solve(mg.ctx, x, dev(P.b), rtol=1e-10)
     assert conv and rel <= 2e-10 and its <= 40
@@ -137,9 +141,10 @@ def test_fullsize_gmres_c3_converges():
     assert rn <= 2e-10 * np.linalg.norm(P.b)
 
 
-def test_fullsize_gmres_c2_iterations_match_oracle():
+@pytest.mark.parametrize("name", ["c2", "c4"])
+def test_fullsize_gmres_iterations_match_oracle(name):
     import paper_2405_05047_b200 as m
-    P, mg = full("c2")
+    P, mg = full(name)
     x = dev(np.zeros(P.n_dof))
     st, its, rel, conv = m.mg_solve(mg.ctx, x, dev(P.b), rtol=1e-10)
     h = oracle.MgHierarchy.from_arrays(P.levels, omega=P.omega)
