@@ -20,7 +20,7 @@ namespace mgk {
 
 constexpr int kWarpsPerCta = 8;
 constexpr int kCta = 32 * kWarpsPerCta;
-constexpr int kRedThreads = 512;
+constexpr int kRedThreads = 256;
 
 struct Sell {
   const int64_t *slice_ptr;  // [n_slices+1] entry offsets (multiples of 32)
@@ -67,6 +67,25 @@ __device__ __forceinline__ void load_entry(const double *__restrict__ gval, int 
 // gval = valf + (e - lane) * VPE
 template <int VPE, bool STREAM>
 __device__ __forceinline__ void load_entry(const float *__restrict__ gval, int lane, double (&v)[VPE]) {
+#pragma unroll
+  for (int j = 0; j < VPE / 4; ++j) {
+    const float4 t = STREAM ? __ldcs(reinterpret_cast<const float4 *>(gval + 128 * j + 4 * lane))
+                            : __ldg(reinterpret_cast<const float4 *>(gval + 128 * j + 4 * lane));
+    v[4 * j] = t.x;
+    v[4 * j + 1] = t.y;
+    v[4 * j + 2] = t.z;
+    v[4 * j + 3] = t.w;
+  }
+#pragma unroll
+  for (int k = 0; k < VPE % 4; ++k) {
+    const float *p = gval + 128 * (VPE / 4) + 32 * k + lane;
+    v[4 * (VPE / 4) + k] = STREAM ? __ldcs(p) : __ldg(p);
+  }
+}
+
+// raw fp32 values of one entry (converted at use)
+template <int VPE, bool STREAM>
+__device__ __forceinline__ void load_entry_raw(const float *__restrict__ gval, int lane, float (&v)[VPE]) {
 #pragma unroll
   for (int j = 0; j < VPE / 4; ++j) {
     const float4 t = STREAM ? __ldcs(reinterpret_cast<const float4 *>(gval + 128 * j + 4 * lane))
@@ -139,6 +158,34 @@ __global__ void __launch_bounds__(kCta) k_sell_apply(Sell A, const double *__res
     row = A.perm[s * 32 + lane];
     int64_t g = e0 + 32 * sub;
     int cn = g < e1 ? ld_col<STREAM>(A.col + g + lane) : 0;  // column of the next entry (prefetched)
+    if constexpr (F32) {
+      // fp32 values carry half the bytes per entry: issue the loads of U
+      // entries before the first use so twice as many bytes are in flight
+      constexpr int U = 4, step = 32 * KS;
+      for (; g + (U - 1) * step < e1; g += U * step) {
+        int cc[U];
+        cc[0] = cn;
+#pragma unroll
+        for (int u = 1; u < U; ++u) cc[u] = ld_col<STREAM>(A.col + g + u * step + lane);
+        if (g + U * step < e1) cn = ld_col<STREAM>(A.col + g + U * step + lane);
+        float vf[U][V];
+#pragma unroll
+        for (int u = 0; u < U; ++u) load_entry_raw<V, STREAM>(A.valf + (g + u * step) * V, lane, vf[u]);
+        double xv[U][BS];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const double *xc = col_ptr<BS, HALO>(x, xg, n_own, cc[u]);
+#pragma unroll
+          for (int q = 0; q < BS; ++q) xv[u][q] = __ldg(xc + q);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int r = 0; r < BS; ++r)
+#pragma unroll
+            for (int q = 0; q < BS; ++q) acc[r] = fma(double(vf[u][r * BS + q]), xv[u][q], acc[r]);
+      }
+    }
 #pragma unroll 4
     for (; g < e1; g += 32 * KS) {
       const int c = cn;
@@ -255,7 +302,21 @@ __global__ void __launch_bounds__(kCta) k_dense_gemv(int64_t N, int64_t ld, cons
   if (r >= N) return;
   const double *row = M + r * ld;
   double acc = 0.0;
-  for (int64_t c = 2 * lane; c < N; c += 64) {
+  int64_t c = 2 * lane;
+  for (; c + 192 + 1 < N; c += 256) {  // four independent 16-byte loads in flight
+    double2 m[4], dv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      m[u] = __ldg(reinterpret_cast<const double2 *>(row + c + 64 * u));
+      dv[u] = make_double2(__ldg(d + c + 64 * u), __ldg(d + c + 64 * u + 1));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc = fma(m[u].x, dv[u].x, acc);
+      acc = fma(m[u].y, dv[u].y, acc);
+    }
+  }
+  for (; c < N; c += 64) {
     const double2 m = __ldg(reinterpret_cast<const double2 *>(row + c));
     acc = fma(m.x, __ldg(d + c), acc);
     if (c + 1 < N) acc = fma(m.y, __ldg(d + c + 1), acc);
@@ -326,26 +387,47 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce(int64_t n, double *__res
   const double hv = MODE == 1 ? *h : 0.0;
   int64_t i0 = 0;
   if constexpr (VEC) {
+    constexpr int U = 4;  // independent 16-byte loads in flight per thread and vector
     const int64_t n2 = n / 2;
     double2 *a2 = reinterpret_cast<double2 *>(a);
     const double2 *b2 = reinterpret_cast<const double2 *>(b);
     const double2 *c2 = reinterpret_cast<const double2 *>(c);
-#pragma unroll 2
-    for (int64_t i = tid; i < n2; i += stride) {
-      if constexpr (MODE == 0) {
-        const double2 x = __ldg(a2 + i), y = __ldg(b2 + i);
-        s = fma(x.x, y.x, s);
-        s2 = fma(x.y, y.y, s2);
-      } else {
-        double2 x = a2[i];
+    int64_t i = tid;
+    for (; i + (U - 1) * stride < n2; i += U * stride) {
+      double2 x[U], y[U], v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if constexpr (MODE == 0) {
+          x[u] = __ldg(a2 + i + u * stride);
+        } else {
+          x[u] = a2[i + u * stride];
+          v[u] = __ldg(c2 + i + u * stride);
+        }
+        if (b) y[u] = __ldg(b2 + i + u * stride);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if constexpr (MODE == 1) {
+          x[u].x = fma(-hv, v[u].x, x[u].x);
+          x[u].y = fma(-hv, v[u].y, x[u].y);
+          a2[i + u * stride] = x[u];
+        }
+        const double2 yy = b ? y[u] : x[u];
+        s = fma(x[u].x, yy.x, s);
+        s2 = fma(x[u].y, yy.y, s2);
+      }
+    }
+    for (; i < n2; i += stride) {
+      double2 x = MODE == 0 ? __ldg(a2 + i) : a2[i];
+      if constexpr (MODE == 1) {
         const double2 v = __ldg(c2 + i);
         x.x = fma(-hv, v.x, x.x);
         x.y = fma(-hv, v.y, x.y);
         a2[i] = x;
-        const double2 y = b ? __ldg(b2 + i) : x;
-        s = fma(x.x, y.x, s);
-        s2 = fma(x.y, y.y, s2);
       }
+      const double2 yy = b ? __ldg(b2 + i) : x;
+      s = fma(x.x, yy.x, s);
+      s2 = fma(x.y, yy.y, s2);
     }
     i0 = 2 * n2;
     s += s2;
@@ -386,19 +468,22 @@ __global__ void k_gmres_start(GmresDev st) {
   }
 }
 
-// out = in / *den (in-place allowed); 16-byte aligned pointers, odd tail in thread 0
+// out = in * (1 / *den) (in-place allowed; a reciprocal multiply: fp64
+// division is a long instruction sequence and halves this kernel's bandwidth);
+// 16-byte aligned pointers, odd tail in thread 0
 __global__ void k_scale_div(int64_t n, const double *in, const double *den, double *out) {
   const double d = *den;
   if (d == 0.0) return;
+  const double r = 1.0 / d;
   const int64_t n2 = n / 2;
   const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   for (int64_t i = tid; i < n2; i += int64_t(gridDim.x) * blockDim.x) {
     double2 v = reinterpret_cast<const double2 *>(in)[i];
-    v.x /= d;
-    v.y /= d;
+    v.x *= r;
+    v.y *= r;
     reinterpret_cast<double2 *>(out)[i] = v;
   }
-  if (tid == 0 && (n & 1)) out[n - 1] = in[n - 1] / d;
+  if (tid == 0 && (n & 1)) out[n - 1] = in[n - 1] * r;
 }
 
 // Apply the previous rotations to column j, form the new one, update g and

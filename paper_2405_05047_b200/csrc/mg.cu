@@ -500,8 +500,8 @@ mg_status localize(int64_t rb, int64_t re, const std::vector<int64_t> &rp, std::
 
 // --- reductions (deterministic; all-reduced over ranks on distributed levels) ---
 unsigned red_grid(const mg_ctx_s *c, int64_t n) {
-  const int64_t want = (n + mgk::kRedThreads * 4 - 1) / (mgk::kRedThreads * 4);
-  return unsigned(std::max<int64_t>(1, std::min<int64_t>(want, 2 * c->n_sm)));
+  const int64_t want = (n + mgk::kRedThreads * 8 - 1) / (mgk::kRedThreads * 8);
+  return unsigned(std::max<int64_t>(1, std::min<int64_t>(want, 4 * c->n_sm)));
 }
 
 mg_status finish_reduce(mg_ctx_s *c, bool dist, double *res, bool sqrt_, double *copy = nullptr) {
@@ -729,7 +729,7 @@ mg_status finalize(mg_ctx_s *c) {
   }
   if (c->cfg.coarse_mode == MG_COARSE_DIRECT && c->cN == 0) TRY(build_coarse_inverse(c));
   if (!c->red_part.p) {
-    TRY(c->red_part.alloc(2 * c->n_sm + 8));
+    TRY(c->red_part.alloc(4 * c->n_sm + 8));
     TRY(c->ticket.alloc(1));
     CU(cudaMemset(c->ticket.p, 0, sizeof(unsigned)));
     TRY(c->scal.alloc(16));
