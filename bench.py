@@ -323,6 +323,9 @@ def run_ours(args):
     vc_ms = e0.elapsed_time(e1) / nv
     vc_bytes = vcycle_bytes(infos, bs, (P.nu_pre, P.nu_post), zero=True, vb=vb)
 
+    # ---------------- per-level split of one (eager) V-cycle --------------------
+    prof = mg.vcycle_profile(ctx, z, b, L + 1)
+
     # ---------------- dominant kernel: fine-level fused block-Jacobi sweep -----
     peak, peak_src = measured_peaks()
     xin = torch.randn(N, dtype=torch.float64, device="cuda")
@@ -345,6 +348,30 @@ def run_ours(args):
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get(args.config, {}).get("sweep_fine_dram_bytes")
+
+    # ---------------- mixed precision on the same workload ---------
+    mixed = None
+    if ws == 1 and args.precision == "fp64" and not args.no_mixed:
+        solver.close()
+        t = time.time()
+        solver = mg.Multigrid(P.levels, bs, omega=P.omega, nu_pre=P.nu_pre, nu_post=P.nu_post, H=P.fine.H,
+                              device=dev, stream=stream, use_graphs=not args.no_graphs, precision=mg.MG_PREC_MIXED)
+        log(f"[bench] mixed-precision setup {time.time() - t:.1f}s")
+        for _ in range(args.warmup):
+            step(x, b)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        m_its = 0
+        for _ in range(args.steps):
+            its, rel = step(x, b)
+            m_its += its
+        e1.record(stream)
+        torch.cuda.synchronize()
+        m_ms = e0.elapsed_time(e1)
+        mixed = {"value": m_its / (m_ms / 1e3), "unit": "V-cycles/s", "solve_ms": m_ms / args.steps,
+                 "iterations_per_solve": m_its // args.steps, "true_rel_residual": rel,
+                 "note": "V-cycle operators A_l stored fp32 (fp64 vectors, accumulation, D^-1, transfers, "
+                         "coarse inverse), fp64 GMRES operator; converges to the fp64 1e-10 residual"}
 
     # ---------------- CPU baseline: the oracle on the host cores ----------------
     cpu = None
@@ -375,6 +402,11 @@ def run_ours(args):
                        "iterations_per_solve": total_its // args.steps},
             "dof_cycles_per_s": value * n_global,
             "solve_ms": t_ms / args.steps,
+            "solve_dofs_per_s": n_global / (t_ms / args.steps / 1e3),
+            "vcycle_levels": {"rows_rank0": [i["n"] for i in infos], "ms": prof["level_ms"],
+                              "halo_ms": prof["halo_ms"], "agglomeration_ms": prof["agglomeration_ms"],
+                              "note": "one eager V(2,2) from zero, CUDA events between phases"},
+            "mixed_precision": mixed,
             "vcycle_only": {"ms": vc_ms, "per_s": 1e3 / vc_ms, "alg_bytes": vc_bytes,
                             "alg_gbs": vc_bytes / (vc_ms / 1e3) / 1e9,
                             "frac": vc_bytes / (vc_ms / 1e3) / 1e9 / peak},
@@ -404,6 +436,7 @@ def main():
     ap.add_argument("--rtol", type=float, default=1e-10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--no-mixed", action="store_true", help="skip the mixed-precision side measurement")
     ap.add_argument("--precision", choices=["fp64", "mixed"], default="fp64",
                     help="mixed: fp32-stored V-cycle operators inside fp64 GMRES (SURVEY N1)")
     ap.add_argument("--min-rows-per-rank", type=int, default=16384,

@@ -104,6 +104,13 @@ int mgi_assemble_routed_rows(int64_t m, const int64_t *J, const int64_t *i, cons
 typedef struct mg_ctx_s *mgi_ctx;
 int64_t mgi_launch_count(mgi_ctx ctx);
 
+/* One V-cycle (eager, not graph-launched) with CUDA events between its
+ * phases: out[l] = ms spent on level l's kernels (both legs; level 0 = the
+ * coarse solve), out[n_levels + l] = ms in level l's halo exchanges,
+ * out[2 n_levels] = ms in agglomeration all-gathers.  n_out >= 2 n_levels + 1.
+ * Returns an mg_status. */
+int mgi_vcycle_profile(mgi_ctx ctx, double *x, const double *b, int zero, double *out, int n_out);
+
 /* Per-level sizes after setup: n rows, true nnzb, stored SELL entries of A,
  * nnz of P (into the level) and of R.  Returns 0 or MG_ERR_INVALID_ARG. */
 int mgi_level_info(mgi_ctx ctx, int level, int64_t *n, int64_t *nnzb, int64_t *sell_entries, int64_t *nnz_p,

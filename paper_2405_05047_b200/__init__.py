@@ -103,6 +103,8 @@ _lib.mg_version.restype = ctypes.c_char_p
 _lib.mg_version.argtypes = []
 _lib.mgi_launch_count.restype = ctypes.c_int64
 _lib.mgi_launch_count.argtypes = [_P]
+_lib.mgi_vcycle_profile.restype = ctypes.c_int
+_lib.mgi_vcycle_profile.argtypes = [_P, _P, _P, _I, _P, _I]
 _lib.mgi_level_info.restype = ctypes.c_int
 _lib.mgi_level_info.argtypes = [_P, _I] + [ctypes.POINTER(ctypes.c_int64)] * 6
 
@@ -286,6 +288,14 @@ def mg_dot(ctx, level, a, b) -> float:
 def launch_count(ctx) -> int:
     """Kernels launched by the context so far (eager + CUDA-graph kernel nodes)."""
     return int(_lib.mgi_launch_count(ctx))
+
+
+def vcycle_profile(ctx, x, b, n_levels, zero=True) -> dict:
+    """Per-level time split of one eager V-cycle (mgi_vcycle_profile), ms."""
+    out = (ctypes.c_double * (2 * n_levels + 1))()
+    _check(_lib.mgi_vcycle_profile(ctx, _dptr(x), _dptr(b), int(zero), out, 2 * n_levels + 1), "mgi_vcycle_profile")
+    v = list(out)
+    return {"level_ms": v[:n_levels], "halo_ms": v[n_levels:2 * n_levels], "agglomeration_ms": v[2 * n_levels]}
 
 
 def level_info(ctx, level) -> dict:

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -242,6 +243,10 @@ struct mg_ctx_s {
   DevArray<double> red_part, scal;
   DevArray<unsigned> ticket;
   bool finalized = false;
+  // per-level profiling (mgi_vcycle_profile): tagged events on the stream
+  bool prof_on = false;
+  int cur_level = 0;
+  std::vector<std::pair<int, cudaEvent_t>> prof;
   std::map<GraphKey, GraphExec> graphs;
   std::map<std::tuple<int, double, int>, GraphExec> iter_graphs;  // GMRES iteration j (j, rtol, m)
   int64_t launches = 0;
@@ -294,9 +299,16 @@ inline unsigned grid_for_slices(int64_t n_slices, int ks = 1) {
 
 // split-k factor of an A operator, decided on the GLOBAL level size so every
 // rank of a distributed solve (and the single-GPU solve) sums identically
+// thresholds in slices (overridable for tuning: MGB200_KS4_SLICES, MGB200_KS2_SLICES)
+int64_t env_i64(const char *name, int64_t dflt) {
+  const char *v = std::getenv(name);
+  return v && *v ? std::atoll(v) : dflt;
+}
+
 int ks_for_level(int64_t n_global) {
+  static const int64_t t4 = env_i64("MGB200_KS4_SLICES", 4096), t2 = env_i64("MGB200_KS2_SLICES", 32768);
   const int64_t slices = (n_global + 31) / 32;
-  return slices < 4096 ? 4 : slices < 32768 ? 2 : 1;
+  return slices < t4 ? 4 : slices < t2 ? 2 : 1;
 }
 
 mg_status check_launch(const char *what = "kernel") {
@@ -419,9 +431,23 @@ mg_status launch_transfer(int bs, bool acc, const SellOp &T, In in, double *out,
   return check_launch(acc ? "prolong-add" : "transfer");
 }
 
+// profiling marks: tag = level (compute), 100 + level (halo), 200 + level (agglomeration)
+void mark(mg_ctx_s *c, int tag) {
+  if (!c->prof_on) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, c->stream);
+  c->prof.emplace_back(tag, e);
+}
+
 // --- halo exchange: pack owned rows, transport into the ghost buffer ----------
 mg_status halo_exchange(mg_ctx_s *c, Halo &h, const double *v) {
   if (!h.active) return MG_OK;
+  mark(c, 100 + c->cur_level);
+  struct Back {
+    mg_ctx_s *c;
+    ~Back() { mark(c, c->cur_level); }
+  } back{c};
   const int bs = c->bs();
   const int64_t ns = h.pat.n_send;
   if (ns > 0) {
@@ -775,7 +801,11 @@ mg_status do_restrict(mg_ctx_s *c, int l, const double *r, double *d) {
   const int bs = c->bs();
   TRY(halo_exchange(c, L.hr, r));
   TRY(launch_transfer(bs, false, L.R, in_of(L, L.hr, r), d + L.r_row0 * bs, c->stream));
-  if (L.agglomerate) TRY(c->tr->allgatherv(d + L.r_row0 * bs, d, L.ag_counts, L.ag_displs, c->stream));
+  if (L.agglomerate) {
+    mark(c, 200 + l);
+    TRY(c->tr->allgatherv(d + L.r_row0 * bs, d, L.ag_counts, L.ag_displs, c->stream));
+    mark(c, l);
+  }
   return MG_OK;
 }
 
@@ -819,6 +849,8 @@ mg_status coarse_solve(mg_ctx_s *c, const double *b, double *x) {
 
 // GMG(l, x, b) of Alg. gmg; zero: x enters as 0.
 mg_status vcycle_rec(mg_ctx_s *c, int l, double *x, const double *b, bool zero) {
+  c->cur_level = l;
+  mark(c, l);
   if (l == 0) return coarse_solve(c, b, x);  // Step 0; ignores x (Z21)
   Level &L = c->lv[l];
   Level &C = c->lv[l - 1];
@@ -826,6 +858,8 @@ mg_status vcycle_rec(mg_ctx_s *c, int l, double *x, const double *b, bool zero) 
   TRY(a_pass_resid(c, l, x, b, L.w.p));              // Step 2: r = b - A x
   TRY(do_restrict(c, l, L.w.p, C.b.p));              //         d = R r
   TRY(vcycle_rec(c, l - 1, C.x.p, C.b.p, true));     // Step 3
+  c->cur_level = l;
+  mark(c, l);
   TRY(do_prolong(c, l, C.x.p, x));                   // Step 4
   return smooth(c, l, x, b, lv_nu_post(c, L), false);  // Step 5
 }
@@ -1362,6 +1396,34 @@ mg_status mg_dot(mg_ctx c, int level, const double *a, const double *b, double *
 }
 
 int64_t mgi_launch_count(mgi_ctx c) { return c ? c->launches : -1; }
+
+int mgi_vcycle_profile(mgi_ctx c, double *x, const double *b, int zero, double *out, int n_out) {
+  if (!c || !x || !b || !out) return MG_ERR_INVALID_ARG;
+  const int nl = c->L() + 1;
+  if (n_out < 2 * nl + 1) return MG_ERR_DIMENSION;
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  TRY(finalize(c));
+  for (auto &pe : c->prof) cudaEventDestroy(pe.second);
+  c->prof.clear();
+  c->prof_on = true;
+  const mg_status st = vcycle_rec(c, c->L(), x, b, zero != 0);
+  mark(c, -1);
+  c->prof_on = false;
+  CU(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < 2 * nl + 1; ++i) out[i] = 0.0;
+  for (size_t i = 0; i + 1 < c->prof.size(); ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->prof[i].second, c->prof[i + 1].second);
+    const int tag = c->prof[i].first;
+    if (tag >= 200) out[2 * nl] += ms;
+    else if (tag >= 100) out[nl + tag - 100] += ms;
+    else if (tag >= 0) out[tag] += ms;
+  }
+  for (auto &pe : c->prof) cudaEventDestroy(pe.second);
+  c->prof.clear();
+  return st;
+}
 
 int mgi_level_info(mgi_ctx c, int level, int64_t *n, int64_t *nnzb, int64_t *sell_entries, int64_t *nnz_p,
                    int64_t *sell_entries_p, int64_t *sell_entries_r) {

@@ -338,3 +338,18 @@ def test_user_smoother_override_matches_oracle():
     sc = np.abs(x0) + 0.6 * np.abs(t)
     assert_close_scaled(host(x), exp, sc + absA_x(L, x0), what="override sweep")
     gpu_mg.cache_clear()
+
+
+def test_vcycle_profile_split_and_result():
+    """mgi_vcycle_profile: per-level split of an eager V-cycle; the result is the
+    same V-cycle (bit-identical to the graph-launched one)."""
+    import paper_2405_05047_b200 as m
+    lv, bs, om, b, H = case("c3_small")
+    mg = gpu_mg("c3_small")
+    z1 = dev(np.zeros(lv[-1].n * bs))
+    prof = m.vcycle_profile(mg.ctx, z1, dev(b), len(lv))
+    z2 = dev(np.zeros(lv[-1].n * bs))
+    m.mg_vcycle_zero(mg.ctx, z2, dev(b))
+    assert np.array_equal(host(z1), host(z2))
+    assert len(prof["level_ms"]) == len(lv) and all(t > 0 for t in prof["level_ms"])
+    assert all(t == 0 for t in prof["halo_ms"]) and prof["agglomeration_ms"] == 0

@@ -231,3 +231,28 @@ def test_localize_columns_bruteforce():
         assert list(gh[:ng.value]) == ghosts
         back = np.where(loc < r1 - r0, loc + r0, np.array(ghosts + [0])[np.maximum(loc - (r1 - r0), 0)])
         assert np.array_equal(back, col)
+
+
+def test_nccl_transport_loads_and_makes_unique_id():
+    """The NCCL transport is dlopen'd: the library loads without it, and
+    mg_get_unique_id (rank 0's bootstrap id) works without a GPU."""
+    import paper_2405_05047_b200 as m
+    uid = m.mg_get_unique_id()
+    assert len(uid) == 128 and any(uid)
+    assert uid != m.mg_get_unique_id()
+
+
+def test_bench_byte_model_matches_survey():
+    """bench.py's algorithmic-byte model on a hand-checkable level."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    info = {"n": 10, "nnzb": 27, "nnz_p": 5}
+    sweep, sweep0, resid = bench.level_bytes(info, 3, False)
+    a_stream = 27 * (8 * 9 + 4) + 8 * 11
+    assert sweep == a_stream + 8 * 3 * 10 * 3 + 8 * 9 * 10
+    assert sweep0 == 16 * 3 * 10 + 8 * 9 * 10
+    assert resid == a_stream + 24 * 3 * 10
+    sweep32, _, _ = bench.level_bytes(info, 3, False, vb=4)
+    assert sweep - sweep32 == 27 * 4 * 9
