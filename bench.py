@@ -151,14 +151,27 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def oracle_vcycle_rate(P, n_cycles=1, warmup=0):
+_ORACLE_H = {}
+
+
+def oracle_vcycle_rate(P, n_cycles=1, warmup=0, threads=None):
     """The oracle (as it stands) timed on the host cores: V-cycles/s of
     GMG(L, 0, b) -- the preconditioner application of one GMRES step."""
     import oracle
-    cores = cpu_cores()
+    cores = threads or cpu_cores()
     oracle.set_threads(cores)
+    if id(P) in _ORACLE_H:
+        h = _ORACLE_H[id(P)]
+        L = len(P.levels) - 1
+        times = []
+        for _ in range(n_cycles):
+            t = time.perf_counter()
+            oracle.vcycle(h, L, np.zeros_like(P.b), P.b)
+            times.append(time.perf_counter() - t)
+        return times, cores
     t = time.time()
     h = oracle.MgHierarchy.from_arrays(P.levels, omega=P.omega, nu_pre=P.nu_pre, nu_post=P.nu_post)
+    _ORACLE_H[id(P)] = h
     log(f"[bench] oracle setup {time.time() - t:.1f}s on {cores} cores")
     L = len(P.levels) - 1
     for _ in range(warmup):
@@ -380,6 +393,18 @@ def run_ours(args):
         cpu = {"value": 1.0 / times[0], "unit": "V-cycles/s", "cores": cores, "kind": "oracle",
                "sample": f"one oracle V(2,2) GMG(L,0,b) on the full {args.config} ({N} DOFs), "
                          f"{times[0]:.2f} s, OpenMP over rows"}
+        # thread scan (1 thread, the paper's 8 threads, all cores); results are
+        # bit-identical across thread counts
+        scan = {}
+        for th in sorted({1, min(8, cores), cores}):
+            if th == cores:
+                scan[str(th)] = cpu["value"]
+                continue
+            tt, _ = oracle_vcycle_rate(P, n_cycles=1, threads=th)
+            scan[str(th)] = 1.0 / tt[0]
+        cpu["threads_scan_vcycles_per_s"] = scan
+        import oracle
+        oracle.set_threads(cores)
 
     if rank == 0:
         line = {
@@ -404,6 +429,8 @@ def run_ours(args):
             "solve_ms": t_ms / args.steps,
             "solve_dofs_per_s": n_global / (t_ms / args.steps / 1e3),
             "vcycle_levels": {"rows_rank0": [i["n"] for i in infos], "ms": prof["level_ms"],
+                              "eager_total_ms": sum(prof["level_ms"]) + sum(prof["halo_ms"])
+                              + prof["agglomeration_ms"],
                               "halo_ms": prof["halo_ms"], "agglomeration_ms": prof["agglomeration_ms"],
                               "note": "one eager V(2,2) from zero, CUDA events between phases"},
             "mixed_precision": mixed,

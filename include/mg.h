@@ -261,6 +261,12 @@ mg_status mg_coarse_solve(mg_ctx ctx, const double *d, double *y);
 /* x <- H x on the finest level.  In place (uses a work vector). */
 mg_status mg_apply_constraints(mg_ctx ctx, double *x);
 
+/* b_bar = H^T b on the finest level: condensation of an unconstrained load
+ * vector onto the regular nodes (the "distributing" hanging-node operation of
+ * P:338).  Hanging entries of b_bar come out 0 (hanging nodes are never
+ * masters).  b_bar must not alias b. */
+mg_status mg_condense_rhs(mg_ctx ctx, const double *b, double *b_bar);
+
 /* *out_host = (a, b) over the level's rows (deterministic single-pass grid
  * reduction; all-reduced over ranks).  Synchronises. */
 mg_status mg_dot(mg_ctx ctx, int level, const double *a, const double *b, double *out_host);

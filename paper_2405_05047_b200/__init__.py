@@ -91,6 +91,7 @@ _SIGS = {
     "mg_prolong_add": [_P, _I, _P, _P],
     "mg_coarse_solve": [_P, _P, _P],
     "mg_apply_constraints": [_P, _P],
+    "mg_condense_rhs": [_P, _P, _P],
     "mg_dot": [_P, _I, _P, _P, ctypes.POINTER(_D)],
 }
 for _name, _args in _SIGS.items():
@@ -277,6 +278,10 @@ def mg_coarse_solve(ctx, d, y):
 
 def mg_apply_constraints(ctx, x):
     _check(_lib.mg_apply_constraints(ctx, _dptr(x)), "mg_apply_constraints")
+
+
+def mg_condense_rhs(ctx, b, b_bar):
+    _check(_lib.mg_condense_rhs(ctx, _dptr(b), _dptr(b_bar)), "mg_condense_rhs")
 
 
 def mg_dot(ctx, level, a, b) -> float:

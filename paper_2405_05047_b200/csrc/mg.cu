@@ -236,8 +236,8 @@ struct mg_ctx_s {
   int n_sm = 148;
   std::unique_ptr<mgc::Transport> tr;  // null => single GPU
   std::vector<Level> lv;
-  SellOp H;
-  Halo hh;
+  SellOp H, HT;     // hanging-node matrix H (averaging) and H^T (distributing)
+  Halo hh, hht_halo;
   DevArray<double> cinv;  // dense A_0^-1, row stride cld
   int64_t cN = 0, cld = 0;
   DevArray<double> red_part, scal;
@@ -966,6 +966,47 @@ mg_status ensure_gmres(mg_ctx_s *c, int m) {
   return MG_OK;
 }
 
+// Transpose setup across ranks: route every entry (local row i of level L,
+// global column J, weights) to the rank that computes row J of the transpose
+// (output row ranges rb).  Arrival order: source ranks ascending, each in CSR
+// order -> the stable assembly lists the original rows ascending.  Collective.
+mg_status route_entries(mg_ctx_s *c, const Level &L, const std::vector<int64_t> &rp, const std::vector<int64_t> &cl,
+                        const std::vector<double> &v, int wpe, const std::vector<int64_t> &rb,
+                        std::vector<int64_t> &J, std::vector<int64_t> &I, std::vector<double> &W) {
+  const int P = c->nranks();
+  std::vector<std::vector<char>> out(P), in;
+  const size_t rec = sizeof(int64_t) * 2 + sizeof(double) * wpe;
+  std::vector<int64_t> cnt(P, 0);
+  for (size_t t = 0; t < cl.size(); ++t) cnt[mgi_owner(cl[t], rb.data(), P)]++;
+  for (int r = 0; r < P; ++r) out[r].resize(size_t(cnt[r]) * rec);
+  std::vector<size_t> pos(P, 0);
+  for (int64_t i = 0; i < L.n; ++i)
+    for (int64_t t = rp[i]; t < rp[i + 1]; ++t) {
+      const int o = mgi_owner(cl[t], rb.data(), P);
+      char *dst = out[o].data() + pos[o];
+      const int64_t gi = L.row_begin + i;
+      std::memcpy(dst, &cl[t], 8);
+      std::memcpy(dst + 8, &gi, 8);
+      std::memcpy(dst + 16, &v[size_t(t) * wpe], sizeof(double) * wpe);
+      pos[o] += rec;
+    }
+  TRY(c->tr->alltoallv_host(out, in));
+  J.clear();
+  I.clear();
+  W.clear();
+  for (int r = 0; r < P; ++r)
+    for (size_t off = 0; off < in[r].size(); off += rec) {
+      int64_t j, i;
+      std::memcpy(&j, in[r].data() + off, 8);
+      std::memcpy(&i, in[r].data() + off + 8, 8);
+      J.push_back(j);
+      I.push_back(i);
+      const double *ww = reinterpret_cast<const double *>(in[r].data() + off + 16);
+      W.insert(W.end(), ww, ww + wpe);
+    }
+  return MG_OK;
+}
+
 // validated host copies of a CSR/BSR input
 mg_status fetch_csr(mg_ctx_s *c, int64_t n, int64_t n_cols, const int64_t *row_ptr, const int64_t *col,
                     const double *vals, int64_t nnz, int vpe, int mem, bool need_diag, int64_t diag_offset,
@@ -1173,36 +1214,9 @@ mg_status mg_set_transfer(mg_ctx c, int fine_level, const int64_t *row_ptr, cons
     } else {
       for (int r = 0; r <= P; ++r) rb[r] = C.n_global * r / P;
     }
-    // route every P entry (i_fine, J) to the rank computing R row J
-    std::vector<std::vector<char>> out(P), in;
-    const size_t rec = sizeof(int64_t) * 2 + sizeof(double) * wpe;
-    std::vector<int64_t> cnt(P, 0);
-    for (int64_t t = 0; t < nnz; ++t) cnt[mgi_owner(cl[t], rb.data(), P)]++;
-    for (int r = 0; r < P; ++r) out[r].resize(size_t(cnt[r]) * rec);
-    std::vector<size_t> pos(P, 0);
-    for (int64_t i = 0; i < L.n; ++i)
-      for (int64_t t = rp[i]; t < rp[i + 1]; ++t) {
-        const int o = mgi_owner(cl[t], rb.data(), P);
-        char *dst = out[o].data() + pos[o];
-        const int64_t gi = L.row_begin + i;
-        std::memcpy(dst, &cl[t], 8);
-        std::memcpy(dst + 8, &gi, 8);
-        std::memcpy(dst + 16, &v[size_t(t) * wpe], sizeof(double) * wpe);
-        pos[o] += rec;
-      }
-    TRY(c->tr->alltoallv_host(out, in));
     std::vector<int64_t> J, I;
     std::vector<double> W;
-    for (int r = 0; r < P; ++r)
-      for (size_t off = 0; off < in[r].size(); off += rec) {
-        int64_t j, i;
-        std::memcpy(&j, in[r].data() + off, 8);
-        std::memcpy(&i, in[r].data() + off + 8, 8);
-        J.push_back(j);
-        I.push_back(i);
-        const double *ww = reinterpret_cast<const double *>(in[r].data() + off + 16);
-        W.insert(W.end(), ww, ww + wpe);
-      }
+    TRY(route_entries(c, L, rp, cl, v, wpe, rb, J, I, W));
     // output offset into the coarse vector: local rows start at 0 on a
     // distributed coarse level; the full vector is addressed when replicated
     L.r_row0 = C.dist ? 0 : rb[me];
@@ -1269,6 +1283,28 @@ mg_status mg_set_constraints(mg_ctx c, const int64_t *H_row_ptr, const int64_t *
   std::vector<int64_t> rp, cl;
   std::vector<double> v;
   TRY(fetch_csr(c, F.n, F.n_global, H_row_ptr, H_col, H_w, nnz, 1, mem, false, 0, rp, cl, v, "H"));
+  // H^T (the "distributing" operation of P:338): rows = my fine rows
+  std::vector<int64_t> trp(F.n + 1), tcl;
+  std::vector<double> tv;
+  if (!F.dist) {
+    tcl.resize(nnz);
+    tv.resize(nnz);
+    mgi_csr_transpose(F.n, F.n, rp.data(), cl.data(), v.data(), 1, trp.data(), tcl.data(), tv.data());
+    c->hht_halo = Halo();
+  } else {
+    std::vector<int64_t> J, I;
+    std::vector<double> W;
+    TRY(route_entries(c, F, rp, cl, v, 1, F.bounds, J, I, W));
+    tcl.resize(J.size());
+    tv.resize(J.size());
+    const int st = mgi_assemble_routed_rows(int64_t(J.size()), J.data(), I.data(), W.data(), 1, F.row_begin, F.n,
+                                            trp.data(), tcl.data(), tv.data());
+    if (st) return fail(MG_ERR_STRUCTURE, "H^T routing failed");
+    std::vector<int64_t> ghosts;
+    TRY(localize(F.row_begin, F.row_end, trp, tcl, ghosts));
+    TRY(build_halo(c, c->hht_halo, ghosts, F.bounds, F.row_begin, F.row_end));
+  }
+  TRY(build_sell(c->HT, F.n, trp.data(), tcl.data(), tv.data(), 1));
   if (F.dist) {
     std::vector<int64_t> ghosts;
     TRY(localize(F.row_begin, F.row_end, rp, cl, ghosts));
@@ -1381,6 +1417,18 @@ mg_status mg_apply_constraints(mg_ctx c, double *x) {
                       c->stream));
   if (F.n) CU(cudaMemcpyAsync(x, F.w.p, size_t(F.n) * c->bs() * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   return MG_OK;
+}
+
+mg_status mg_condense_rhs(mg_ctx c, const double *b, double *b_bar) {
+  TRY(check_ctx(c));
+  if (!b || !b_bar || b == b_bar) return fail(MG_ERR_INVALID_ARG, "b, b_bar must be distinct non-NULL device pointers");
+  if (!c->HT.set) return fail(MG_ERR_STATE, "no hanging-node matrix (mg_set_constraints)");
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  Level &F = c->lv[c->L()];
+  TRY(halo_exchange(c, c->hht_halo, b));
+  return launch_transfer(c->bs(), false, c->HT, In{b, c->hht_halo.active ? c->hht_halo.ghost.p : nullptr, int(F.n)},
+                         b_bar, c->stream);
 }
 
 mg_status mg_dot(mg_ctx c, int level, const double *a, const double *b, double *out_host) {

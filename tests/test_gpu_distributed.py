@@ -150,6 +150,9 @@ def test_distributed_per_op(name, P):
         hx = dev(sl(xs[Lf], Lf, r))
         m.mg_apply_constraints(mgs[r].ctx, hx)
         res["H"] = host(hx)
+        ht = dev(np.zeros(len(sl(xs[Lf], Lf, r))))
+        m.mg_condense_rhs(mgs[r].ctx, dev(sl(bb[Lf], Lf, r)), ht)
+        res["HT"] = host(ht)
         return res
     out = run_ranks(P, ops)
     s = build_gpu(Pr.levels, bs, omega=Pr.omega, H=Pr.fine.H)
@@ -177,6 +180,9 @@ def test_distributed_per_op(name, P):
     hx = dev(xs[Lf])
     m.mg_apply_constraints(s.ctx, hx)
     assert np.array_equal(np.concatenate([o["H"] for o in out]), host(hx))
+    ht = dev(np.zeros(Pr.n_dof))
+    m.mg_condense_rhs(s.ctx, dev(bb[Lf]), ht)
+    assert np.array_equal(np.concatenate([o["HT"] for o in out]), host(ht))
 
 
 @pytest.mark.parametrize("name,P", [("c3_small", 2), ("c3_mid", 4), ("c2_small", 3), ("c5_mid", 2)])

@@ -353,3 +353,28 @@ def test_vcycle_profile_split_and_result():
     assert np.array_equal(host(z1), host(z2))
     assert len(prof["level_ms"]) == len(lv) and all(t > 0 for t in prof["level_ms"])
     assert all(t == 0 for t in prof["halo_ms"]) and prof["agglomeration_ms"] == 0
+
+
+@pytest.mark.parametrize("name", ["c2_small", "c3_small", "c4_small"])
+def test_condense_rhs_is_HT(name):
+    """b_bar = H^T b ("distributing"); hanging entries come out 0."""
+    import paper_2405_05047_b200 as m
+    lv, bs, om, b, H = case(name)
+    mg = gpu_mg(name)
+    F = lv[-1]
+    v = rng(70).standard_normal(F.n * bs)
+    out = dev(np.full(F.n * bs, np.nan))
+    m.mg_condense_rhs(mg.ctx, dev(v), out)
+    trp, tcol, tw = oracle.csr_transpose(F.n, F.n, *H)
+    exp = oracle.transfer(F.n, bs, trp, tcol, tw, 1, v)
+    sc = oracle.transfer(F.n, bs, trp, tcol, np.abs(tw), 1, np.abs(v))
+    got = host(out)
+    assert_close_scaled(got, exp, sc, what=f"{name} H^T")
+    hang = np.diff(H[0]) > 1                       # hanging rows of H hold 2 or 4 master weights
+    assert np.all(got.reshape(-1, bs)[hang] == 0.0)  # hanging nodes are never masters: column empty
+    # adjoint identity (H^T b, x) = (b, H x) up to rounding
+    x0 = rng(71).standard_normal(F.n * bs)
+    hx = dev(x0)
+    m.mg_apply_constraints(mg.ctx, hx)
+    lhs, rhs = float(got @ x0), float(v @ host(hx))
+    assert abs(lhs - rhs) <= 1e-12 * (np.abs(got) @ np.abs(x0) + np.abs(v) @ np.abs(host(hx)))
