@@ -184,6 +184,16 @@ mg_status mg_create_level(mg_ctx ctx, int level, int64_t n_rows_global, int64_t 
 mg_status mg_set_matrix(mg_ctx ctx, int level, const int64_t *row_ptr, const int64_t *col,
                         const double *vals, int64_t nnzb, int mem);
 
+/* Replace the VALUES of level `level`'s matrix, keeping the sparsity of the
+ * last mg_set_matrix (the Newton / time-step re-upload of P:821): vals
+ * [nnzb * bs * bs] in the same BSR entry order.  Scattered into the device
+ * layout through a stored index map, D^-1 (unless user-supplied) and, on
+ * level 0 with the direct coarse solve, the dense coarse inverse are rebuilt
+ * on the device; halo plans and captured CUDA graphs stay valid.  Rank-local
+ * (no communication).  Synchronises.  MG_ERR_NONFINITE / MG_ERR_SINGULAR as
+ * for mg_set_matrix. */
+mg_status mg_update_matrix(mg_ctx ctx, int level, const double *vals, int mem);
+
 /* Set P_{fine_level-1}: level fine_level-1 -> level fine_level (n_fine x
  * n_coarse CSR).  The restriction R = P^T is built by the
  * library with a stable counting sort (columns of each R row ascending). */

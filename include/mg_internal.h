@@ -53,6 +53,12 @@ int mgi_sell_fill_f32(int64_t n, const int64_t *row_ptr, const int64_t *col_in, 
                       int vpe, int sigma, int64_t *slice_ptr, int32_t *perm, int32_t *col,
                       float *val);
 
+/* Value-update map of a SELL-32-sigma layout (mg_update_matrix): map[k] = the
+ * SELL entry e holding original CSR entry k (k < row_ptr[n]); row_pos[r] =
+ * slice*32 + lane of row r (row_pos may be NULL). */
+int mgi_sell_entry_map(int64_t n, const int64_t *row_ptr, const int64_t *slice_ptr, const int32_t *perm,
+                       int64_t *map, int32_t *row_pos);
+
 /* Stable counting-sort transpose (R = P^T): out_row_ptr[n_cols+1],
  * out_col[nnz], out_w[nnz*wpe]; entries of each output row in ascending
  * input-row order. */

@@ -75,6 +75,7 @@ _SIGS = {
     "mg_create": [ctypes.POINTER(_P), ctypes.POINTER(mg_config), _I, _P, ctypes.POINTER(mg_comm)],
     "mg_create_level": [_P, _I, _I64, _I64, _I64],
     "mg_set_matrix": [_P, _I, _P, _P, _P, _I64, _I],
+    "mg_update_matrix": [_P, _I, _P, _I],
     "mg_set_transfer": [_P, _I, _P, _P, _P, _I64, _I, _I],
     "mg_set_smoother": [_P, _I, _D, _I, _I, _P, _I],
     "mg_set_constraints": [_P, _P, _P, _P, _I64, _I],
@@ -203,6 +204,11 @@ def mg_set_matrix(ctx, level, row_ptr, col, vals):
     nnzb = int(col.shape[0])
     _check(_lib.mg_set_matrix(ctx, level, _ptr(row_ptr, np.int64)[0], _ptr(col, np.int64)[0],
                               _ptr(vals, np.float64)[0], nnzb, mem), "mg_set_matrix")
+
+
+def mg_update_matrix(ctx, level, vals):
+    p, mem = _ptr(vals, np.float64)
+    _check(_lib.mg_update_matrix(ctx, level, p, mem), "mg_update_matrix")
 
 
 def mg_set_transfer(ctx, fine_level, row_ptr, col, w, weights_per_entry=1):

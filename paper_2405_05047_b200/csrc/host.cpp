@@ -181,6 +181,20 @@ int mgi_sell_fill_f32(int64_t n, const int64_t *rp, const int64_t *col_in, const
   return sell_fill<float>(n, rp, col_in, val_in, vpe, sigma, slice_ptr, perm, col, val);
 }
 
+int mgi_sell_entry_map(int64_t n, const int64_t *rp, const int64_t *slice_ptr, const int32_t *perm, int64_t *map,
+                       int32_t *row_pos) {
+  const int64_t ns = (n + kSlice - 1) / kSlice;
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t s = 0; s < ns; ++s)
+    for (int lane = 0; lane < kSlice; ++lane) {
+      const int32_t r = perm[s * kSlice + lane];
+      if (r < 0) continue;
+      if (row_pos) row_pos[r] = int32_t(s * kSlice + lane);
+      for (int64_t k = 0; k < rp[r + 1] - rp[r]; ++k) map[rp[r] + k] = slice_ptr[s] + k * kSlice + lane;
+    }
+  return 0;
+}
+
 int mgi_csr_transpose(int64_t n_rows, int64_t n_cols, const int64_t *rp, const int64_t *col,
                       const double *w, int wpe, int64_t *orp, int64_t *ocol, double *ow) {
   if (n_rows < 0 || n_cols < 0 || wpe < 1) return MG_ERR_INVALID_ARG;

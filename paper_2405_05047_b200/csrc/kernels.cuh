@@ -555,6 +555,123 @@ __global__ void k_sqrt_copy(double *p, double *copy) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Value-only matrix update (mg_update_matrix): same structure, new values.
+// ---------------------------------------------------------------------------
+// element j of SELL entry e (chunked fp64 layout / fp32 layout)
+__device__ __forceinline__ int64_t sell_off64(int64_t e, int V, int j) {
+  const int lane = int(e & 31);
+  const int64_t base = (e - lane) * V;
+  return j < 2 * (V / 2) ? base + 64 * (j / 2) + 2 * lane + (j % 2) : base + 64 * (V / 2) + lane;
+}
+__device__ __forceinline__ int64_t sell_off32(int64_t e, int V, int j) {
+  const int lane = int(e & 31);
+  const int64_t base = (e - lane) * V;
+  const int q = V / 4;
+  return j < 4 * q ? base + 128 * (j / 4) + 4 * lane + (j % 4) : base + 128 * q + 32 * (j - 4 * q) + lane;
+}
+
+// original BSR entry k (V = bs*bs row-major values) -> SELL entry map[k],
+// chunked fp64 layout (out64) or fp32 layout (out32, rounded to nearest)
+__global__ void k_scatter_values(int64_t nnz, int V, const int64_t *__restrict__ map, const double *__restrict__ vals,
+                                 double *__restrict__ out64, float *__restrict__ out32, int *flag) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < nnz; k += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t e = map[k];
+    for (int j = 0; j < V; ++j) {
+      const double v = vals[k * V + j];
+      if (!isfinite(v)) atomicOr(flag, 1);
+      if (out32) out32[sell_off32(e, V, j)] = float(v);
+      else out64[sell_off64(e, V, j)] = v;
+    }
+  }
+}
+
+// D^-1 of the diagonal blocks (read from the SELL operator at entries diag_e)
+// by Gauss-Jordan with partial pivoting (max |a|, ties -> lowest row), the
+// operation sequence of the host mgi_block_diag_inverse with explicit
+// round-to-nearest intrinsics (no FMA contraction).  Written to the sliced
+// D^-1 layout at row_pos.  flag |= 2 on a singular block.
+template <int BS>
+__global__ void k_block_inverse(int64_t n, const int64_t *__restrict__ diag_e, const double *__restrict__ val64,
+                                const float *__restrict__ val32, const int32_t *__restrict__ row_pos,
+                                double *__restrict__ dinv, int *flag) {
+  constexpr int V = BS * BS;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    double a[V], inv[V];
+    const int64_t e = diag_e[i];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      a[j] = val32 ? double(val32[sell_off32(e, V, j)]) : val64[sell_off64(e, V, j)];
+      inv[j] = 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < BS; ++r) inv[r * BS + r] = 1.0;
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < BS; ++k) {
+      int p = k;
+      double best = fabs(a[k * BS + k]);
+#pragma unroll
+      for (int r = k + 1; r < BS; ++r) {
+        const double v = fabs(a[r * BS + k]);
+        if (v > best) best = v, p = r;
+      }
+      if (!(best > 0.0)) ok = false;
+      if (!ok) continue;
+      if (p != k) {
+#pragma unroll
+        for (int c = 0; c < BS; ++c) {
+          double t = a[k * BS + c];
+          a[k * BS + c] = a[p * BS + c];
+          a[p * BS + c] = t;
+          t = inv[k * BS + c];
+          inv[k * BS + c] = inv[p * BS + c];
+          inv[p * BS + c] = t;
+        }
+      }
+      const double d = a[k * BS + k];
+#pragma unroll
+      for (int c = 0; c < BS; ++c) {
+        a[k * BS + c] = __ddiv_rn(a[k * BS + c], d);
+        inv[k * BS + c] = __ddiv_rn(inv[k * BS + c], d);
+      }
+#pragma unroll
+      for (int r = 0; r < BS; ++r) {
+        if (r == k) continue;
+        const double f = a[r * BS + k];
+        if (f == 0.0) continue;
+#pragma unroll
+        for (int c = 0; c < BS; ++c) {
+          a[r * BS + c] = __dsub_rn(a[r * BS + c], __dmul_rn(f, a[k * BS + c]));
+          inv[r * BS + c] = __dsub_rn(inv[r * BS + c], __dmul_rn(f, inv[k * BS + c]));
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+      if (!isfinite(inv[j])) ok = false;
+    if (!ok) atomicOr(flag, 2);
+    const int pos = row_pos[i];
+    const int lane = pos & 31;
+    double *base = dinv + int64_t(pos >> 5) * 32 * V;
+#pragma unroll
+    for (int j = 0; j < 2 * (V / 2); ++j) base[64 * (j / 2) + 2 * lane + (j % 2)] = ok ? inv[j] : 0.0;
+    if (V & 1) base[64 * (V / 2) + lane] = ok ? inv[V - 1] : 0.0;
+  }
+}
+
+// dense (row-major, leading dimension ld) coarse matrix from BSR entries
+__global__ void k_dense_scatter(int64_t nnzb, int bs, const int32_t *__restrict__ brow, const int32_t *__restrict__ bcol,
+                                const double *__restrict__ vals, int round32, int64_t ld, double *__restrict__ dense) {
+  const int V = bs * bs;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < nnzb * V; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t k = t / V;
+    const int j = int(t % V), r = j / bs, c = j % bs;
+    const double v = vals[t];
+    dense[(int64_t(brow[k]) * bs + r) * ld + int64_t(bcol[k]) * bs + c] = round32 ? double(float(v)) : v;
+  }
+}
+
 // x += z
 __global__ void k_axpy1(int64_t n, const double *__restrict__ z, double *__restrict__ x) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)

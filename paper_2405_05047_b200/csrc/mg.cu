@@ -131,7 +131,7 @@ struct SellOp {
 // Build SELL-32-sigma on the host and upload it (col: LOCAL column indices);
 // f32: values rounded to fp32 in the fp32 chunk layout.
 mg_status build_sell(SellOp &op, int64_t n, const int64_t *rp, const int64_t *col, const double *val, int vpe,
-                     bool f32 = false) {
+                     bool f32 = false, std::vector<int64_t> *sp_out = nullptr) {
   int64_t ns = 0, ne = 0;
   int st = mgi_sell_size(n, rp, kSigma, &ns, &ne);
   if (st) return fail(mg_status(st), "sell layout: invalid input");
@@ -153,6 +153,7 @@ mg_status build_sell(SellOp &op, int64_t n, const int64_t *rp, const int64_t *co
   TRY(op.perm.upload(perm.data(), perm.size()));
   TRY(op.col.upload(c.data(), c.size()));
   op.perm_host.swap(perm);
+  if (sp_out) sp_out->swap(sp);
   op.n_rows = n;
   op.n_slices = ns;
   op.n_entries = ne;
@@ -195,8 +196,12 @@ struct Level {
   SellOp A64;                     // mixed precision, finest level: fp64 operator for Krylov / residuals
   int64_t nnzb = 0;
   Halo hx;                        // ghosts of x for A-passes on this level
-  std::vector<double> diag_host;  // diagonal blocks until D^-1 is built
   std::vector<double> dinv_host;  // user-supplied D^-1 (row-major blocks)
+  // value-update maps (mg_update_matrix): original entry -> SELL entry, SELL
+  // entry of each row's diagonal block, slice position of each row
+  DevArray<int64_t> umap, udiag_e;
+  DevArray<int32_t> upos;
+  DevArray<int32_t> ublk_row, ublk_col;  // level 0: block coordinates for the dense coarse matrix
   std::vector<int64_t> rp0, col0;  // level-0 copy for the dense coarse inverse
   std::vector<double> val0;
   DevArray<double> dinv;  // sliced D^-1 (chunked like a 1-entry slice)
@@ -655,6 +660,9 @@ __global__ void k_gj_unswap(int64_t N, int64_t ld, double *a, const int64_t *piv
   }
 }
 
+// in-place Gauss-Jordan inversion of the dense coarse matrix held in c->cinv
+mg_status coarse_gj(mg_ctx_s *c, int64_t N, int64_t ld);
+
 mg_status build_coarse_inverse(mg_ctx_s *c) {
   Level &L0 = c->lv[0];
   const int bs = c->bs();
@@ -665,6 +673,10 @@ mg_status build_coarse_inverse(mg_ctx_s *c) {
   std::vector<double> padded(size_t(N) * ld, 0.0);
   for (int64_t r = 0; r < N; ++r) std::memcpy(&padded[r * ld], &dense[r * N], N * sizeof(double));
   TRY(c->cinv.upload(padded.data(), padded.size()));
+  return coarse_gj(c, N, ld);
+}
+
+mg_status coarse_gj(mg_ctx_s *c, int64_t N, int64_t ld) {
   DevArray<int64_t> piv;
   DevArray<double> f;
   DevArray<int> sing;
@@ -710,6 +722,36 @@ mg_status upload_dinv(Level &L, int bs, const std::vector<double> &blocks) {
   return MG_OK;
 }
 
+// D^-1 of the level's diagonal blocks on the device (from the V-cycle operator's
+// values: fp32-rounded in mixed precision).  Synchronises.
+mg_status device_dinv(mg_ctx_s *c, int l) {
+  Level &L = c->lv[l];
+  const int bs = c->bs(), V = bs * bs;
+  if (L.dinv.n < size_t(L.A.n_slices) * 32 * V) TRY(L.dinv.alloc(size_t(std::max<int64_t>(1, L.A.n_slices)) * 32 * V));
+  CU(cudaMemsetAsync(L.dinv.p, 0, L.dinv.n * sizeof(double), c->stream));
+  DevArray<int> flag;
+  TRY(flag.alloc(1));
+  CU(cudaMemsetAsync(flag.p, 0, sizeof(int), c->stream));
+  if (L.n > 0) {
+    const unsigned g = unsigned(std::min<int64_t>((L.n + 255) / 256, 16 * c->n_sm));
+    const double *v64 = L.A.f32 ? nullptr : L.A.val.p;
+    const float *v32 = L.A.f32 ? L.A.valf.p : nullptr;
+    switch (bs) {
+      case 1: mgk::k_block_inverse<1><<<g, 256, 0, c->stream>>>(L.n, L.udiag_e.p, v64, v32, L.upos.p, L.dinv.p, flag.p); break;
+      case 2: mgk::k_block_inverse<2><<<g, 256, 0, c->stream>>>(L.n, L.udiag_e.p, v64, v32, L.upos.p, L.dinv.p, flag.p); break;
+      case 3: mgk::k_block_inverse<3><<<g, 256, 0, c->stream>>>(L.n, L.udiag_e.p, v64, v32, L.upos.p, L.dinv.p, flag.p); break;
+      default: mgk::k_block_inverse<4><<<g, 256, 0, c->stream>>>(L.n, L.udiag_e.p, v64, v32, L.upos.p, L.dinv.p, flag.p); break;
+    }
+    TRY(check_launch("block inverse"));
+  }
+  int f = 0;
+  CU(cudaMemcpyAsync(&f, flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (f & 2) return fail(MG_ERR_SINGULAR, "level %d: singular diagonal block", l);
+  L.dinv_ready = true;
+  return MG_OK;
+}
+
 double lv_omega(const mg_ctx_s *c, const Level &L) { return L.omega > 0.0 ? L.omega : c->cfg.omega; }
 int lv_nu_pre(const mg_ctx_s *c, const Level &L) { return L.nu_pre >= 0 ? L.nu_pre : c->cfg.nu_pre; }
 int lv_nu_post(const mg_ctx_s *c, const Level &L) { return L.nu_post >= 0 ? L.nu_post : c->cfg.nu_post; }
@@ -731,20 +773,8 @@ mg_status finalize(mg_ctx_s *c) {
   for (int l = 0; l <= c->L(); ++l) {
     Level &L = c->lv[l];
     if (!L.dinv_ready) {
-      if (!L.dinv_host.empty()) {
-        TRY(upload_dinv(L, bs, L.dinv_host));
-      } else {
-        const int V = bs * bs;
-        std::vector<double> inv(size_t(L.n) * V);
-        std::vector<int64_t> rp(L.n + 1), cl(L.n);
-        for (int64_t i = 0; i <= L.n; ++i) rp[i] = i;
-        for (int64_t i = 0; i < L.n; ++i) cl[i] = i;
-        const int st = mgi_block_diag_inverse(L.n, bs, rp.data(), cl.data(), L.diag_host.data(), inv.data());
-        if (st == MG_ERR_SINGULAR) return fail(MG_ERR_SINGULAR, "level %d: singular diagonal block", l);
-        if (st) return fail(mg_status(st), "level %d: D^-1 failed", l);
-        TRY(upload_dinv(L, bs, inv));
-      }
-      std::vector<double>().swap(L.diag_host);
+      if (!L.dinv_host.empty()) TRY(upload_dinv(L, bs, L.dinv_host));
+      else TRY(device_dinv(c, l));
     }
     const size_t nv = size_t(std::max<int64_t>(1, L.n)) * bs;
     if (L.w.n < nv) TRY(L.w.alloc(nv));
@@ -1149,17 +1179,38 @@ mg_status mg_set_matrix(mg_ctx c, int level, const int64_t *row_ptr, const int64
     if (level == c->L()) v64 = v;
     for (double &a : v) a = double(float(a));
   }
-  L.diag_host.assign(size_t(L.n) * V, 0.0);
+  std::vector<int64_t> diag_k(L.n, -1);
   for (int64_t i = 0; i < L.n; ++i)
     for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
-      if (cl[k] == L.row_begin + i) std::memcpy(&L.diag_host[size_t(i) * V], &v[size_t(k) * V], V * sizeof(double));
+      if (cl[k] == L.row_begin + i) diag_k[i] = k;
+  std::vector<int32_t> brow, bcol;
+  if (level == 0 && !L.dist) {
+    brow.resize(nnzb);
+    bcol.resize(nnzb);
+    for (int64_t i = 0; i < L.n; ++i)
+      for (int64_t k = rp[i]; k < rp[i + 1]; ++k) brow[k] = int32_t(i), bcol[k] = int32_t(cl[k]);
+  }
   if (L.dist) {
     std::vector<int64_t> ghosts;
     TRY(localize(L.row_begin, L.row_end, rp, cl, ghosts));
     TRY(build_halo(c, L.hx, ghosts, L.bounds, L.row_begin, L.row_end));
   }
-  TRY(build_sell(L.A, L.n, rp.data(), cl.data(), v.data(), V, mixed));
+  std::vector<int64_t> sp;
+  TRY(build_sell(L.A, L.n, rp.data(), cl.data(), v.data(), V, mixed, &sp));
   L.A.ks = ks_for_level(L.n_global);
+  {
+    std::vector<int64_t> map(std::max<int64_t>(1, nnzb)), de(std::max<int64_t>(1, L.n));
+    std::vector<int32_t> pos(std::max<int64_t>(1, L.n));
+    mgi_sell_entry_map(L.n, rp.data(), sp.data(), L.A.perm_host.data(), map.data(), pos.data());
+    for (int64_t i = 0; i < L.n; ++i) de[i] = map[diag_k[i]];
+    TRY(L.umap.upload(map.data(), map.size()));
+    TRY(L.udiag_e.upload(de.data(), de.size()));
+    TRY(L.upos.upload(pos.data(), pos.size()));
+    if (!brow.empty()) {
+      TRY(L.ublk_row.upload(brow.data(), brow.size()));
+      TRY(L.ublk_col.upload(bcol.data(), bcol.size()));
+    }
+  }
   if (!v64.empty()) {
     TRY(build_sell(L.A64, L.n, rp.data(), cl.data(), v64.data(), V, false));
     L.A64.ks = L.A.ks;
@@ -1416,6 +1467,49 @@ mg_status mg_apply_constraints(mg_ctx c, double *x) {
   TRY(launch_transfer(c->bs(), false, c->H, In{x, c->hh.active ? c->hh.ghost.p : nullptr, int(F.n)}, F.w.p,
                       c->stream));
   if (F.n) CU(cudaMemcpyAsync(x, F.w.p, size_t(F.n) * c->bs() * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  return MG_OK;
+}
+
+mg_status mg_update_matrix(mg_ctx c, int level, const double *vals, int mem) {
+  TRY(check_level(c, level));
+  if (!vals) return fail(MG_ERR_INVALID_ARG, "NULL values");
+  Level &L = c->lv[level];
+  if (!L.A.set) return fail(MG_ERR_STATE, "level %d has no matrix: call mg_set_matrix first", level);
+  if (mem != MG_MEM_HOST && mem != MG_MEM_DEVICE) return fail(MG_ERR_INVALID_ARG, "bad mem");
+  DeviceGuard dg(c->device);
+  const int bs = c->bs(), V = bs * bs;
+  const int64_t nnzb = L.nnzb;
+  DevArray<double> tmp;
+  const double *dv = vals;
+  if (mem == MG_MEM_HOST) {
+    TRY(tmp.upload(vals, size_t(std::max<int64_t>(1, nnzb)) * V));
+    dv = tmp.p;
+  }
+  DevArray<int> flag;
+  TRY(flag.alloc(1));
+  CU(cudaMemsetAsync(flag.p, 0, sizeof(int), c->stream));
+  const unsigned g = unsigned(std::min<int64_t>(std::max<int64_t>(1, (nnzb + 255) / 256), 16 * c->n_sm));
+  if (nnzb > 0) {
+    mgk::k_scatter_values<<<g, 256, 0, c->stream>>>(nnzb, V, L.umap.p, dv, L.A.f32 ? nullptr : L.A.val.p,
+                                                    L.A.f32 ? L.A.valf.p : nullptr, flag.p);
+    if (L.A64.set)
+      mgk::k_scatter_values<<<g, 256, 0, c->stream>>>(nnzb, V, L.umap.p, dv, L.A64.val.p, nullptr, flag.p);
+    TRY(check_launch("value scatter"));
+  }
+  int f = 0;
+  CU(cudaMemcpyAsync(&f, flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (f & 1) return fail(MG_ERR_NONFINITE, "level %d: non-finite matrix value", level);
+  if (L.dinv_host.empty()) TRY(device_dinv(c, level));  // a user-supplied D^-1 is kept
+  if (level == 0 && c->cfg.coarse_mode == MG_COARSE_DIRECT && !L.dist && c->cN > 0) {
+    CU(cudaMemsetAsync(c->cinv.p, 0, c->cinv.n * sizeof(double), c->stream));
+    const unsigned gd = unsigned(std::min<int64_t>(std::max<int64_t>(1, (nnzb * V + 255) / 256), 16 * c->n_sm));
+    mgk::k_dense_scatter<<<gd, 256, 0, c->stream>>>(nnzb, bs, L.ublk_row.p, L.ublk_col.p, dv,
+                                                    c->cfg.precision == MG_PREC_MIXED ? 1 : 0, c->cld, c->cinv.p);
+    TRY(check_launch("dense scatter"));
+    TRY(coarse_gj(c, c->cN, c->cld));
+  }
+  // graphs hold pointers only: they stay valid
   return MG_OK;
 }
 

@@ -256,3 +256,31 @@ def test_bench_byte_model_matches_survey():
     assert resid == a_stream + 24 * 3 * 10
     sweep32, _, _ = bench.level_bytes(info, 3, False, vb=4)
     assert sweep - sweep32 == 27 * 4 * 9
+
+
+def test_sell_entry_map_places_values_like_fill():
+    """mgi_sell_entry_map (mg_update_matrix): scattering original entries through
+    the map reproduces the layout mgi_sell_fill builds, bit for bit."""
+    L = _lib()
+    P = problem("c3_small")
+    lv = P.levels[-1]
+    V = lv.bs * lv.bs
+    val = np.ascontiguousarray(lv.val.reshape(-1))
+    sp, perm, c, v = _sell(lv.row_ptr, lv.col, val, V, 4096)
+    m = np.zeros(lv.nnzb, np.int64)
+    pos = np.zeros(lv.n, np.int32)
+    L.mgi_sell_entry_map.argtypes = [ctypes.c_int64] + [ctypes.c_void_p] * 5
+    assert L.mgi_sell_entry_map(lv.n, _p(lv.row_ptr), _p(sp), _p(perm), _p(m), _p(pos)) == 0
+    out = np.zeros_like(v)
+    for k in range(lv.nnzb):
+        e = m[k]
+        lane = e % 32
+        base = (e - lane) * V
+        for j in range(V // 2):
+            out[base + 64 * j + 2 * lane] = val[k * V + 2 * j]
+            out[base + 64 * j + 2 * lane + 1] = val[k * V + 2 * j + 1]
+        if V & 1:
+            out[base + 64 * (V // 2) + lane] = val[k * V + V - 1]
+        assert c[e] == lv.col[k]
+    assert np.array_equal(out, v)
+    assert np.array_equal(perm[pos], np.arange(lv.n))
