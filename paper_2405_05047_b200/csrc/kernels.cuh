@@ -13,6 +13,7 @@
 // prolongation / restriction, coarse solve, GMRES MGS and
 // Givens.
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -48,6 +49,14 @@ __device__ __forceinline__ double ld_val1(const double *p) {
 template <bool STREAM>
 __device__ __forceinline__ int ld_col(const int32_t *p) {
   if constexpr (STREAM) return __ldcs(p);
+  else return __ldg(p);
+}
+
+// vectors: read-only cache (CG = false) or L2-coherent loads (CG = true: the
+// persistent coarse-tail kernel reads vectors written by its earlier phases)
+template <bool CG>
+__device__ __forceinline__ double ldv(const double *p) {
+  if constexpr (CG) return __ldcg(p);
   else return __ldg(p);
 }
 
@@ -137,16 +146,17 @@ __device__ __forceinline__ bool combine_split(double (&acc)[BS], int wid, int su
   return true;
 }
 
-template <int BS, int OP, bool STREAM, bool HALO, int KS, bool F32 = false>
-__global__ void __launch_bounds__(kCta) k_sell_apply(Sell A, const double *__restrict__ x,
-                                                     const double *__restrict__ xg, int n_own,
-                                                     const double *__restrict__ b,
-                                                     const double *__restrict__ dinv,
-                                                     double *__restrict__ out, double alpha, double beta) {
+// One CTA-task of an A-pass: slice s = task * (8 / KS) + warp / KS.  All warps
+// of the CTA must call it (the split-k combine synchronises the CTA).
+template <int BS, int OP, bool STREAM, bool HALO, int KS, bool F32, bool CG>
+__device__ __forceinline__ void sell_apply_task(const Sell &A, int64_t task, const double *__restrict__ x,
+                                                const double *__restrict__ xg, int n_own,
+                                                const double *__restrict__ b, const double *__restrict__ dinv,
+                                                double *__restrict__ out, double alpha, double beta) {
   constexpr int V = BS * BS;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int sub = KS == 1 ? 0 : wid % KS;
-  const int64_t s = int64_t(blockIdx.x) * (kWarpsPerCta / KS) + wid / KS;
+  const int64_t s = task * (kWarpsPerCta / KS) + wid / KS;
   const bool live = s < A.n_slices;
   if (KS == 1 && !live) return;
   double acc[BS];
@@ -176,7 +186,7 @@ __global__ void __launch_bounds__(kCta) k_sell_apply(Sell A, const double *__res
         for (int u = 0; u < U; ++u) {
           const double *xc = col_ptr<BS, HALO>(x, xg, n_own, cc[u]);
 #pragma unroll
-          for (int q = 0; q < BS; ++q) xv[u][q] = __ldg(xc + q);
+          for (int q = 0; q < BS; ++q) xv[u][q] = ldv<CG>(xc + q);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -196,7 +206,7 @@ __global__ void __launch_bounds__(kCta) k_sell_apply(Sell A, const double *__res
       const double *xc = col_ptr<BS, HALO>(x, xg, n_own, c);
       double xv[BS];
 #pragma unroll
-      for (int q = 0; q < BS; ++q) xv[q] = __ldg(xc + q);
+      for (int q = 0; q < BS; ++q) xv[q] = ldv<CG>(xc + q);
 #pragma unroll
       for (int r = 0; r < BS; ++r)
 #pragma unroll
@@ -211,11 +221,11 @@ __global__ void __launch_bounds__(kCta) k_sell_apply(Sell A, const double *__res
     for (int r = 0; r < BS; ++r) out[o + r] = (beta == 0.0) ? alpha * acc[r] : alpha * acc[r] + beta * out[o + r];
   } else if constexpr (OP == OP_RESID) {
 #pragma unroll
-    for (int r = 0; r < BS; ++r) out[o + r] = __ldg(b + o + r) - acc[r];
+    for (int r = 0; r < BS; ++r) out[o + r] = ldv<CG>(b + o + r) - acc[r];
   } else {
     double t[BS];
 #pragma unroll
-    for (int r = 0; r < BS; ++r) t[r] = __ldg(b + o + r) - acc[r];
+    for (int r = 0; r < BS; ++r) t[r] = ldv<CG>(b + o + r) - acc[r];
     double d[V];
     load_entry<V, STREAM>(dinv + s * 32 * V, lane, d);
 #pragma unroll
@@ -223,19 +233,28 @@ __global__ void __launch_bounds__(kCta) k_sell_apply(Sell A, const double *__res
       double u = 0.0;
 #pragma unroll
       for (int q = 0; q < BS; ++q) u = fma(d[r * BS + q], t[q], u);
-      out[o + r] = fma(alpha, u, __ldg(x + o + r));
+      out[o + r] = fma(alpha, u, ldv<CG>(x + o + r));
     }
   }
 }
 
+template <int BS, int OP, bool STREAM, bool HALO, int KS, bool F32 = false>
+__global__ void __launch_bounds__(kCta) k_sell_apply(Sell A, const double *__restrict__ x,
+                                                     const double *__restrict__ xg, int n_own,
+                                                     const double *__restrict__ b,
+                                                     const double *__restrict__ dinv,
+                                                     double *__restrict__ out, double alpha, double beta) {
+  sell_apply_task<BS, OP, STREAM, HALO, KS, F32, false>(A, blockIdx.x, x, xg, n_own, b, dinv, out, alpha, beta);
+}
+
 // First smoothing step from the zero guess: x = omega D^-1 b, A-free.
-template <int BS>
-__global__ void __launch_bounds__(kCta) k_sweep0(int64_t n_slices, const int32_t *__restrict__ perm,
-                                                 const double *__restrict__ dinv, const double *__restrict__ b,
-                                                 double *__restrict__ x, double omega) {
+template <int BS, bool CG>
+__device__ __forceinline__ void sweep0_task(int64_t n_slices, int64_t task, const int32_t *__restrict__ perm,
+                                            const double *__restrict__ dinv, const double *__restrict__ b,
+                                            double *__restrict__ x, double omega) {
   constexpr int V = BS * BS;
   const int lane = threadIdx.x & 31;
-  const int64_t s = (int64_t(blockIdx.x) * kCta + threadIdx.x) >> 5;
+  const int64_t s = task * kWarpsPerCta + (threadIdx.x >> 5);
   if (s >= n_slices) return;
   const int row = perm[s * 32 + lane];
   double d[V];
@@ -244,7 +263,7 @@ __global__ void __launch_bounds__(kCta) k_sweep0(int64_t n_slices, const int32_t
   const int64_t o = int64_t(row) * BS;
   double t[BS];
 #pragma unroll
-  for (int q = 0; q < BS; ++q) t[q] = __ldg(b + o + q);
+  for (int q = 0; q < BS; ++q) t[q] = ldv<CG>(b + o + q);
 #pragma unroll
   for (int r = 0; r < BS; ++r) {
     double u = 0.0;
@@ -254,16 +273,22 @@ __global__ void __launch_bounds__(kCta) k_sweep0(int64_t n_slices, const int32_t
   }
 }
 
+template <int BS>
+__global__ void __launch_bounds__(kCta) k_sweep0(int64_t n_slices, const int32_t *__restrict__ perm,
+                                                 const double *__restrict__ dinv, const double *__restrict__ b,
+                                                 double *__restrict__ x, double omega) {
+  sweep0_task<BS, false>(n_slices, blockIdx.x, perm, dinv, b, x, omega);
+}
+
 // Transfer y = T x (ACCUM = 0) or y += T x (ACCUM = 1) with scalar weights
 // (WPE = 1) or per-component weights (WPE = BS): restriction R r (P:131,
 // P:337), prolongation x + P y, hanging interpolation H x.
-template <int BS, int WPE, bool ACCUM, bool STREAM, bool HALO, int KS>
-__global__ void __launch_bounds__(kCta) k_transfer(Sell T, const double *__restrict__ in,
-                                                   const double *__restrict__ ing, int n_own,
-                                                   double *__restrict__ out) {
+template <int BS, int WPE, bool ACCUM, bool STREAM, bool HALO, int KS, bool CG>
+__device__ __forceinline__ void transfer_task(const Sell &T, int64_t task, const double *__restrict__ in,
+                                              const double *__restrict__ ing, int n_own, double *__restrict__ out) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int sub = KS == 1 ? 0 : wid % KS;
-  const int64_t s = int64_t(blockIdx.x) * (kWarpsPerCta / KS) + wid / KS;
+  const int64_t s = task * (kWarpsPerCta / KS) + wid / KS;
   const bool live = s < T.n_slices;
   if (KS == 1 && !live) return;
   double acc[BS];
@@ -283,7 +308,7 @@ __global__ void __launch_bounds__(kCta) k_transfer(Sell T, const double *__restr
       load_entry<WPE, STREAM>(T.val + g * WPE, lane, w);
       const double *xc = col_ptr<BS, HALO>(in, ing, n_own, c);
 #pragma unroll
-      for (int q = 0; q < BS; ++q) acc[q] = fma(w[WPE == 1 ? 0 : q], __ldg(xc + q), acc[q]);
+      for (int q = 0; q < BS; ++q) acc[q] = fma(w[WPE == 1 ? 0 : q], ldv<CG>(xc + q), acc[q]);
     }
   }
   if (!combine_split<BS, KS>(acc, wid, sub, lane)) return;
@@ -293,13 +318,19 @@ __global__ void __launch_bounds__(kCta) k_transfer(Sell T, const double *__restr
   for (int q = 0; q < BS; ++q) out[o + q] = ACCUM ? out[o + q] + acc[q] : acc[q];
 }
 
+template <int BS, int WPE, bool ACCUM, bool STREAM, bool HALO, int KS>
+__global__ void __launch_bounds__(kCta) k_transfer(Sell T, const double *__restrict__ in,
+                                                   const double *__restrict__ ing, int n_own,
+                                                   double *__restrict__ out) {
+  transfer_task<BS, WPE, ACCUM, STREAM, HALO, KS, false>(T, blockIdx.x, in, ing, n_own, out);
+}
+
 // Coarse solve y = A_0^{-1} d with the dense inverse (row stride ld, even,
 // zero padded): one warp per row, 16-byte loads, shuffle reduction.
-__global__ void __launch_bounds__(kCta) k_dense_gemv(int64_t N, int64_t ld, const double *__restrict__ M,
-                                                     const double *__restrict__ d, double *__restrict__ y) {
+template <bool CG>
+__device__ __forceinline__ void gemv_row(int64_t N, int64_t ld, const double *__restrict__ M,
+                                         const double *__restrict__ d, double *__restrict__ y, int64_t r) {
   const int lane = threadIdx.x & 31;
-  const int64_t r = (int64_t(blockIdx.x) * kCta + threadIdx.x) >> 5;
-  if (r >= N) return;
   const double *row = M + r * ld;
   double acc = 0.0;
   int64_t c = 2 * lane;
@@ -308,7 +339,7 @@ __global__ void __launch_bounds__(kCta) k_dense_gemv(int64_t N, int64_t ld, cons
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       m[u] = __ldg(reinterpret_cast<const double2 *>(row + c + 64 * u));
-      dv[u] = make_double2(__ldg(d + c + 64 * u), __ldg(d + c + 64 * u + 1));
+      dv[u] = make_double2(ldv<CG>(d + c + 64 * u), ldv<CG>(d + c + 64 * u + 1));
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -318,12 +349,100 @@ __global__ void __launch_bounds__(kCta) k_dense_gemv(int64_t N, int64_t ld, cons
   }
   for (; c < N; c += 64) {
     const double2 m = __ldg(reinterpret_cast<const double2 *>(row + c));
-    acc = fma(m.x, __ldg(d + c), acc);
-    if (c + 1 < N) acc = fma(m.y, __ldg(d + c + 1), acc);
+    acc = fma(m.x, ldv<CG>(d + c), acc);
+    if (c + 1 < N) acc = fma(m.y, ldv<CG>(d + c + 1), acc);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if (lane == 0) y[r] = acc;
+}
+
+__global__ void __launch_bounds__(kCta) k_dense_gemv(int64_t N, int64_t ld, const double *__restrict__ M,
+                                                     const double *__restrict__ d, double *__restrict__ y) {
+  const int64_t r = (int64_t(blockIdx.x) * kCta + threadIdx.x) >> 5;
+  if (r >= N) return;
+  gemv_row<false>(N, ld, M, d, y, r);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent coarse-tail kernel: the V-cycle below a level T (all levels small:
+// split-k 4, not distributed) as ONE cooperative launch.  Each phase is the
+// standalone kernel's task function over a grid-stride task loop; phases are
+// separated by grid-wide barriers.  Same task functions and split factors as
+// the standalone kernels, so results are bit-identical; vectors written by an
+// earlier phase are read with L2-coherent loads.
+// ---------------------------------------------------------------------------
+enum { T_SWEEP0 = 0, T_SWEEP, T_RESID, T_RESTRICT, T_PROLONG, T_GEMV, T_COPY, T_ZERO };
+
+struct TailOp {
+  int type;
+  int f32;  // A values stored fp32 (mixed precision)
+  int wpe;  // transfers: weights per entry
+  Sell A;   // operator: A (sweeps / residual), R or P
+  const double *x;
+  const double *b;
+  const double *dinv;  // D^-1 (sweeps) or the dense coarse inverse (GEMV)
+  double *out;
+  double alpha;
+  int64_t n;   // GEMV rows / COPY, ZERO length
+  int64_t ld;  // GEMV leading dimension
+};
+
+template <int BS, int OP>
+__device__ __forceinline__ void tail_apply(const TailOp &op) {
+  const int64_t nt = (op.A.n_slices + 1) / 2;  // split-k 4: two slices per CTA-task
+  for (int64_t t = blockIdx.x; t < nt; t += gridDim.x) {
+    if (op.f32)
+      sell_apply_task<BS, OP, false, false, 4, true, true>(op.A, t, op.x, nullptr, 0, op.b, op.dinv, op.out, op.alpha,
+                                                            0.0);
+    else
+      sell_apply_task<BS, OP, false, false, 4, false, true>(op.A, t, op.x, nullptr, 0, op.b, op.dinv, op.out,
+                                                             op.alpha, 0.0);
+  }
+}
+
+template <int BS, bool ACC, int KS, bool STREAM>
+__device__ __forceinline__ void tail_transfer(const TailOp &op) {
+  const int per = kWarpsPerCta / KS;
+  const int64_t nt = (op.A.n_slices + per - 1) / per;
+  for (int64_t t = blockIdx.x; t < nt; t += gridDim.x) {
+    if (op.wpe == 1 || BS == 1)
+      transfer_task<BS, 1, ACC, STREAM, false, KS, true>(op.A, t, op.x, nullptr, 0, op.out);
+    else
+      transfer_task<BS, BS, ACC, STREAM, false, KS, true>(op.A, t, op.x, nullptr, 0, op.out);
+  }
+}
+
+template <int BS>
+__global__ void __launch_bounds__(kCta) k_tail(const TailOp *__restrict__ ops, int nops) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nth = int64_t(gridDim.x) * blockDim.x;
+  for (int p = 0; p < nops; ++p) {
+    const TailOp op = ops[p];
+    switch (op.type) {
+      case T_SWEEP0: {
+        const int64_t nt = (op.A.n_slices + kWarpsPerCta - 1) / kWarpsPerCta;
+        for (int64_t t = blockIdx.x; t < nt; t += gridDim.x)
+          sweep0_task<BS, true>(op.A.n_slices, t, op.A.perm, op.dinv, op.b, op.out, op.alpha);
+        break;
+      }
+      case T_SWEEP: tail_apply<BS, OP_SWEEP>(op); break;
+      case T_RESID: tail_apply<BS, OP_RESID>(op); break;
+      case T_RESTRICT: tail_transfer<BS, false, 4, true>(op); break;
+      case T_PROLONG: tail_transfer<BS, true, 1, false>(op); break;
+      case T_GEMV:
+        for (int64_t r = tid >> 5; r < op.n; r += nth >> 5) gemv_row<true>(op.n, op.ld, op.dinv, op.b, op.out, r);
+        break;
+      case T_COPY:
+        for (int64_t i = tid; i < op.n; i += nth) op.out[i] = __ldcg(op.x + i);
+        break;
+      default:
+        for (int64_t i = tid; i < op.n; i += nth) op.out[i] = 0.0;
+        break;
+    }
+    grid.sync();
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -252,6 +252,10 @@ struct mg_ctx_s {
   bool prof_on = false;
   int cur_level = 0;
   std::vector<std::pair<int, cudaEvent_t>> prof;
+  // persistent coarse tail: levels 0..tail_T run as one cooperative launch
+  DevArray<mgk::TailOp> tail_ops;
+  int tail_nops = 0, tail_T = -1;
+  unsigned tail_grid = 0;
   std::map<GraphKey, GraphExec> graphs;
   std::map<std::tuple<int, double, int>, GraphExec> iter_graphs;  // GMRES iteration j (j, rtol, m)
   int64_t launches = 0;
@@ -311,9 +315,10 @@ int64_t env_i64(const char *name, int64_t dflt) {
 }
 
 int ks_for_level(int64_t n_global) {
-  static const int64_t t4 = env_i64("MGB200_KS4_SLICES", 4096), t2 = env_i64("MGB200_KS2_SLICES", 32768);
+  static const int64_t t4 = env_i64("MGB200_KS4_SLICES", 4096), t2 = env_i64("MGB200_KS2_SLICES", 32768),
+                       t8 = env_i64("MGB200_KS8_SLICES", 256);
   const int64_t slices = (n_global + 31) / 32;
-  return slices < t4 ? 4 : slices < t2 ? 2 : 1;
+  return slices < t8 ? 8 : slices < t4 ? 4 : slices < t2 ? 2 : 1;
 }
 
 mg_status check_launch(const char *what = "kernel") {
@@ -334,7 +339,14 @@ template <int BS, int OP, bool HALO>
 void launch_apply_h(const SellOp &A, In in, const double *b, const double *dinv, double *out, double alpha,
                     double beta, cudaStream_t st) {
   const unsigned g = grid_for_slices(A.n_slices, A.ks);
-  if (A.f32) {
+  if (A.ks == 8) {
+    if (A.f32)
+      ++g_tally, mgk::k_sell_apply<BS, OP, false, HALO, 8, true>
+                     <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+    else
+      ++g_tally, mgk::k_sell_apply<BS, OP, false, HALO, 8, false>
+                     <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+  } else if (A.f32) {
     if (A.ks == 4)
       ++g_tally, mgk::k_sell_apply<BS, OP, false, HALO, 4, true>
                      <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
@@ -756,6 +768,158 @@ double lv_omega(const mg_ctx_s *c, const Level &L) { return L.omega > 0.0 ? L.om
 int lv_nu_pre(const mg_ctx_s *c, const Level &L) { return L.nu_pre >= 0 ? L.nu_pre : c->cfg.nu_pre; }
 int lv_nu_post(const mg_ctx_s *c, const Level &L) { return L.nu_post >= 0 ? L.nu_post : c->cfg.nu_post; }
 
+// --- persistent coarse tail ----------------------------------------------------
+template <int BS>
+mg_status tail_grid_size(mg_ctx_s *c) {
+  int per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgk::k_tail<BS>, mgk::kCta, 0));
+  const int want = int(env_i64("MGB200_TAIL_CTAS", per_sm));
+  c->tail_grid = unsigned(std::max(1, std::min(per_sm, want)) * c->n_sm);
+  return MG_OK;
+}
+
+// Tail level T: the highest level below the finest whose levels 0..T all use
+// split-k 4 (few slices) and are not distributed; T >= 1.  MGB200_TAIL=0
+// disables the tail (standalone kernels only).
+mg_status build_tail(mg_ctx_s *c) {
+  c->tail_nops = 0;
+  c->tail_T = -1;
+  // opt-in (MGB200_TAIL=1): measured slower than graph-launched standalone
+  // kernels on B200 (C2 0.39 vs 0.35 ms, C3 5.30 vs 5.18 ms per V-cycle) --
+  // its grid barriers cost more than CUDA-graph kernel boundaries
+  const char *env = std::getenv("MGB200_TAIL");
+  if (!env || env[0] != '1') return MG_OK;
+  static const int64_t max_slices = env_i64("MGB200_TAIL_SLICES", 1024);
+  int T = -1;
+  for (int l = 0; l < c->L(); ++l) {
+    const Level &L = c->lv[l];
+    if (L.dist || L.A.ks != 4 || (l > 0 && c->lv[l].R.ks != 4) || L.A.n_slices > max_slices) break;
+    T = l;
+  }
+  if (T < 1) return MG_OK;
+  const int bs = c->bs();
+  std::vector<mgk::TailOp> ops;
+  auto base = [&](int type) {
+    mgk::TailOp o{};
+    o.type = type;
+    return o;
+  };
+  auto emit_smooth = [&](int l, double *x, const double *b, int k, bool zero) {
+    Level &L = c->lv[l];
+    const double om = lv_omega(c, L);
+    if (k <= 0) {
+      if (zero) {
+        mgk::TailOp o = base(mgk::T_ZERO);
+        o.out = x;
+        o.n = L.n * bs;
+        ops.push_back(o);
+      }
+      return;
+    }
+    if (zero) {
+      mgk::TailOp o = base(mgk::T_SWEEP0);
+      o.A = L.A.view();
+      o.dinv = L.dinv.p;
+      o.b = b;
+      o.out = x;
+      o.alpha = om;
+      ops.push_back(o);
+      --k;
+    }
+    double *src = x, *dst = L.w.p;
+    for (int i = 0; i < k; ++i) {
+      mgk::TailOp o = base(mgk::T_SWEEP);
+      o.A = L.A.view();
+      o.f32 = L.A.f32;
+      o.x = src;
+      o.b = b;
+      o.dinv = L.dinv.p;
+      o.out = dst;
+      o.alpha = om;
+      ops.push_back(o);
+      std::swap(src, dst);
+    }
+    if (src != x) {
+      mgk::TailOp o = base(mgk::T_COPY);
+      o.x = src;
+      o.out = x;
+      o.n = L.n * bs;
+      ops.push_back(o);
+    }
+  };
+  for (int l = T; l >= 1; --l) {
+    Level &L = c->lv[l];
+    emit_smooth(l, L.x.p, L.b.p, lv_nu_pre(c, L), true);
+    mgk::TailOp r = base(mgk::T_RESID);
+    r.A = L.A.view();
+    r.f32 = L.A.f32;
+    r.x = L.x.p;
+    r.b = L.b.p;
+    r.out = L.w.p;
+    r.alpha = 1.0;
+    ops.push_back(r);
+    mgk::TailOp t = base(mgk::T_RESTRICT);
+    t.A = L.R.view();
+    t.wpe = L.R.vpe;
+    t.x = L.w.p;
+    t.out = c->lv[l - 1].b.p;
+    ops.push_back(t);
+  }
+  if (c->cfg.coarse_mode == MG_COARSE_DIRECT) {
+    mgk::TailOp g = base(mgk::T_GEMV);
+    g.dinv = c->cinv.p;
+    g.b = c->lv[0].b.p;
+    g.out = c->lv[0].x.p;
+    g.n = c->cN;
+    g.ld = c->cld;
+    ops.push_back(g);
+  } else {
+    emit_smooth(0, c->lv[0].x.p, c->lv[0].b.p, std::max(1, c->cfg.coarse_sweeps), true);
+  }
+  for (int l = 1; l <= T; ++l) {
+    Level &L = c->lv[l];
+    mgk::TailOp pr = base(mgk::T_PROLONG);
+    pr.A = L.P.view();
+    pr.wpe = L.P.vpe;
+    pr.x = c->lv[l - 1].x.p;
+    pr.out = L.x.p;
+    ops.push_back(pr);
+    emit_smooth(l, L.x.p, L.b.p, lv_nu_post(c, L), false);
+  }
+  TRY(c->tail_ops.upload(ops.data(), ops.size()));
+  c->tail_nops = int(ops.size());
+  c->tail_T = T;
+  switch (bs) {
+    case 1: TRY(tail_grid_size<1>(c)); break;
+    case 2: TRY(tail_grid_size<2>(c)); break;
+    case 3: TRY(tail_grid_size<3>(c)); break;
+    default: TRY(tail_grid_size<4>(c)); break;
+  }
+  return MG_OK;
+}
+
+mg_status launch_tail(mg_ctx_s *c) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(c->tail_grid);
+  cfg.blockDim = dim3(mgk::kCta);
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const mgk::TailOp *ops = c->tail_ops.p;
+  const int n = c->tail_nops;
+  ++g_tally;
+  switch (c->bs()) {
+    case 1: CU(cudaLaunchKernelEx(&cfg, mgk::k_tail<1>, ops, n)); break;
+    case 2: CU(cudaLaunchKernelEx(&cfg, mgk::k_tail<2>, ops, n)); break;
+    case 3: CU(cudaLaunchKernelEx(&cfg, mgk::k_tail<3>, ops, n)); break;
+    default: CU(cudaLaunchKernelEx(&cfg, mgk::k_tail<4>, ops, n)); break;
+  }
+  return MG_OK;
+}
+
 mg_status finalize(mg_ctx_s *c) {
   if (c->finalized) return MG_OK;
   const int bs = c->bs();
@@ -784,6 +948,7 @@ mg_status finalize(mg_ctx_s *c) {
     }
   }
   if (c->cfg.coarse_mode == MG_COARSE_DIRECT && c->cN == 0) TRY(build_coarse_inverse(c));
+  TRY(build_tail(c));
   if (!c->red_part.p) {
     TRY(c->red_part.alloc(4 * c->n_sm + 8));
     TRY(c->ticket.alloc(1));
@@ -881,6 +1046,8 @@ mg_status coarse_solve(mg_ctx_s *c, const double *b, double *x) {
 mg_status vcycle_rec(mg_ctx_s *c, int l, double *x, const double *b, bool zero) {
   c->cur_level = l;
   mark(c, l);
+  if (l == c->tail_T && c->tail_nops > 0 && zero && x == c->lv[l].x.p && b == c->lv[l].b.p)
+    return launch_tail(c);                   // GMG(T, 0, b_T), levels T..0 in one launch
   if (l == 0) return coarse_solve(c, b, x);  // Step 0; ignores x (Z21)
   Level &L = c->lv[l];
   Level &C = c->lv[l - 1];

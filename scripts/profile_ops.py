@@ -18,7 +18,7 @@ import paper_2405_05047_b200 as m  # noqa: E402
 from problems import configs  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("mode", choices=["step", "kernels"])
+ap.add_argument("mode", choices=["step", "kernels", "vcycle"])
 ap.add_argument("--config", default="c3")
 a = ap.parse_args()
 
@@ -42,6 +42,15 @@ if a.mode == "step":
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
     print(f"step: {its} iterations, rel {rel:.2e}", file=sys.stderr)
+elif a.mode == "vcycle":
+    z = torch.zeros_like(b)
+    for _ in range(3):
+        S.precondition(z, b)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    S.precondition(z, b)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
 else:
     xin = torch.randn_like(b)
     out = torch.empty_like(b)
