@@ -692,12 +692,15 @@ __device__ __forceinline__ int64_t sell_off32(int64_t e, int V, int j) {
 
 // original BSR entry k (V = bs*bs row-major values) -> SELL entry map[k],
 // chunked fp64 layout (out64) or fp32 layout (out32, rounded to nearest)
-__global__ void k_scatter_values(int64_t nnz, int V, const int64_t *__restrict__ map, const double *__restrict__ vals,
-                                 double *__restrict__ out64, float *__restrict__ out32, int *flag) {
+// (src: the level entry of part entry k, or nullptr for the identity)
+__global__ void k_scatter_values(int64_t nnz, int V, const int64_t *__restrict__ map, const int64_t *__restrict__ src,
+                                 const double *__restrict__ vals, double *__restrict__ out64, float *__restrict__ out32,
+                                 int *flag) {
   for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < nnz; k += int64_t(gridDim.x) * blockDim.x) {
     const int64_t e = map[k];
+    const int64_t ks = src ? src[k] : k;
     for (int j = 0; j < V; ++j) {
-      const double v = vals[k * V + j];
+      const double v = vals[ks * V + j];
       if (!isfinite(v)) atomicOr(flag, 1);
       if (out32) out32[sell_off32(e, V, j)] = float(v);
       else out64[sell_off64(e, V, j)] = v;

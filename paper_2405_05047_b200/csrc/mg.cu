@@ -131,7 +131,8 @@ struct SellOp {
 // Build SELL-32-sigma on the host and upload it (col: LOCAL column indices);
 // f32: values rounded to fp32 in the fp32 chunk layout.
 mg_status build_sell(SellOp &op, int64_t n, const int64_t *rp, const int64_t *col, const double *val, int vpe,
-                     bool f32 = false, std::vector<int64_t> *sp_out = nullptr) {
+                     bool f32 = false, std::vector<int64_t> *sp_out = nullptr,
+                     const std::vector<int64_t> *row_ids = nullptr) {
   int64_t ns = 0, ne = 0;
   int st = mgi_sell_size(n, rp, kSigma, &ns, &ne);
   if (st) return fail(mg_status(st), "sell layout: invalid input");
@@ -149,6 +150,9 @@ mg_status build_sell(SellOp &op, int64_t n, const int64_t *rp, const int64_t *co
     op.valf.release();
   }
   if (st) return fail(mg_status(st), "sell layout: fill failed (%d)", st);
+  if (row_ids)  // operator over a subset of rows: lanes address the level's local rows
+    for (auto &r : perm)
+      if (r >= 0) r = int32_t((*row_ids)[r]);
   TRY(op.slice_ptr.upload(sp.data(), sp.size()));
   TRY(op.perm.upload(perm.data(), perm.size()));
   TRY(op.col.upload(c.data(), c.size()));
@@ -192,19 +196,27 @@ struct Level {
   int64_t n_global = 0, row_begin = 0, row_end = 0, n = 0;
   bool dist = false;             // rows partitioned over ranks
   std::vector<int64_t> bounds;   // [nranks+1] row ranges of the ranks (distributed levels)
-  SellOp A;                       // the V-cycle operator (fp32 values in mixed precision)
-  SellOp A64;                     // mixed precision, finest level: fp64 operator for Krylov / residuals
+  // The level operator as one part (all rows) or, on distributed levels, two
+  // parts -- interior rows (no ghost columns) and boundary rows -- so the
+  // interior is computed while the halo exchange is in flight.  Each part has
+  // its own SELL layout, D^-1 slices and value-update maps.
+  struct Part {
+    SellOp A;    // V-cycle operator (fp32 values in mixed precision)
+    SellOp A64;  // mixed precision, finest level: fp64 operator for Krylov / residuals
+    DevArray<double> dinv;
+    DevArray<int64_t> umap, udiag_e, usrc;  // part entry -> SELL entry; row diag -> SELL entry; part entry -> level entry
+    DevArray<int32_t> upos;                 // part row -> slice position
+    int64_t n = 0, nnz = 0;
+    bool halo = false;                      // reads ghost columns
+  };
+  Part part[2];
+  int nparts = 1;
   int64_t nnzb = 0;
   Halo hx;                        // ghosts of x for A-passes on this level
   std::vector<double> dinv_host;  // user-supplied D^-1 (row-major blocks)
-  // value-update maps (mg_update_matrix): original entry -> SELL entry, SELL
-  // entry of each row's diagonal block, slice position of each row
-  DevArray<int64_t> umap, udiag_e;
-  DevArray<int32_t> upos;
   DevArray<int32_t> ublk_row, ublk_col;  // level 0: block coordinates for the dense coarse matrix
   std::vector<int64_t> rp0, col0;  // level-0 copy for the dense coarse inverse
   std::vector<double> val0;
-  DevArray<double> dinv;  // sliced D^-1 (chunked like a 1-entry slice)
   bool dinv_ready = false;
   SellOp P, R;  // P_{l-1}: level l-1 -> l (rows: owned fine rows), R_{l-1} = P^T (rows: r_row0 ...)
   Halo hp;      // ghosts of the coarse vector y for P (coarse level distributed)
@@ -252,6 +264,9 @@ struct mg_ctx_s {
   bool prof_on = false;
   int cur_level = 0;
   std::vector<std::pair<int, cudaEvent_t>> prof;
+  // halo / interior overlap (split levels): side stream + fork/join events
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // persistent coarse tail: levels 0..tail_T run as one cooperative launch
   DevArray<mgk::TailOp> tail_ops;
   int tail_nops = 0, tail_T = -1;
@@ -267,6 +282,9 @@ struct mg_ctx_s {
   mgk::GmresDev gm{};
   ~mg_ctx_s() {
     clear_graphs();
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
     if (gm_host) cudaFreeHost(gm_host);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -458,13 +476,7 @@ void mark(mg_ctx_s *c, int tag) {
 }
 
 // --- halo exchange: pack owned rows, transport into the ghost buffer ----------
-mg_status halo_exchange(mg_ctx_s *c, Halo &h, const double *v) {
-  if (!h.active) return MG_OK;
-  mark(c, 100 + c->cur_level);
-  struct Back {
-    mg_ctx_s *c;
-    ~Back() { mark(c, c->cur_level); }
-  } back{c};
+mg_status halo_pack(mg_ctx_s *c, Halo &h, const double *v) {
   const int bs = c->bs();
   const int64_t ns = h.pat.n_send;
   if (ns > 0) {
@@ -477,7 +489,18 @@ mg_status halo_exchange(mg_ctx_s *c, Halo &h, const double *v) {
     }
     TRY(check_launch("halo pack"));
   }
-  return c->tr->exchange(h.pat, bs, h.sendbuf.p, h.ghost.p, c->stream);
+  return MG_OK;
+}
+
+mg_status halo_exchange(mg_ctx_s *c, Halo &h, const double *v) {
+  if (!h.active) return MG_OK;
+  mark(c, 100 + c->cur_level);
+  struct Back {
+    mg_ctx_s *c;
+    ~Back() { mark(c, c->cur_level); }
+  } back{c};
+  TRY(halo_pack(c, h, v));
+  return c->tr->exchange(h.pat, c->bs(), h.sendbuf.p, h.ghost.p, c->stream);
 }
 
 // Build a halo from sorted unique ghost global rows of a level with ranges
@@ -712,47 +735,54 @@ mg_status coarse_gj(mg_ctx_s *c, int64_t N, int64_t ld) {
   return MG_OK;
 }
 
-// sliced D^-1 from row-major blocks (lane order = A's perm)
+// sliced D^-1 from row-major blocks (lane order = each part's perm; perm holds
+// the level's local row ids)
 mg_status upload_dinv(Level &L, int bs, const std::vector<double> &blocks) {
   const int V = bs * bs;
-  const int64_t ns = L.A.n_slices;
-  std::vector<double> sl(size_t(ns) * 32 * V, 0.0);
-  for (int64_t s = 0; s < ns; ++s)
-    for (int lane = 0; lane < 32; ++lane) {
-      const int32_t r = L.A.perm_host[s * 32 + lane];
-      if (r < 0) continue;
-      double *base = &sl[size_t(s) * 32 * V];
-      const double *src = &blocks[size_t(r) * V];
-      for (int j = 0; j < V / 2; ++j) {
-        base[64 * j + 2 * lane] = src[2 * j];
-        base[64 * j + 2 * lane + 1] = src[2 * j + 1];
+  for (int pi = 0; pi < L.nparts; ++pi) {
+    Level::Part &Pt = L.part[pi];
+    const int64_t ns = Pt.A.n_slices;
+    std::vector<double> sl(size_t(std::max<int64_t>(1, ns)) * 32 * V, 0.0);
+    for (int64_t s = 0; s < ns; ++s)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int32_t r = Pt.A.perm_host[s * 32 + lane];
+        if (r < 0) continue;
+        double *base = &sl[size_t(s) * 32 * V];
+        const double *src = &blocks[size_t(r) * V];
+        for (int j = 0; j < V / 2; ++j) {
+          base[64 * j + 2 * lane] = src[2 * j];
+          base[64 * j + 2 * lane + 1] = src[2 * j + 1];
+        }
+        if (V & 1) base[64 * (V / 2) + lane] = src[V - 1];
       }
-      if (V & 1) base[64 * (V / 2) + lane] = src[V - 1];
-    }
-  TRY(L.dinv.upload(sl.data(), sl.size()));
+    TRY(Pt.dinv.upload(sl.data(), sl.size()));
+  }
   L.dinv_ready = true;
   return MG_OK;
 }
 
 // D^-1 of the level's diagonal blocks on the device (from the V-cycle operator's
-// values: fp32-rounded in mixed precision).  Synchronises.
+// values: fp32-rounded in mixed precision), per part.  Synchronises.
 mg_status device_dinv(mg_ctx_s *c, int l) {
   Level &L = c->lv[l];
   const int bs = c->bs(), V = bs * bs;
-  if (L.dinv.n < size_t(L.A.n_slices) * 32 * V) TRY(L.dinv.alloc(size_t(std::max<int64_t>(1, L.A.n_slices)) * 32 * V));
-  CU(cudaMemsetAsync(L.dinv.p, 0, L.dinv.n * sizeof(double), c->stream));
   DevArray<int> flag;
   TRY(flag.alloc(1));
   CU(cudaMemsetAsync(flag.p, 0, sizeof(int), c->stream));
-  if (L.n > 0) {
-    const unsigned g = unsigned(std::min<int64_t>((L.n + 255) / 256, 16 * c->n_sm));
-    const double *v64 = L.A.f32 ? nullptr : L.A.val.p;
-    const float *v32 = L.A.f32 ? L.A.valf.p : nullptr;
+  for (int pi = 0; pi < L.nparts; ++pi) {
+    Level::Part &Pt = L.part[pi];
+    const size_t need = size_t(std::max<int64_t>(1, Pt.A.n_slices)) * 32 * V;
+    if (Pt.dinv.n < need) TRY(Pt.dinv.alloc(need));
+    CU(cudaMemsetAsync(Pt.dinv.p, 0, Pt.dinv.n * sizeof(double), c->stream));
+    if (Pt.n == 0) continue;
+    const unsigned g = unsigned(std::min<int64_t>((Pt.n + 255) / 256, 16 * c->n_sm));
+    const double *v64 = Pt.A.f32 ? nullptr : Pt.A.val.p;
+    const float *v32 = Pt.A.f32 ? Pt.A.valf.p : nullptr;
     switch (bs) {
-      case 1: mgk::k_block_inverse<1><<<g, 256, 0, c->stream>>>(L.n, L.udiag_e.p, v64, v32, L.upos.p, L.dinv.p, flag.p); break;
-      case 2: mgk::k_block_inverse<2><<<g, 256, 0, c->stream>>>(L.n, L.udiag_e.p, v64, v32, L.upos.p, L.dinv.p, flag.p); break;
-      case 3: mgk::k_block_inverse<3><<<g, 256, 0, c->stream>>>(L.n, L.udiag_e.p, v64, v32, L.upos.p, L.dinv.p, flag.p); break;
-      default: mgk::k_block_inverse<4><<<g, 256, 0, c->stream>>>(L.n, L.udiag_e.p, v64, v32, L.upos.p, L.dinv.p, flag.p); break;
+      case 1: mgk::k_block_inverse<1><<<g, 256, 0, c->stream>>>(Pt.n, Pt.udiag_e.p, v64, v32, Pt.upos.p, Pt.dinv.p, flag.p); break;
+      case 2: mgk::k_block_inverse<2><<<g, 256, 0, c->stream>>>(Pt.n, Pt.udiag_e.p, v64, v32, Pt.upos.p, Pt.dinv.p, flag.p); break;
+      case 3: mgk::k_block_inverse<3><<<g, 256, 0, c->stream>>>(Pt.n, Pt.udiag_e.p, v64, v32, Pt.upos.p, Pt.dinv.p, flag.p); break;
+      default: mgk::k_block_inverse<4><<<g, 256, 0, c->stream>>>(Pt.n, Pt.udiag_e.p, v64, v32, Pt.upos.p, Pt.dinv.p, flag.p); break;
     }
     TRY(check_launch("block inverse"));
   }
@@ -793,7 +823,7 @@ mg_status build_tail(mg_ctx_s *c) {
   int T = -1;
   for (int l = 0; l < c->L(); ++l) {
     const Level &L = c->lv[l];
-    if (L.dist || L.A.ks != 4 || (l > 0 && c->lv[l].R.ks != 4) || L.A.n_slices > max_slices) break;
+    if (L.dist || L.part[0].A.ks != 4 || (l > 0 && c->lv[l].R.ks != 4) || L.part[0].A.n_slices > max_slices) break;
     T = l;
   }
   if (T < 1) return MG_OK;
@@ -818,8 +848,8 @@ mg_status build_tail(mg_ctx_s *c) {
     }
     if (zero) {
       mgk::TailOp o = base(mgk::T_SWEEP0);
-      o.A = L.A.view();
-      o.dinv = L.dinv.p;
+      o.A = L.part[0].A.view();
+      o.dinv = L.part[0].dinv.p;
       o.b = b;
       o.out = x;
       o.alpha = om;
@@ -829,11 +859,11 @@ mg_status build_tail(mg_ctx_s *c) {
     double *src = x, *dst = L.w.p;
     for (int i = 0; i < k; ++i) {
       mgk::TailOp o = base(mgk::T_SWEEP);
-      o.A = L.A.view();
-      o.f32 = L.A.f32;
+      o.A = L.part[0].A.view();
+      o.f32 = L.part[0].A.f32;
       o.x = src;
       o.b = b;
-      o.dinv = L.dinv.p;
+      o.dinv = L.part[0].dinv.p;
       o.out = dst;
       o.alpha = om;
       ops.push_back(o);
@@ -851,8 +881,8 @@ mg_status build_tail(mg_ctx_s *c) {
     Level &L = c->lv[l];
     emit_smooth(l, L.x.p, L.b.p, lv_nu_pre(c, L), true);
     mgk::TailOp r = base(mgk::T_RESID);
-    r.A = L.A.view();
-    r.f32 = L.A.f32;
+    r.A = L.part[0].A.view();
+    r.f32 = L.part[0].A.f32;
     r.x = L.x.p;
     r.b = L.b.p;
     r.out = L.w.p;
@@ -926,7 +956,7 @@ mg_status finalize(mg_ctx_s *c) {
   for (int l = 0; l <= c->L(); ++l) {
     Level &L = c->lv[l];
     if (!L.declared) return fail(MG_ERR_STATE, "level %d not created (mg_create_level)", l);
-    if (!L.A.set) return fail(MG_ERR_STATE, "level %d has no matrix (mg_set_matrix)", l);
+    if (!L.part[0].A.set) return fail(MG_ERR_STATE, "level %d has no matrix (mg_set_matrix)", l);
     if (l > 0 && !L.P.set) return fail(MG_ERR_STATE, "level %d has no transfer (mg_set_transfer)", l);
   }
   if (c->cfg.coarse_mode == MG_COARSE_DIRECT && c->lv[0].dist)
@@ -964,30 +994,49 @@ In in_of(Level &L, Halo &h, const double *v) {
   return In{v, h.active ? h.ghost.p : nullptr, int(L.n)};
 }
 
-mg_status a_pass_sweep(mg_ctx_s *c, int l, const double *src, const double *b, double *dst) {
-  Level &L = c->lv[l];
-  TRY(halo_exchange(c, L.hx, src));
-  return launch_apply<mgk::OP_SWEEP>(c->bs(), L.A, in_of(L, L.hx, src), b, L.dinv.p, dst, lv_omega(c, L), 0.0,
-                                     c->stream);
-}
-
 // krylov = true: the problem operator (fp64 A64 on the finest level in mixed
 // precision); false: the V-cycle's operator.
-const SellOp &op_of(Level &L, bool krylov) { return krylov && L.A64.set ? L.A64 : L.A; }
+const SellOp &op_of(Level::Part &Pt, bool krylov) { return krylov && Pt.A64.set ? Pt.A64 : Pt.A; }
+
+// One A-pass over every part of level l.  Split levels overlap the halo
+// exchange (comm stream) with the interior part and run the boundary part after
+// the join; single-part levels exchange first (if distributed) and then compute.
+template <int OP>
+mg_status a_pass(mg_ctx_s *c, int l, const double *x, const double *b, double *out, double alpha, double beta,
+                 bool krylov) {
+  Level &L = c->lv[l];
+  const int bs = c->bs();
+  const double om = lv_omega(c, L);
+  auto run = [&](Level::Part &Pt, const double *xg) -> mg_status {
+    const double *dv = OP == mgk::OP_SWEEP ? Pt.dinv.p : nullptr;
+    return launch_apply<OP>(bs, op_of(Pt, krylov), In{x, xg, int(L.n)}, b, dv, out,
+                            OP == mgk::OP_SWEEP ? om : alpha, beta, c->stream);
+  };
+  if (L.nparts == 1) {
+    TRY(halo_exchange(c, L.hx, x));
+    return run(L.part[0], L.hx.active ? L.hx.ghost.p : nullptr);
+  }
+  TRY(halo_pack(c, L.hx, x));
+  CU(cudaEventRecord(c->ev_fork, c->stream));
+  CU(cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
+  TRY(c->tr->exchange(L.hx.pat, bs, L.hx.sendbuf.p, L.hx.ghost.p, c->comm_stream));
+  CU(cudaEventRecord(c->ev_join, c->comm_stream));
+  TRY(run(L.part[0], nullptr));  // interior rows: no ghost columns
+  CU(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  return run(L.part[1], L.hx.ghost.p);
+}
+
+mg_status a_pass_sweep(mg_ctx_s *c, int l, const double *src, const double *b, double *dst) {
+  return a_pass<mgk::OP_SWEEP>(c, l, src, b, dst, 1.0, 0.0, false);
+}
 
 mg_status a_pass_resid(mg_ctx_s *c, int l, const double *x, const double *b, double *r, bool krylov = false) {
-  Level &L = c->lv[l];
-  TRY(halo_exchange(c, L.hx, x));
-  return launch_apply<mgk::OP_RESID>(c->bs(), op_of(L, krylov), in_of(L, L.hx, x), b, nullptr, r, 1.0, 0.0,
-                                     c->stream);
+  return a_pass<mgk::OP_RESID>(c, l, x, b, r, 1.0, 0.0, krylov);
 }
 
 mg_status a_pass_spmv(mg_ctx_s *c, int l, double alpha, const double *x, double beta, double *y,
                       bool krylov = false) {
-  Level &L = c->lv[l];
-  TRY(halo_exchange(c, L.hx, x));
-  return launch_apply<mgk::OP_SPMV>(c->bs(), op_of(L, krylov), in_of(L, L.hx, x), nullptr, nullptr, y, alpha, beta,
-                                    c->stream);
+  return a_pass<mgk::OP_SPMV>(c, l, x, nullptr, y, alpha, beta, krylov);
 }
 
 // d_coarse = R r_fine (all coarse rows on every rank if the coarse level is replicated)
@@ -1021,7 +1070,7 @@ mg_status smooth(mg_ctx_s *c, int l, double *x, const double *b, int k, bool zer
     return MG_OK;
   }
   if (zero) {
-    TRY(launch_sweep0(bs, L.A, L.dinv.p, b, x, om, c->stream));
+    for (int pi = 0; pi < L.nparts; ++pi) TRY(launch_sweep0(bs, L.part[pi].A, L.part[pi].dinv.p, b, x, om, c->stream));
     --k;
   }
   double *src = x, *dst = L.w.p;
@@ -1362,27 +1411,92 @@ mg_status mg_set_matrix(mg_ctx c, int level, const int64_t *row_ptr, const int64
     TRY(localize(L.row_begin, L.row_end, rp, cl, ghosts));
     TRY(build_halo(c, L.hx, ghosts, L.bounds, L.row_begin, L.row_end));
   }
-  std::vector<int64_t> sp;
-  TRY(build_sell(L.A, L.n, rp.data(), cl.data(), v.data(), V, mixed, &sp));
-  L.A.ks = ks_for_level(L.n_global);
-  {
-    std::vector<int64_t> map(std::max<int64_t>(1, nnzb)), de(std::max<int64_t>(1, L.n));
-    std::vector<int32_t> pos(std::max<int64_t>(1, L.n));
-    mgi_sell_entry_map(L.n, rp.data(), sp.data(), L.A.perm_host.data(), map.data(), pos.data());
-    for (int64_t i = 0; i < L.n; ++i) de[i] = map[diag_k[i]];
-    TRY(L.umap.upload(map.data(), map.size()));
-    TRY(L.udiag_e.upload(de.data(), de.size()));
-    TRY(L.upos.upload(pos.data(), pos.size()));
-    if (!brow.empty()) {
-      TRY(L.ublk_row.upload(brow.data(), brow.size()));
-      TRY(L.ublk_col.upload(bcol.data(), bcol.size()));
+  // parts: distributed levels split into interior rows (no ghost column, computed
+  // while the halo is in flight) and boundary rows; MGB200_OVERLAP=0 disables
+  const char *ov = std::getenv("MGB200_OVERLAP");
+  std::vector<char> bnd(L.n, 0);
+  int64_t nb = 0;
+  if (L.dist && !(ov && ov[0] == '0')) {
+    for (int64_t i = 0; i < L.n; ++i) {
+      for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
+        if (cl[k] >= L.n) bnd[i] = 1;
+      nb += bnd[i];
     }
   }
-  if (!v64.empty()) {
-    TRY(build_sell(L.A64, L.n, rp.data(), cl.data(), v64.data(), V, false));
-    L.A64.ks = L.A.ks;
-  } else {
-    L.A64 = SellOp();
+  const bool split = L.dist && !(ov && ov[0] == '0') && nb > 0 && nb < L.n;
+  if (split && !c->comm_stream) {
+    CU(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  }
+  L.nparts = split ? 2 : 1;
+  for (int pi = 0; pi < L.nparts; ++pi) {
+    Level::Part &Pt = L.part[pi];
+    Pt = Level::Part();
+    Pt.halo = L.dist && (!split || pi == 1);
+    // rows of this part (all rows, or interior / boundary) and its sub-CSR
+    std::vector<int64_t> rows;
+    for (int64_t i = 0; i < L.n; ++i)
+      if (!split || bnd[i] == pi) rows.push_back(i);
+    const int64_t pn = int64_t(rows.size());
+    std::vector<int64_t> prp, pcl, src;
+    std::vector<double> pv, pv64;
+    if (!split) {  // the whole level: no copies
+      prp.swap(rp);
+      pcl.swap(cl);
+      pv.swap(v);
+      pv64.swap(v64);
+    } else {
+      prp.assign(pn + 1, 0);
+    }
+    for (int64_t j = 0; split && j < pn; ++j) {
+      const int64_t i = rows[j];
+      for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+        pcl.push_back(cl[k]);
+        src.push_back(k);
+        pv.insert(pv.end(), v.begin() + k * V, v.begin() + (k + 1) * V);
+        if (!v64.empty()) pv64.insert(pv64.end(), v64.begin() + k * V, v64.begin() + (k + 1) * V);
+      }
+      prp[j + 1] = int64_t(pcl.size());
+    }
+    std::vector<int64_t> sp;
+    TRY(build_sell(Pt.A, pn, prp.data(), pcl.data(), pv.data(), V, mixed, &sp, split ? &rows : nullptr));
+    Pt.A.ks = ks_for_level(L.n_global);
+    Pt.n = pn;
+    Pt.nnz = prp[pn];
+    // value-update maps: part entry -> SELL entry (sub-row ids), diag entries, slice positions
+    std::vector<int64_t> map(std::max<int64_t>(1, Pt.nnz)), de(std::max<int64_t>(1, pn));
+    std::vector<int32_t> pos(std::max<int64_t>(1, pn));
+    std::vector<int32_t> sub_perm(Pt.A.perm_host);  // sub-row ids for the map
+    if (split) {
+      std::vector<int64_t> inv(L.n, -1);
+      for (int64_t j = 0; j < pn; ++j) inv[rows[j]] = j;
+      for (auto &r : sub_perm)
+        if (r >= 0) r = int32_t(inv[r]);
+    }
+    mgi_sell_entry_map(pn, prp.data(), sp.data(), sub_perm.data(), map.data(), pos.data());
+    for (int64_t j = 0; j < pn; ++j) {
+      const int64_t i = rows[j];
+      const int64_t row_start = split ? rp[i] : prp[i];
+      de[j] = map[prp[j] + (diag_k[i] - row_start)];
+    }
+    TRY(Pt.umap.upload(map.data(), map.size()));
+    TRY(Pt.udiag_e.upload(de.data(), de.size()));
+    TRY(Pt.upos.upload(pos.data(), pos.size()));
+    if (split) TRY(Pt.usrc.upload(src.data(), src.size()));
+    if (!pv64.empty()) {
+      TRY(build_sell(Pt.A64, pn, prp.data(), pcl.data(), pv64.data(), V, false, nullptr, split ? &rows : nullptr));
+      Pt.A64.ks = Pt.A.ks;
+    }
+    if (!split) {  // hand the level arrays back (level-0 coarse copy below)
+      prp.swap(rp);
+      pcl.swap(cl);
+      pv.swap(v);
+    }
+  }
+  if (!brow.empty()) {
+    TRY(L.ublk_row.upload(brow.data(), brow.size()));
+    TRY(L.ublk_col.upload(bcol.data(), bcol.size()));
   }
   L.nnzb = nnzb;
   L.dinv_ready = false;  // (re)built at finalize; a user D^-1 is re-sliced with the new permutation
@@ -1561,7 +1675,7 @@ mg_status mg_vcycle_zero(mg_ctx c, double *z, const double *v) {
 mg_status mg_spmv(mg_ctx c, int level, double alpha, const double *x, double beta, double *y) {
   TRY(check_level(c, level));
   if (!x || !y || x == y) return fail(MG_ERR_INVALID_ARG, "x, y must be distinct non-NULL device pointers");
-  if (!c->lv[level].A.set) return fail(MG_ERR_STATE, "level %d has no matrix", level);
+  if (!c->lv[level].part[0].A.set) return fail(MG_ERR_STATE, "level %d has no matrix", level);
   DeviceGuard dg(c->device);
   Tally tally(c);
   return a_pass_spmv(c, level, alpha, x, beta, y, true);
@@ -1579,7 +1693,7 @@ mg_status mg_sweep(mg_ctx c, int level, const double *x, const double *b, double
 mg_status mg_residual(mg_ctx c, int level, const double *x, const double *b, double *r) {
   TRY(check_level(c, level));
   if (!x || !b || !r || r == x || r == b) return fail(MG_ERR_INVALID_ARG, "r must not alias x or b");
-  if (!c->lv[level].A.set) return fail(MG_ERR_STATE, "level %d has no matrix", level);
+  if (!c->lv[level].part[0].A.set) return fail(MG_ERR_STATE, "level %d has no matrix", level);
   DeviceGuard dg(c->device);
   Tally tally(c);
   return a_pass_resid(c, level, x, b, r, true);
@@ -1641,7 +1755,7 @@ mg_status mg_update_matrix(mg_ctx c, int level, const double *vals, int mem) {
   TRY(check_level(c, level));
   if (!vals) return fail(MG_ERR_INVALID_ARG, "NULL values");
   Level &L = c->lv[level];
-  if (!L.A.set) return fail(MG_ERR_STATE, "level %d has no matrix: call mg_set_matrix first", level);
+  if (!L.part[0].A.set) return fail(MG_ERR_STATE, "level %d has no matrix: call mg_set_matrix first", level);
   if (mem != MG_MEM_HOST && mem != MG_MEM_DEVICE) return fail(MG_ERR_INVALID_ARG, "bad mem");
   DeviceGuard dg(c->device);
   const int bs = c->bs(), V = bs * bs;
@@ -1656,13 +1770,19 @@ mg_status mg_update_matrix(mg_ctx c, int level, const double *vals, int mem) {
   TRY(flag.alloc(1));
   CU(cudaMemsetAsync(flag.p, 0, sizeof(int), c->stream));
   const unsigned g = unsigned(std::min<int64_t>(std::max<int64_t>(1, (nnzb + 255) / 256), 16 * c->n_sm));
-  if (nnzb > 0) {
-    mgk::k_scatter_values<<<g, 256, 0, c->stream>>>(nnzb, V, L.umap.p, dv, L.A.f32 ? nullptr : L.A.val.p,
-                                                    L.A.f32 ? L.A.valf.p : nullptr, flag.p);
-    if (L.A64.set)
-      mgk::k_scatter_values<<<g, 256, 0, c->stream>>>(nnzb, V, L.umap.p, dv, L.A64.val.p, nullptr, flag.p);
+  for (int pi = 0; pi < L.nparts; ++pi) {
+    Level::Part &Pt = L.part[pi];
+    if (Pt.nnz == 0) continue;
+    const unsigned gp = unsigned(std::min<int64_t>(std::max<int64_t>(1, (Pt.nnz + 255) / 256), 16 * c->n_sm));
+    mgk::k_scatter_values<<<gp, 256, 0, c->stream>>>(Pt.nnz, V, Pt.umap.p, Pt.usrc.p, dv,
+                                                     Pt.A.f32 ? nullptr : Pt.A.val.p, Pt.A.f32 ? Pt.A.valf.p : nullptr,
+                                                     flag.p);
+    if (Pt.A64.set)
+      mgk::k_scatter_values<<<gp, 256, 0, c->stream>>>(Pt.nnz, V, Pt.umap.p, Pt.usrc.p, dv, Pt.A64.val.p, nullptr,
+                                                       flag.p);
     TRY(check_launch("value scatter"));
   }
+  (void)g;
   int f = 0;
   CU(cudaMemcpyAsync(&f, flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
@@ -1740,7 +1860,7 @@ int mgi_level_info(mgi_ctx c, int level, int64_t *n, int64_t *nnzb, int64_t *sel
   const Level &L = c->lv[level];
   if (n) *n = L.n;
   if (nnzb) *nnzb = L.nnzb;
-  if (sell_entries) *sell_entries = L.A.n_entries;
+  if (sell_entries) *sell_entries = L.part[0].A.n_entries + (L.nparts > 1 ? L.part[1].A.n_entries : 0);
   if (nnz_p) *nnz_p = L.nnz_p;
   if (sell_entries_p) *sell_entries_p = L.P.n_entries;
   if (sell_entries_r) *sell_entries_r = L.R.n_entries;
@@ -1766,7 +1886,7 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
   if (!c->gm_host) CU(cudaMallocHost(&c->gm_host, 16 * sizeof(double)));
   double *hst = c->gm_host;
 
-  const bool mixed = F.A64.set;
+  const bool mixed = F.part[0].A64.set;
   if (opts->method == MG_RICHARDSON) {
     // mixed precision: defect correction x += GMG(L, 0, r), r = b - A x in fp64,
     // kept in a buffer of its own (F.w is the V-cycle's work vector)

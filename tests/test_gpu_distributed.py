@@ -229,3 +229,37 @@ def test_distributed_coarse_smoothing_mode():
         return host(z)
     got = np.concatenate(run_ranks(2, cyc))
     assert np.array_equal(got, host(z1))
+
+
+@pytest.mark.parametrize("overlap", ["1", "0"])
+def test_distributed_mixed_precision_and_overlap(overlap, monkeypatch):
+    """Row-partitioned mixed-precision V-cycle and GMRES, with and without the
+    halo / interior overlap (interior and boundary parts): bit-identical V-cycle
+    to the single-GPU mixed solver."""
+    import paper_2405_05047_b200 as m
+    from problems.partition import partition
+    monkeypatch.setenv("MGB200_OVERLAP", overlap)
+    Pr = problem("c3_mid")
+    parts, extras, ranges = partition(Pr, 3, min_rows_per_rank=32)
+    key = os.urandom(16)
+    mgs = run_ranks(3, lambda r: build_gpu(parts[r], Pr.bs, omega=Pr.omega, H=extras[r][1],
+                                           precision=m.MG_PREC_MIXED, comm=(3, r, key, m.MG_TRANSPORT_LOCAL)))
+    s = build_gpu(Pr.levels, Pr.bs, omega=Pr.omega, H=Pr.fine.H, precision=m.MG_PREC_MIXED)
+    z = dev(np.zeros(Pr.n_dof))
+    m.mg_vcycle_zero(s.ctx, z, dev(Pr.b))
+    x1 = dev(np.zeros(Pr.n_dof))
+    _, its1, _, _ = m.mg_solve(s.ctx, x1, dev(Pr.b), rtol=1e-10)
+    fr = ranges[-1]
+
+    def work(r):
+        f0, f1 = fr[r]
+        zz = dev(np.zeros((f1 - f0) * Pr.bs))
+        m.mg_vcycle_zero(mgs[r].ctx, zz, dev(extras[r][0]))
+        xx = dev(np.zeros((f1 - f0) * Pr.bs))
+        out = m.mg_solve(mgs[r].ctx, xx, dev(extras[r][0]), rtol=1e-10)
+        return host(zz), out
+    out = run_ranks(3, work)
+    assert np.array_equal(np.concatenate([o[0] for o in out]), host(z))
+    assert all(o[1][3] for o in out) and abs(out[0][1][1] - its1) <= 1
+    for g in mgs:
+        g.close()
