@@ -137,11 +137,14 @@ __device__ __forceinline__ bool combine_split(double (&acc)[BS], int wid, int su
       for (int r = 0; r < BS; ++r) part[wid][r][lane] = acc[r];
     }
     __syncthreads();
-    if (sub) return false;
+    if (!sub) {
 #pragma unroll
-    for (int k = 1; k < KS; ++k)
+      for (int k = 1; k < KS; ++k)
 #pragma unroll
-      for (int r = 0; r < BS; ++r) acc[r] += part[wid + k][r][lane];
+        for (int r = 0; r < BS; ++r) acc[r] += part[wid + k][r][lane];
+    }
+    __syncthreads();  // partials are reused by the CTA's next task (persistent kernels)
+    return !sub;
   }
   return true;
 }
@@ -168,32 +171,44 @@ __device__ __forceinline__ void sell_apply_task(const Sell &A, int64_t task, con
     row = A.perm[s * 32 + lane];
     int64_t g = e0 + 32 * sub;
     int cn = g < e1 ? ld_col<STREAM>(A.col + g + lane) : 0;  // column of the next entry (prefetched)
-    if constexpr (F32) {
-      // fp32 values carry half the bytes per entry: issue the loads of U
-      // entries before the first use so twice as many bytes are in flight
-      constexpr int U = 4, step = 32 * KS;
-      for (; g + (U - 1) * step < e1; g += U * step) {
-        int cc[U];
+    // Few bytes per entry (fp32 values, or bs <= 2): issue the loads of UB
+    // entries before the first use so enough bytes are in flight per warp.
+    // Entries are still accumulated in order (bit-identical to UB = 1).
+    constexpr int UB = F32 ? 4 : (V == 1 ? 8 : (V == 4 ? 4 : 1));
+    if constexpr (UB > 1) {
+      constexpr int step = 32 * KS;
+      for (; g + (UB - 1) * step < e1; g += UB * step) {
+        int cc[UB];
         cc[0] = cn;
 #pragma unroll
-        for (int u = 1; u < U; ++u) cc[u] = ld_col<STREAM>(A.col + g + u * step + lane);
-        if (g + U * step < e1) cn = ld_col<STREAM>(A.col + g + U * step + lane);
-        float vf[U][V];
+        for (int u = 1; u < UB; ++u) cc[u] = ld_col<STREAM>(A.col + g + u * step + lane);
+        if (g + UB * step < e1) cn = ld_col<STREAM>(A.col + g + UB * step + lane);
+        double vd[UB][V];
+        if constexpr (F32) {
+          float vf[UB][V];
 #pragma unroll
-        for (int u = 0; u < U; ++u) load_entry_raw<V, STREAM>(A.valf + (g + u * step) * V, lane, vf[u]);
-        double xv[U][BS];
+          for (int u = 0; u < UB; ++u) load_entry_raw<V, STREAM>(A.valf + (g + u * step) * V, lane, vf[u]);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
+          for (int u = 0; u < UB; ++u)
+#pragma unroll
+            for (int j = 0; j < V; ++j) vd[u][j] = double(vf[u][j]);
+        } else {
+#pragma unroll
+          for (int u = 0; u < UB; ++u) load_entry<V, STREAM>(A.val + (g + u * step) * V, lane, vd[u]);
+        }
+        double xv[UB][BS];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
           const double *xc = col_ptr<BS, HALO>(x, xg, n_own, cc[u]);
 #pragma unroll
           for (int q = 0; q < BS; ++q) xv[u][q] = ldv<CG>(xc + q);
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+        for (int u = 0; u < UB; ++u)
 #pragma unroll
           for (int r = 0; r < BS; ++r)
 #pragma unroll
-            for (int q = 0; q < BS; ++q) acc[r] = fma(double(vf[u][r * BS + q]), xv[u][q], acc[r]);
+            for (int q = 0; q < BS; ++q) acc[r] = fma(vd[u][r * BS + q], xv[u][q], acc[r]);
       }
     }
 #pragma unroll 4
@@ -300,6 +315,28 @@ __device__ __forceinline__ void transfer_task(const Sell &T, int64_t task, const
     row = T.perm[s * 32 + lane];
     int64_t g = e0 + 32 * sub;
     int cn = g < e1 ? ld_col<STREAM>(T.col + g + lane) : 0;
+    constexpr int UB = 4;  // scalar weights: batch the loads of 4 entries (summed in order)
+    constexpr int step = 32 * KS;
+    for (; g + (UB - 1) * step < e1; g += UB * step) {
+      int cc[UB];
+      cc[0] = cn;
+#pragma unroll
+      for (int u = 1; u < UB; ++u) cc[u] = ld_col<STREAM>(T.col + g + u * step + lane);
+      if (g + UB * step < e1) cn = ld_col<STREAM>(T.col + g + UB * step + lane);
+      double w[UB][WPE], xv[UB][BS];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) load_entry<WPE, STREAM>(T.val + (g + u * step) * WPE, lane, w[u]);
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const double *xc = col_ptr<BS, HALO>(in, ing, n_own, cc[u]);
+#pragma unroll
+        for (int q = 0; q < BS; ++q) xv[u][q] = ldv<CG>(xc + q);
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u)
+#pragma unroll
+        for (int q = 0; q < BS; ++q) acc[q] = fma(w[u][WPE == 1 ? 0 : q], xv[u][q], acc[q]);
+    }
 #pragma unroll 4
     for (; g < e1; g += 32 * KS) {
       const int c = cn;
@@ -376,6 +413,7 @@ enum { T_SWEEP0 = 0, T_SWEEP, T_RESID, T_RESTRICT, T_PROLONG, T_GEMV, T_COPY, T_
 
 struct TailOp {
   int type;
+  int ks;   // split-k of A-passes (4 or 8, as in the standalone kernels)
   int f32;  // A values stored fp32 (mixed precision)
   int wpe;  // transfers: weights per entry
   Sell A;   // operator: A (sweeps / residual), R or P
@@ -388,17 +426,24 @@ struct TailOp {
   int64_t ld;  // GEMV leading dimension
 };
 
-template <int BS, int OP>
-__device__ __forceinline__ void tail_apply(const TailOp &op) {
-  const int64_t nt = (op.A.n_slices + 1) / 2;  // split-k 4: two slices per CTA-task
+template <int BS, int OP, int KS>
+__device__ __forceinline__ void tail_apply_ks(const TailOp &op) {
+  constexpr int per = kWarpsPerCta / KS;  // slices per CTA-task
+  const int64_t nt = (op.A.n_slices + per - 1) / per;
   for (int64_t t = blockIdx.x; t < nt; t += gridDim.x) {
     if (op.f32)
-      sell_apply_task<BS, OP, false, false, 4, true, true>(op.A, t, op.x, nullptr, 0, op.b, op.dinv, op.out, op.alpha,
-                                                            0.0);
-    else
-      sell_apply_task<BS, OP, false, false, 4, false, true>(op.A, t, op.x, nullptr, 0, op.b, op.dinv, op.out,
+      sell_apply_task<BS, OP, false, false, KS, true, true>(op.A, t, op.x, nullptr, 0, op.b, op.dinv, op.out,
                                                              op.alpha, 0.0);
+    else
+      sell_apply_task<BS, OP, false, false, KS, false, true>(op.A, t, op.x, nullptr, 0, op.b, op.dinv, op.out,
+                                                              op.alpha, 0.0);
   }
+}
+
+template <int BS, int OP>
+__device__ __forceinline__ void tail_apply(const TailOp &op) {
+  if (op.ks == 8) tail_apply_ks<BS, OP, 8>(op);
+  else tail_apply_ks<BS, OP, 4>(op);
 }
 
 template <int BS, bool ACC, int KS, bool STREAM>
@@ -413,9 +458,10 @@ __device__ __forceinline__ void tail_transfer(const TailOp &op) {
   }
 }
 
-template <int BS>
+// CLUSTER: the whole grid is one thread-block cluster (<= 16 CTAs) and phases
+// are separated by the hardware cluster barrier instead of a grid barrier.
+template <int BS, bool CLUSTER>
 __global__ void __launch_bounds__(kCta) k_tail(const TailOp *__restrict__ ops, int nops) {
-  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nth = int64_t(gridDim.x) * blockDim.x;
   for (int p = 0; p < nops; ++p) {
@@ -441,7 +487,8 @@ __global__ void __launch_bounds__(kCta) k_tail(const TailOp *__restrict__ ops, i
         for (int64_t i = tid; i < op.n; i += nth) op.out[i] = 0.0;
         break;
     }
-    grid.sync();
+    if constexpr (CLUSTER) cooperative_groups::this_cluster().sync();
+    else cooperative_groups::this_grid().sync();
   }
 }
 

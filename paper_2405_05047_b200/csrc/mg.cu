@@ -270,6 +270,7 @@ struct mg_ctx_s {
   // persistent coarse tail: levels 0..tail_T run as one cooperative launch
   DevArray<mgk::TailOp> tail_ops;
   int tail_nops = 0, tail_T = -1;
+  bool tail_cluster = true;
   unsigned tail_grid = 0;
   std::map<GraphKey, GraphExec> graphs;
   std::map<std::tuple<int, double, int>, GraphExec> iter_graphs;  // GMRES iteration j (j, rtol, m)
@@ -801,8 +802,15 @@ int lv_nu_post(const mg_ctx_s *c, const Level &L) { return L.nu_post >= 0 ? L.nu
 // --- persistent coarse tail ----------------------------------------------------
 template <int BS>
 mg_status tail_grid_size(mg_ctx_s *c) {
+  if (c->tail_cluster) {
+    // one cluster: 16 CTAs (non-portable size, opt-in) or the portable 8
+    cudaError_t e = cudaFuncSetAttribute(mgk::k_tail<BS, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    c->tail_grid = e == cudaSuccess ? 16 : 8;
+    cudaGetLastError();
+    return MG_OK;
+  }
   int per_sm = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgk::k_tail<BS>, mgk::kCta, 0));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgk::k_tail<BS, false>, mgk::kCta, 0));
   const int want = int(env_i64("MGB200_TAIL_CTAS", per_sm));
   c->tail_grid = unsigned(std::max(1, std::min(per_sm, want)) * c->n_sm);
   return MG_OK;
@@ -814,16 +822,22 @@ mg_status tail_grid_size(mg_ctx_s *c) {
 mg_status build_tail(mg_ctx_s *c) {
   c->tail_nops = 0;
   c->tail_T = -1;
-  // opt-in (MGB200_TAIL=1): measured slower than graph-launched standalone
-  // kernels on B200 (C2 0.39 vs 0.35 ms, C3 5.30 vs 5.18 ms per V-cycle) --
-  // its grid barriers cost more than CUDA-graph kernel boundaries
+  // MGB200_TAIL (opt-in, both measured slower than the graph-launched standalone
+  // kernels on B200): "1" -- grid-wide cooperative variant (grid barriers cost
+  // more than CUDA-graph kernel boundaries: C2 0.39 vs 0.35 ms per V-cycle);
+  // "c" -- tiny levels in one thread-block cluster with hardware cluster
+  // barriers (16 SMs lack the latency hiding of the whole GPU: C2 0.44 vs
+  // 0.32 ms, C1 47 vs 43 us).  Default off.
   const char *env = std::getenv("MGB200_TAIL");
-  if (!env || env[0] != '1') return MG_OK;
-  static const int64_t max_slices = env_i64("MGB200_TAIL_SLICES", 1024);
+  const char mode = env && *env ? env[0] : '0';
+  if (mode != '1' && mode != 'c') return MG_OK;
+  c->tail_cluster = mode == 'c';
+  const int64_t max_slices = env_i64("MGB200_TAIL_SLICES", c->tail_cluster ? 256 : 1024);
   int T = -1;
   for (int l = 0; l < c->L(); ++l) {
     const Level &L = c->lv[l];
-    if (L.dist || L.part[0].A.ks != 4 || (l > 0 && c->lv[l].R.ks != 4) || L.part[0].A.n_slices > max_slices) break;
+    const int ks = L.part[0].A.ks;
+    if (L.dist || (ks != 4 && ks != 8) || (l > 0 && c->lv[l].R.ks != 4) || L.part[0].A.n_slices > max_slices) break;
     T = l;
   }
   if (T < 1) return MG_OK;
@@ -860,6 +874,7 @@ mg_status build_tail(mg_ctx_s *c) {
     for (int i = 0; i < k; ++i) {
       mgk::TailOp o = base(mgk::T_SWEEP);
       o.A = L.part[0].A.view();
+      o.ks = L.part[0].A.ks;
       o.f32 = L.part[0].A.f32;
       o.x = src;
       o.b = b;
@@ -882,6 +897,7 @@ mg_status build_tail(mg_ctx_s *c) {
     emit_smooth(l, L.x.p, L.b.p, lv_nu_pre(c, L), true);
     mgk::TailOp r = base(mgk::T_RESID);
     r.A = L.part[0].A.view();
+    r.ks = L.part[0].A.ks;
     r.f32 = L.part[0].A.f32;
     r.x = L.x.p;
     r.b = L.b.p;
@@ -934,18 +950,26 @@ mg_status launch_tail(mg_ctx_s *c) {
   cfg.blockDim = dim3(mgk::kCta);
   cfg.stream = c->stream;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  if (c->tail_cluster) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = c->tail_grid;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+  } else {
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+  }
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const mgk::TailOp *ops = c->tail_ops.p;
   const int n = c->tail_nops;
   ++g_tally;
+  const bool cl = c->tail_cluster;
   switch (c->bs()) {
-    case 1: CU(cudaLaunchKernelEx(&cfg, mgk::k_tail<1>, ops, n)); break;
-    case 2: CU(cudaLaunchKernelEx(&cfg, mgk::k_tail<2>, ops, n)); break;
-    case 3: CU(cudaLaunchKernelEx(&cfg, mgk::k_tail<3>, ops, n)); break;
-    default: CU(cudaLaunchKernelEx(&cfg, mgk::k_tail<4>, ops, n)); break;
+    case 1: CU(cl ? cudaLaunchKernelEx(&cfg, mgk::k_tail<1, true>, ops, n) : cudaLaunchKernelEx(&cfg, mgk::k_tail<1, false>, ops, n)); break;
+    case 2: CU(cl ? cudaLaunchKernelEx(&cfg, mgk::k_tail<2, true>, ops, n) : cudaLaunchKernelEx(&cfg, mgk::k_tail<2, false>, ops, n)); break;
+    case 3: CU(cl ? cudaLaunchKernelEx(&cfg, mgk::k_tail<3, true>, ops, n) : cudaLaunchKernelEx(&cfg, mgk::k_tail<3, false>, ops, n)); break;
+    default: CU(cl ? cudaLaunchKernelEx(&cfg, mgk::k_tail<4, true>, ops, n) : cudaLaunchKernelEx(&cfg, mgk::k_tail<4, false>, ops, n)); break;
   }
   return MG_OK;
 }

@@ -16,19 +16,17 @@ for _ in range(50): S.precondition(z, b)
 e1.record(); torch.cuda.synchronize()
 print(json.dumps({"vcycle_ms": e0.elapsed_time(e1) / 50}))
 '''
-settings = [("0", "1024", "0"), ("1", "256", "0")]
+settings = [("0", "1024", "0"), ("c", "64", "0"), ("c", "128", "0"), ("c", "256", "0"), ("c", "600", "0")]
 for cfg in sys.argv[1:]:
     path = f"/tmp/tail_{cfg}.pkl"
     if not os.path.exists(path):
         from problems import configs
         pickle.dump(configs.build(cfg, keep_geometry=False), open(path, "wb"), protocol=4)
-    for ks8 in ("0", "256", "1024"):
+    for ks8 in ("256",):
       for tail, sl, ctas in settings:
         env = dict(os.environ, MGB200_TAIL=tail, MGB200_TAIL_SLICES=sl, MGB200_KS8_SLICES=ks8)
         if ctas != "0":
             env["MGB200_TAIL_CTAS"] = ctas
-        if tail == "1" and ks8 != "0":
-            continue
         out = subprocess.run([sys.executable, "-c", child, path], env=env, capture_output=True, text=True)
         line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-300:]
         print(cfg, "ks8<", ks8, "tail", tail, "slices<=", sl, line, flush=True)

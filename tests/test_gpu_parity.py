@@ -389,7 +389,7 @@ def test_coarse_tail_kernel_bitidentical(name, coarse_mode, precision, monkeypat
     import paper_2405_05047_b200 as m
     lv, bs, om, b, H = case(name)
     outs = []
-    for tail in ("1", "0"):                       # opt-in kernel vs the default standalone path
+    for tail in ("1", "c", "0"):                  # grid-barrier tail, cluster tail, standalone kernels
         monkeypatch.setenv("MGB200_TAIL", tail)
         g = build_gpu(lv, bs, omega=om, H=H, coarse_mode=coarse_mode, precision=precision)
         z = dev(np.zeros(lv[-1].n * bs))
@@ -398,5 +398,6 @@ def test_coarse_tail_kernel_bitidentical(name, coarse_mode, precision, monkeypat
         st, its, rel, conv = m.mg_solve(g.ctx, x, dev(b), rtol=1e-10)
         outs.append((host(z), its, host(x)))
         g.close()
-    assert np.array_equal(outs[0][0], outs[1][0])
-    assert outs[0][1] == outs[1][1] and np.array_equal(outs[0][2], outs[1][2])
+    for o in outs[1:]:
+        assert np.array_equal(outs[0][0], o[0])
+        assert outs[0][1] == o[1] and np.array_equal(outs[0][2], o[2])
