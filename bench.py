@@ -377,6 +377,19 @@ def run_ours(args):
     sw_ms = sum(a.elapsed_time(c) for a, c in evs) / ns
     sweep_b, _, _ = level_bytes(infos[L], bs, False, vb)
     achieved = sweep_b / (sw_ms / 1e3) / 1e9
+    # plain SpMV y = A x of the finest level (the GMRES operator; BASELINE metric
+    # "SpMV HBM GB/s as % of peak"): z (8 bs^2 + 4) + 8 (n + 1) + 16 bs n bytes
+    for _ in range(3):
+        mg.mg_spmv(ctx, L, 1.0, xin, 0.0, xout)
+    torch.cuda.synchronize()
+    for a, c_ in evs:
+        a.record(stream)
+        mg.mg_spmv(ctx, L, 1.0, xin, 0.0, xout)
+        c_.record(stream)
+    torch.cuda.synchronize()
+    spmv_ms = sum(a.elapsed_time(c_) for a, c_ in evs) / ns
+    nL, zL = infos[L]["n"], infos[L]["nnzb"]
+    spmv_b = zL * (8 * bs * bs + 4) + 8 * (nL + 1) + 16 * bs * nL
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -463,6 +476,9 @@ def run_ours(args):
                          "achieved": achieved,
                          "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "alg_bytes_per_launch": sweep_b, "avg_launch_ms": sw_ms},
+            "spmv_hbm": {"kernel": f"k_sell_apply<{bs},SPMV> finest level (fp64)", "avg_launch_ms": spmv_ms,
+                         "alg_bytes_per_launch": spmv_b, "gbs": spmv_b / (spmv_ms / 1e3) / 1e9,
+                         "frac": spmv_b / (spmv_ms / 1e3) / 1e9 / peak},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "V-cycles/s", "h2d_bytes_per_step": 8 * n_global,
                     "d2h_bytes_per_step": 8 * n_global},

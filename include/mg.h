@@ -37,7 +37,8 @@
  * return.  Vectors x, b, r, y passed to compute calls are caller-owned DEVICE
  * buffers of the level's rows x bs fp64 values; the library never keeps these
  * pointers past the call (graph caches key on the address only).  Outputs
- * must not alias inputs unless stated.
+ * must not alias inputs unless stated.  A rank that owns no rows of a level
+ * may pass NULL vectors for it.
  *
  * Streams: all device work is ordered on the context's stream (the
  * cudaStream_t passed to mg_create, or an internal blocking stream if NULL,

@@ -1188,6 +1188,9 @@ struct Tally {
   }
 };
 
+// rows of the finest level owned here (0 on a rank without rows: NULL vectors allowed)
+int64_t fine_n(const mg_ctx_s *c) { return c->lv[c->L()].n; }
+
 mg_status check_ctx(mg_ctx_s *c) {
   if (!c) return fail(MG_ERR_INVALID_ARG, "NULL context");
   return MG_OK;
@@ -1680,7 +1683,8 @@ mg_status mg_setup(mg_ctx c) {
 
 mg_status mg_vcycle(mg_ctx c, double *x, const double *b) {
   TRY(check_ctx(c));
-  if (!x || !b || x == b) return fail(MG_ERR_INVALID_ARG, "x, b must be distinct non-NULL device pointers");
+  if ((fine_n(c) > 0 && (!x || !b)) || (x && x == b))
+    return fail(MG_ERR_INVALID_ARG, "x, b must be distinct non-NULL device pointers");
   DeviceGuard dg(c->device);
   Tally tally(c);
   TRY(finalize(c));
@@ -1689,7 +1693,8 @@ mg_status mg_vcycle(mg_ctx c, double *x, const double *b) {
 
 mg_status mg_vcycle_zero(mg_ctx c, double *z, const double *v) {
   TRY(check_ctx(c));
-  if (!z || !v || z == v) return fail(MG_ERR_INVALID_ARG, "z, v must be distinct non-NULL device pointers");
+  if ((fine_n(c) > 0 && (!z || !v)) || (z && z == v))
+    return fail(MG_ERR_INVALID_ARG, "z, v must be distinct non-NULL device pointers");
   DeviceGuard dg(c->device);
   Tally tally(c);
   TRY(finalize(c));
@@ -1698,7 +1703,8 @@ mg_status mg_vcycle_zero(mg_ctx c, double *z, const double *v) {
 
 mg_status mg_spmv(mg_ctx c, int level, double alpha, const double *x, double beta, double *y) {
   TRY(check_level(c, level));
-  if (!x || !y || x == y) return fail(MG_ERR_INVALID_ARG, "x, y must be distinct non-NULL device pointers");
+  if ((c->lv[level].n > 0 && (!x || !y)) || (x && x == y))
+    return fail(MG_ERR_INVALID_ARG, "x, y must be distinct non-NULL device pointers");
   if (!c->lv[level].part[0].A.set) return fail(MG_ERR_STATE, "level %d has no matrix", level);
   DeviceGuard dg(c->device);
   Tally tally(c);
@@ -1707,7 +1713,8 @@ mg_status mg_spmv(mg_ctx c, int level, double alpha, const double *x, double bet
 
 mg_status mg_sweep(mg_ctx c, int level, const double *x, const double *b, double *x_out) {
   TRY(check_level(c, level));
-  if (!x || !b || !x_out || x_out == x || x_out == b) return fail(MG_ERR_INVALID_ARG, "x_out must not alias x or b");
+  if ((c->lv[level].n > 0 && (!x || !b || !x_out)) || (x_out && (x_out == x || x_out == b)))
+    return fail(MG_ERR_INVALID_ARG, "x_out must not alias x or b");
   DeviceGuard dg(c->device);
   Tally tally(c);
   TRY(finalize(c));
@@ -1716,7 +1723,8 @@ mg_status mg_sweep(mg_ctx c, int level, const double *x, const double *b, double
 
 mg_status mg_residual(mg_ctx c, int level, const double *x, const double *b, double *r) {
   TRY(check_level(c, level));
-  if (!x || !b || !r || r == x || r == b) return fail(MG_ERR_INVALID_ARG, "r must not alias x or b");
+  if ((c->lv[level].n > 0 && (!x || !b || !r)) || (r && (r == x || r == b)))
+    return fail(MG_ERR_INVALID_ARG, "r must not alias x or b");
   if (!c->lv[level].part[0].A.set) return fail(MG_ERR_STATE, "level %d has no matrix", level);
   DeviceGuard dg(c->device);
   Tally tally(c);
@@ -1725,7 +1733,8 @@ mg_status mg_residual(mg_ctx c, int level, const double *x, const double *b, dou
 
 mg_status mg_smooth(mg_ctx c, int level, double *x, const double *b, int sweeps) {
   TRY(check_level(c, level));
-  if (!x || !b || x == b) return fail(MG_ERR_INVALID_ARG, "x, b must be distinct non-NULL device pointers");
+  if ((c->lv[level].n > 0 && (!x || !b)) || (x && x == b))
+    return fail(MG_ERR_INVALID_ARG, "x, b must be distinct non-NULL device pointers");
   if (sweeps < 0) return fail(MG_ERR_INVALID_ARG, "sweeps < 0");
   DeviceGuard dg(c->device);
   Tally tally(c);
@@ -1762,7 +1771,7 @@ mg_status mg_coarse_solve(mg_ctx c, const double *d, double *y) {
 
 mg_status mg_apply_constraints(mg_ctx c, double *x) {
   TRY(check_ctx(c));
-  if (!x) return fail(MG_ERR_INVALID_ARG, "NULL vector");
+  if (fine_n(c) > 0 && !x) return fail(MG_ERR_INVALID_ARG, "NULL vector");
   if (!c->H.set) return fail(MG_ERR_STATE, "no hanging-node matrix (mg_set_constraints)");
   DeviceGuard dg(c->device);
   Tally tally(c);
@@ -1826,7 +1835,8 @@ mg_status mg_update_matrix(mg_ctx c, int level, const double *vals, int mem) {
 
 mg_status mg_condense_rhs(mg_ctx c, const double *b, double *b_bar) {
   TRY(check_ctx(c));
-  if (!b || !b_bar || b == b_bar) return fail(MG_ERR_INVALID_ARG, "b, b_bar must be distinct non-NULL device pointers");
+  if ((fine_n(c) > 0 && (!b || !b_bar)) || (b && b == b_bar))
+    return fail(MG_ERR_INVALID_ARG, "b, b_bar must be distinct non-NULL device pointers");
   if (!c->HT.set) return fail(MG_ERR_STATE, "no hanging-node matrix (mg_set_constraints)");
   DeviceGuard dg(c->device);
   Tally tally(c);
@@ -1838,7 +1848,7 @@ mg_status mg_condense_rhs(mg_ctx c, const double *b, double *b_bar) {
 
 mg_status mg_dot(mg_ctx c, int level, const double *a, const double *b, double *out_host) {
   TRY(check_level(c, level));
-  if (!a || !b || !out_host) return fail(MG_ERR_INVALID_ARG, "NULL argument");
+  if (!out_host || (c->lv[level].n > 0 && (!a || !b))) return fail(MG_ERR_INVALID_ARG, "NULL argument");
   DeviceGuard dg(c->device);
   Tally tally(c);
   TRY(finalize(c));
@@ -1893,7 +1903,7 @@ int mgi_level_info(mgi_ctx c, int level, int64_t *n, int64_t *nnzb, int64_t *sel
 
 mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *opts, mg_solve_info *info) {
   TRY(check_ctx(c));
-  if (!x || !b || !opts || x == b) return fail(MG_ERR_INVALID_ARG, "bad arguments");
+  if (!opts || (fine_n(c) > 0 && (!x || !b)) || (x && x == b)) return fail(MG_ERR_INVALID_ARG, "bad arguments");
   if (opts->max_iter < 0 || !(opts->rtol >= 0.0)) return fail(MG_ERR_INVALID_ARG, "bad options");
   DeviceGuard dg(c->device);
   Tally tally(c);

@@ -67,10 +67,12 @@ def splitters(problem, nranks, min_rows_per_rank=64, replicate_level0=True):
     return out[::-1]
 
 
-def partition(problem, nranks, min_rows_per_rank=64, replicate_level0=True, only_rank=None):
+def partition(problem, nranks, min_rows_per_rank=64, replicate_level0=True, only_rank=None, ranges=None):
     """Returns (per-rank list of RankLevel lists, per-rank (b_local, H_local), ranges).
-    only_rank: build the data of that rank only (the other entries are None)."""
-    ranges = splitters(problem, nranks, min_rows_per_rank, replicate_level0)
+    only_rank: build the data of that rank only (the other entries are None).
+    ranges: explicit per-level row ranges (overrides the splitters; edge-case tests)."""
+    if ranges is None:
+        ranges = splitters(problem, nranks, min_rows_per_rank, replicate_level0)
     bs = problem.bs
     ranks = []
     extras = []

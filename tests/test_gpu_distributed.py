@@ -263,3 +263,35 @@ def test_distributed_mixed_precision_and_overlap(overlap, monkeypatch):
     assert all(o[1][3] for o in out) and abs(out[0][1][1] - its1) <= 1
     for g in mgs:
         g.close()
+
+
+def test_distributed_rank_without_rows():
+    """Edge case: rank 1 owns no rows of a distributed level (NULL vectors from
+    empty tensors); the V-cycle stays bit-identical and GMRES matches."""
+    import paper_2405_05047_b200 as m
+    from problems.partition import partition
+    Pr = problem("c3_small")                        # levels [125, 455, 2925]
+    n0, n1, n2 = (L.n for L in Pr.levels)
+    ranges = [[(0, n0), (0, n0)], [(0, n1), (n1, n1)], [(0, 1400), (1400, n2)]]
+    parts, extras, _ = partition(Pr, 2, ranges=ranges)
+    key = os.urandom(16)
+    mgs = run_ranks(2, lambda r: build_gpu(parts[r], Pr.bs, omega=Pr.omega, H=extras[r][1],
+                                           comm=(2, r, key, m.MG_TRANSPORT_LOCAL)))
+    s = build_gpu(Pr.levels, Pr.bs, omega=Pr.omega, H=Pr.fine.H)
+    z = dev(np.zeros(Pr.n_dof))
+    m.mg_vcycle_zero(s.ctx, z, dev(Pr.b))
+    _, its1, _, _ = m.mg_solve(s.ctx, dev(np.zeros(Pr.n_dof)), dev(Pr.b), rtol=1e-10)
+
+    def work(r):
+        f0, f1 = ranges[-1][r]
+        zz = dev(np.zeros((f1 - f0) * Pr.bs))
+        m.mg_vcycle_zero(mgs[r].ctx, zz, dev(extras[r][0]))
+        # per-op calls on the level this rank owns no rows of: empty (NULL) vectors
+        e = dev(np.zeros((ranges[1][r][1] - ranges[1][r][0]) * Pr.bs))
+        e2 = dev(np.zeros_like(host(e)))
+        m.mg_residual(mgs[r].ctx, 1, e, e2, dev(np.zeros_like(host(e))))
+        out = m.mg_solve(mgs[r].ctx, dev(np.zeros((f1 - f0) * Pr.bs)), dev(extras[r][0]), rtol=1e-10)
+        return host(zz), out
+    out = run_ranks(2, work)
+    assert np.array_equal(np.concatenate([o[0] for o in out]), host(z))
+    assert all(o[1][3] for o in out) and abs(out[0][1][1] - its1) <= 1

@@ -214,3 +214,27 @@ def test_oh2_convergence_with_hanging_nodes():
         errs.append(_l2_error(p, x))
     ratios = [errs[i] / errs[i + 1] for i in range(len(errs) - 1)]
     assert all(3.6 < r < 4.4 for r in ratios), ratios
+
+
+def test_gmres_outer_operator_pin():
+    """O.gmres(op=...) (mixed-precision preconditioning): with a
+    preconditioner hierarchy built on perturbed (fp32-rounded) operators, GMRES
+    must still converge to the solution of the OUTER operator -- pinned by a
+    dense LU of that operator -- and must not converge to the perturbed one."""
+    from types import SimpleNamespace
+    P = C.build("c3_small")
+    F = P.fine
+    rounded = []
+    for L in P.levels:
+        R = SimpleNamespace(n=L.n, bs=L.bs, row_ptr=L.row_ptr, col=L.col, P=L.P, wpe=L.wpe,
+                            val=L.val.astype(np.float32).astype(np.float64))
+        rounded.append(R)
+    h32 = O.MgHierarchy.from_arrays(rounded, omega=P.omega)
+    op = SimpleNamespace(n=F.n, bs=F.bs, rp=F.row_ptr, col=F.col, val=F.val)
+    x, its, hist, rel = O.gmres(h32, P.b, rtol=1e-12, op=op)
+    A = O.bsr_to_dense(F.n, F.bs, F.row_ptr, F.col, F.val)
+    xe = np.linalg.solve(A, P.b)
+    assert np.linalg.norm(x - xe) <= 1e-9 * np.linalg.norm(xe)
+    A32 = O.bsr_to_dense(F.n, F.bs, F.row_ptr, F.col, rounded[-1].val)
+    x32 = np.linalg.solve(A32, P.b)
+    assert np.linalg.norm(x32 - xe) > 1e3 * np.linalg.norm(x - xe)
