@@ -20,12 +20,13 @@ from problems import configs  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("mode", choices=["step", "kernels", "vcycle"])
 ap.add_argument("--config", default="c3")
+ap.add_argument("--mixed", action="store_true")
 a = ap.parse_args()
 
 t = time.time()
 P = configs.build(a.config, keep_geometry=False)
 print(f"gen {a.config} {P.n_dof} DOFs {time.time() - t:.1f}s", file=sys.stderr, flush=True)
-S = m.Multigrid(P.levels, P.bs, omega=P.omega, H=P.fine.H)
+S = m.Multigrid(P.levels, P.bs, omega=P.omega, H=P.fine.H, precision=m.MG_PREC_MIXED if a.mixed else 0)
 ctx = S.ctx
 Lf = len(P.levels) - 1
 b = torch.from_numpy(P.b).cuda()
