@@ -40,6 +40,9 @@ WORKLOADS = {
     "c1": "C1: 2D transport-diffusion Q1, uniform 32x32 (1089 DOFs), 4 levels",
     "c4": "C4: 2D NS-shaped generalised Stokes (PSPG, eps M_p), Q1 3x3 blocks (p,u,v), lid cavity band-refined "
           "toward the lid (32^2 root, 6 steps), 7 levels, per-component transfers, GMRES(30)+V(2,2) omega=0.8",
+    "e6": "N4: the paper's 6-component elasticity system (u, v), backward Euler (P:441-445), 6x6 blocks, "
+          "Table ndofs face mesh L5 (8^3 root, K=1 band toward x=0): 1,035,030 DOFs as in P:537, "
+          "GMRES(30)+V(2,2) block-Jacobi omega=0.5, direct coarse solve",
     "c5": "C5: 3D NS-shaped generalised Stokes (PSPG, eps M_p), Q1 4x4 blocks (p,u,v,w), (0,1)^2x(0,2) cavity, "
           "128x128x256 cells, 6 levels, per-component transfers, GMRES(30)+V(2,2) omega=0.6",
 }
@@ -139,7 +142,7 @@ def vcycle_bytes(infos, bs, nu=(2, 2), zero=True, coarse_direct=True, vb=8):
 def build_problem(name):
     from problems import configs
     t = time.time()
-    P = configs.build(name, keep_geometry=False)
+    P = configs.build({"e6": "e6_face_l5"}.get(name, name), keep_geometry=False)
     log(f"[bench] generated {name}: {P.n_dof} DOFs, levels {[l.n for l in P.levels]} in {time.time() - t:.1f}s")
     return P
 

@@ -19,7 +19,8 @@
  *   - hanging-node interpolation y = H x.
  *
  * Data layout at the boundary (P:108, P:283 node-blocked unknowns):
- *   - block size bs = number of solution components n_c, 1 <= bs <= 4;
+ *   - block size bs = number of solution components n_c: 1, 2, 3, 4 or 6
+ *     (6: the paper's first-order elasticity system (u, v));
  *   - vectors: fp64, node-major [n_rows * bs] (x_{i,c} at i*bs + c);
  *   - matrices: block-CSR (BSR), int64 row_ptr[n_rows+1] (row_ptr[0] == 0),
  *     int64 block column indices (strictly increasing within a row, in

@@ -405,6 +405,7 @@ mg_status launch_apply(int bs, const SellOp &A, In in, const double *b, const do
     case 2: launch_apply_t<2, OP>(A, in, b, dinv, out, alpha, beta, st); break;
     case 3: launch_apply_t<3, OP>(A, in, b, dinv, out, alpha, beta, st); break;
     case 4: launch_apply_t<4, OP>(A, in, b, dinv, out, alpha, beta, st); break;
+    case 6: launch_apply_t<6, OP>(A, in, b, dinv, out, alpha, beta, st); break;
     default: return fail(MG_ERR_INVALID_ARG, "block size %d not supported", bs);
   }
   return check_launch(OP == mgk::OP_SWEEP ? "sweep" : OP == mgk::OP_RESID ? "residual" : "spmv");
@@ -424,6 +425,7 @@ mg_status launch_sweep0(int bs, const SellOp &A, const double *dinv, const doubl
     case 2: launch_sweep0_t<2>(A, dinv, b, x, omega, st); break;
     case 3: launch_sweep0_t<3>(A, dinv, b, x, omega, st); break;
     case 4: launch_sweep0_t<4>(A, dinv, b, x, omega, st); break;
+    case 6: launch_sweep0_t<6>(A, dinv, b, x, omega, st); break;
     default: return fail(MG_ERR_INVALID_ARG, "block size %d not supported", bs);
   }
   return check_launch("sweep0");
@@ -462,6 +464,7 @@ mg_status launch_transfer(int bs, bool acc, const SellOp &T, In in, double *out,
     case 2: acc ? launch_transfer_bs<2, true>(T, in, out, st) : launch_transfer_bs<2, false>(T, in, out, st); break;
     case 3: acc ? launch_transfer_bs<3, true>(T, in, out, st) : launch_transfer_bs<3, false>(T, in, out, st); break;
     case 4: acc ? launch_transfer_bs<4, true>(T, in, out, st) : launch_transfer_bs<4, false>(T, in, out, st); break;
+    case 6: acc ? launch_transfer_bs<6, true>(T, in, out, st) : launch_transfer_bs<6, false>(T, in, out, st); break;
     default: return fail(MG_ERR_INVALID_ARG, "block size %d not supported", bs);
   }
   return check_launch(acc ? "prolong-add" : "transfer");
@@ -486,7 +489,8 @@ mg_status halo_pack(mg_ctx_s *c, Halo &h, const double *v) {
       case 1: ++g_tally, mgk::k_pack<1><<<g, 256, 0, c->stream>>>(ns, h.send_idx.p, v, h.sendbuf.p); break;
       case 2: ++g_tally, mgk::k_pack<2><<<g, 256, 0, c->stream>>>(ns, h.send_idx.p, v, h.sendbuf.p); break;
       case 3: ++g_tally, mgk::k_pack<3><<<g, 256, 0, c->stream>>>(ns, h.send_idx.p, v, h.sendbuf.p); break;
-      default: ++g_tally, mgk::k_pack<4><<<g, 256, 0, c->stream>>>(ns, h.send_idx.p, v, h.sendbuf.p); break;
+      case 4: ++g_tally, mgk::k_pack<4><<<g, 256, 0, c->stream>>>(ns, h.send_idx.p, v, h.sendbuf.p); break;
+      default: ++g_tally, mgk::k_pack<6><<<g, 256, 0, c->stream>>>(ns, h.send_idx.p, v, h.sendbuf.p); break;
     }
     TRY(check_launch("halo pack"));
   }
@@ -783,7 +787,8 @@ mg_status device_dinv(mg_ctx_s *c, int l) {
       case 1: mgk::k_block_inverse<1><<<g, 256, 0, c->stream>>>(Pt.n, Pt.udiag_e.p, v64, v32, Pt.upos.p, Pt.dinv.p, flag.p); break;
       case 2: mgk::k_block_inverse<2><<<g, 256, 0, c->stream>>>(Pt.n, Pt.udiag_e.p, v64, v32, Pt.upos.p, Pt.dinv.p, flag.p); break;
       case 3: mgk::k_block_inverse<3><<<g, 256, 0, c->stream>>>(Pt.n, Pt.udiag_e.p, v64, v32, Pt.upos.p, Pt.dinv.p, flag.p); break;
-      default: mgk::k_block_inverse<4><<<g, 256, 0, c->stream>>>(Pt.n, Pt.udiag_e.p, v64, v32, Pt.upos.p, Pt.dinv.p, flag.p); break;
+      case 4: mgk::k_block_inverse<4><<<g, 256, 0, c->stream>>>(Pt.n, Pt.udiag_e.p, v64, v32, Pt.upos.p, Pt.dinv.p, flag.p); break;
+      default: mgk::k_block_inverse<6><<<g, 256, 0, c->stream>>>(Pt.n, Pt.udiag_e.p, v64, v32, Pt.upos.p, Pt.dinv.p, flag.p); break;
     }
     TRY(check_launch("block inverse"));
   }
@@ -939,7 +944,8 @@ mg_status build_tail(mg_ctx_s *c) {
     case 1: TRY(tail_grid_size<1>(c)); break;
     case 2: TRY(tail_grid_size<2>(c)); break;
     case 3: TRY(tail_grid_size<3>(c)); break;
-    default: TRY(tail_grid_size<4>(c)); break;
+    case 4: TRY(tail_grid_size<4>(c)); break;
+    default: TRY(tail_grid_size<6>(c)); break;
   }
   return MG_OK;
 }
@@ -969,7 +975,8 @@ mg_status launch_tail(mg_ctx_s *c) {
     case 1: CU(cl ? cudaLaunchKernelEx(&cfg, mgk::k_tail<1, true>, ops, n) : cudaLaunchKernelEx(&cfg, mgk::k_tail<1, false>, ops, n)); break;
     case 2: CU(cl ? cudaLaunchKernelEx(&cfg, mgk::k_tail<2, true>, ops, n) : cudaLaunchKernelEx(&cfg, mgk::k_tail<2, false>, ops, n)); break;
     case 3: CU(cl ? cudaLaunchKernelEx(&cfg, mgk::k_tail<3, true>, ops, n) : cudaLaunchKernelEx(&cfg, mgk::k_tail<3, false>, ops, n)); break;
-    default: CU(cl ? cudaLaunchKernelEx(&cfg, mgk::k_tail<4, true>, ops, n) : cudaLaunchKernelEx(&cfg, mgk::k_tail<4, false>, ops, n)); break;
+    case 4: CU(cl ? cudaLaunchKernelEx(&cfg, mgk::k_tail<4, true>, ops, n) : cudaLaunchKernelEx(&cfg, mgk::k_tail<4, false>, ops, n)); break;
+    default: CU(cl ? cudaLaunchKernelEx(&cfg, mgk::k_tail<6, true>, ops, n) : cudaLaunchKernelEx(&cfg, mgk::k_tail<6, false>, ops, n)); break;
   }
   return MG_OK;
 }
@@ -1316,7 +1323,8 @@ mg_status mg_create(mg_ctx *out, const mg_config *cfg, int device, void *cuda_st
   if (!out || !cfg) return fail(MG_ERR_INVALID_ARG, "NULL argument");
   *out = nullptr;
   if (cfg->n_levels < 1 || cfg->n_levels > 64) return fail(MG_ERR_INVALID_ARG, "n_levels must be in [1, 64]");
-  if (cfg->block_size < 1 || cfg->block_size > 4) return fail(MG_ERR_INVALID_ARG, "block_size must be in [1, 4]");
+  if (cfg->block_size < 1 || cfg->block_size > 6 || cfg->block_size == 5)
+    return fail(MG_ERR_INVALID_ARG, "block_size must be 1, 2, 3, 4 or 6");
   if (cfg->nu_pre < 0 || cfg->nu_post < 0) return fail(MG_ERR_INVALID_ARG, "nu_pre/nu_post must be >= 0");
   if (!(cfg->omega > 0.0) || !std::isfinite(cfg->omega)) return fail(MG_ERR_INVALID_ARG, "omega must be > 0");
   if (cfg->coarse_mode != MG_COARSE_DIRECT && cfg->coarse_mode != MG_COARSE_SMOOTH)

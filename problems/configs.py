@@ -222,6 +222,15 @@ CONFIGS = {
 
 
 CONFIGS.update({
+    # N4: the paper's 6-component (u, v) elasticity system on Table `ndofs` face meshes (8^3 root,
+    # K = 1 band toward x = 0): L2 = 2,925 nodes = 17,550 DOFs ... L5 = 172,505 nodes = 1,035,030 DOFs
+    #
+    "e6_face_l2": ((8, 8, 8), (1.0, 1.0, 1.0), [("band", [0], 1)] * 1,
+                   F.Operator("elasticity6", 6, False, ELAST), 0.5, 5),
+    "e6_face_l3": ((8, 8, 8), (1.0, 1.0, 1.0), [("band", [0], 1)] * 2,
+                   F.Operator("elasticity6", 6, False, ELAST), 0.5, 5),
+    "e6_face_l5": ((8, 8, 8), (1.0, 1.0, 1.0), [("band", [0], 1)] * 4,
+                   F.Operator("elasticity6", 6, False, ELAST), 0.5, 5),
     # C4: 2D NS-shaped generalised Stokes, 3x3 blocks (p, u, v), lid cavity, band toward the lid
     "c4": ((32, 32), (1.0, 1.0), [("band", [1], 20)] * 6, F.Operator("stokes", 3, False, STOKES2), 0.8, 3),
     "c4_small": ((8, 8), (1.0, 1.0), [("band", [1], 2)] * 3, F.Operator("stokes", 3, False, STOKES2), 0.8, 3),

@@ -149,6 +149,37 @@ def element_terms(op: Operator, dim: int, h: np.ndarray):
                     T2.append(_sym(T[ia] + T[ib]))
                 S2.append(S[ia])
         T, S = T2, S2
+    elif op.name == "elasticity6":
+        # The paper's first-order system for (u, v), backward Euler,
+        # unknowns (u_1..u_d, v_1..v_d) node-major (reading N4):
+        #   (u^m - u^{m-1})/dt - v^m = 0        ->  M u - dt M v        = M u^{m-1}
+        #   (v^m - v^{m-1})/dt - div s(u^m) = f  ->  dt K_e u + M v      = M v^{m-1} + dt M f
+        bs = 2 * dim
+        lam, mu, dt = p["lam"], p["mu"], p["dt"]
+        E = np.eye(dim)
+
+        def place(Auu=None, Auv=None, Avu=None, Avv=None):
+            Tb = np.zeros((nloc, bs, nloc, bs))
+            for (blk, r0, c0) in ((Auu, 0, 0), (Auv, 0, dim), (Avu, dim, 0), (Avv, dim, dim)):
+                if blk is not None:
+                    Tb[:, r0:r0 + dim, :, c0:c0 + dim] = blk
+            return Tb.reshape(nloc * bs, nloc * bs)
+
+        Mb = np.einsum("ij,cd->icjd", Mref, E)
+        T.append(place(Auu=Mb, Avv=Mb))
+        S.append(vol)
+        T.append(place(Auv=-Mb))
+        S.append(dt * vol)
+        for a in range(dim):
+            for b in range(dim):
+                Kab = np.zeros((nloc, dim, nloc, dim))
+                Kab[:, a, :, b] += lam * G[a, b]
+                Kab[:, b, :, a] += mu * G[a, b]
+                if a == b:
+                    for c in range(dim):
+                        Kab[:, c, :, c] += mu * G[a, a]
+                T.append(place(Avu=Kab))
+                S.append(dt * vol / (h[:, a] * h[:, b]))
     elif op.name == "stokes":
         # Generalised Stokes, equal-order Q1, unknowns (p, u_1..u_d) node-major
         # (P:108), PSPG stabilisation + pressure-mass regularisation (reading Z23):

@@ -61,7 +61,8 @@ def gather(vals, ranges_fine, bs):
     return np.concatenate([v.reshape(-1, bs) for v in vals]).reshape(-1)
 
 
-CASES = [("c3_small", 2), ("c3_small", 3), ("c2_small", 2), ("c3_mid", 4), ("c4_small", 2), ("c5_mid", 3)]
+CASES = [("c3_small", 2), ("c3_small", 3), ("c2_small", 2), ("c3_mid", 4), ("c4_small", 2), ("c5_mid", 3),
+         ("e6_face_l3", 2)]
 
 
 @pytest.mark.parametrize("name,P", CASES)

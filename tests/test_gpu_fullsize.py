@@ -18,7 +18,7 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 @functools.lru_cache(maxsize=None)
 def full(name):
     from problems import configs
-    P = configs.build(name, keep_geometry=False)
+    P = configs.build({"e6": "e6_face_l5"}.get(name, name), keep_geometry=False)
     mg = build_gpu(P.levels, P.bs, omega=P.omega, H=P.fine.H)
     return P, mg
 
@@ -40,7 +40,7 @@ def sub_csr(rp, col, val, rows, vpe):
     return srp, col[idx], v
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5", "e6"])
 def test_fullsize_residual_sweep_sampled(name):
     import paper_2405_05047_b200 as m
     P, mg = full(name)
@@ -128,7 +128,7 @@ def test_fullsize_vcycle_properties(name):
         assert rn < 0.9 * np.linalg.norm(P.b)
 
 
-@pytest.mark.parametrize("name", ["c3", "c5"])
+@pytest.mark.parametrize("name", ["c3", "c5", "e6"])
 def test_fullsize_gmres_converges(name):
     import paper_2405_05047_b200 as m
     P, mg = full(name)

@@ -17,7 +17,7 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 
-FE_CASES = ["c1", "c2_small", "c3_small", "c4_small", "c5_small"]
+FE_CASES = ["c1", "c2_small", "c3_small", "c4_small", "c5_small", "e6_face_l2"]
 SYN_CASES = ["syn_bs2", "syn_bs4", "syn_bs3_w1"]
 
 
