@@ -183,4 +183,4 @@ def bsr_to_dense(n, bs, rp, col, val):
     return A
 
 
-from .mg import (MgHierarchy, MgLevel, gmres, richardson, vcycle)  # noqa: E402,F401
+from .mg import (MgHierarchy, MgLevel, consistent, gmres, project_zero_mean, richardson, vcycle)  # noqa: E402,F401

@@ -42,11 +42,16 @@ class MgHierarchy:
     coarse_sweeps: int = 20
     H: tuple | None = None        # fine-level hanging matrix
     lu: tuple | None = field(default=None, repr=False)
+    mean: list | None = None      # per level: (w, k) of the global constraint w^T x = 0, or None
 
     @classmethod
-    def from_arrays(cls, levels, omega=0.8, nu_pre=2, nu_post=2, coarse="direct", coarse_sweeps=20, H=None):
+    def from_arrays(cls, levels, omega=0.8, nu_pre=2, nu_post=2, coarse="direct", coarse_sweeps=20, H=None,
+                    mean=None):
         """levels: list (coarse -> fine) of objects with n, bs, row_ptr, col, val,
-        P (or None), wpe."""
+        P (or None), wpe.  mean: per level (w, k) or None -- the global
+        constraint int_Omega p = w^T x = 0 imposed on every level of a
+        singular operator with kernel span{k} (pure-Neumann scalar problems:
+        k = 1 on free DOFs, 0 on identity rows; w = lumped-mass weights)."""
         out = []
         for l, L in enumerate(levels):
             lv = MgLevel(L.n, L.bs, np.asarray(L.row_ptr, np.int64), np.asarray(L.col, np.int64),
@@ -57,9 +62,15 @@ class MgHierarchy:
                 lv.R = csr_transpose(lv.n, out[-1].n, prp, pcol, pw, lv.wpe)
             out.append(lv)
         h = cls(out, omega, nu_pre, nu_post, coarse, coarse_sweeps, H)
+        if mean is not None:
+            h.mean = [None if c is None else (np.asarray(c[0], np.float64), np.asarray(c[1], np.float64))
+                      for c in mean]
         if coarse == "direct":
             c = out[0]
-            h.lu = lu_factor(bsr_to_dense(c.n, c.bs, c.rp, c.col, c.val))
+            A0 = bsr_to_dense(c.n, c.bs, c.rp, c.col, c.val)
+            if h.mean is not None and h.mean[0] is not None:
+                A0 = A0 + coarse_regularisation(A0, h.mean[0][0])
+            h.lu = lu_factor(A0)
         return h
 
     # --- the operations of Alg. gmg on level l -------------------------------
@@ -94,19 +105,51 @@ class MgHierarchy:
         return x
 
 
+def project_zero_mean(x, w, k=None):
+    """x - (w^T x / w^T k) k: zero weighted mean, i.e. int x_h = 0 with lumped-mass
+    weights w (SPEC project_zero_mean S:452-460); k = 1 by default, the
+    kernel vector (1 on free DOFs, 0 on identity rows) otherwise."""
+    x = np.asarray(x, np.float64)
+    k = np.ones_like(x) if k is None else np.asarray(k, np.float64)
+    return x - dot(w, x) / dot(w, k) * k
+
+
+def consistent(b, k=None):
+    """b - (k^T b / k^T k) k: the Euclidean projection onto range(A) = k-perp of a
+    symmetric operator with kernel span{k} (solvability of the Neumann problem)."""
+    b = np.asarray(b, np.float64)
+    k = np.ones_like(b) if k is None else np.asarray(k, np.float64)
+    return b - dot(k, b) / dot(k, k) * k
+
+
+def coarse_regularisation(A0, w):
+    """alpha w w^T with alpha = max|diag A0| / max(w)^2: A0 + alpha w w^T is
+    nonsingular for a kernel span{1} (w > 0), and for consistent b its solution
+    is the solution of A0 x = b with w^T x = 0 (reading DESIGN.md Z25)."""
+    alpha = np.max(np.abs(np.diag(A0))) / np.max(w) ** 2
+    return alpha * np.outer(w, w)
+
+
 def vcycle(h: MgHierarchy, l: int, x: np.ndarray, b: np.ndarray) -> np.ndarray:
-    """GMG(l, x_l, b_l) of Alg. `gmg`."""
+    """GMG(l, x_l, b_l) of Alg. `gmg`.  With a global constraint on
+    level l: the restricted right-hand side is made consistent, and the
+    corrections are shifted to zero weighted mean after the coarse solve and
+    after post-smoothing (reading Z25)."""
+    mc = h.mean[l] if h.mean is not None else None
     if l == 0:                                           # Step 0 (P:127)
-        return h.coarse_solve(b)
+        y = h.coarse_solve(consistent(b, mc[1]) if mc is not None else b)
+        return project_zero_mean(y, *mc) if mc is not None else y
     for _ in range(h.nu_pre):                            # Step 1: pre-smooth (P:129)
         x = h.smooth(l, x, b)
     L = h.levels[l]
     d = h.restrict(l, residual(L.n, L.bs, L.rp, L.col, L.val, x, b))   # Step 2 (P:131)
+    if h.mean is not None and h.mean[l - 1] is not None:
+        d = consistent(d, h.mean[l - 1][1])
     y = vcycle(h, l - 1, np.zeros(h.levels[l - 1].n * L.bs), d)         # Step 3 (P:133)
     x = h.prolongate_add(l, x, y)                        # Step 4 (P:135)
     for _ in range(h.nu_post):                           # Step 5: post-smooth (P:137)
         x = h.smooth(l, x, b)
-    return x
+    return project_zero_mean(x, *mc) if mc is not None else x
 
 
 def richardson(h: MgHierarchy, b, x0=None, rtol=1e-10, max_iter=100):
@@ -114,6 +157,8 @@ def richardson(h: MgHierarchy, b, x0=None, rtol=1e-10, max_iter=100):
     Returns x, iterations, residual history."""
     Lf = len(h.levels) - 1
     F = h.levels[-1]
+    if h.mean is not None and h.mean[-1] is not None:
+        b = consistent(b, h.mean[-1][1])                 # solvable pure-Neumann rhs (P:158)
     x = np.zeros(F.n * F.bs) if x0 is None else np.array(x0, np.float64)
     r0 = nrm2(residual(F.n, F.bs, F.rp, F.col, F.val, x, b))
     hist = [r0]
@@ -138,6 +183,9 @@ def gmres(h: MgHierarchy, b, x0=None, rtol=1e-10, restart=30, max_iter=200, prec
     Lf = len(h.levels) - 1
     F = h.levels[-1] if op is None else op
     N = F.n * F.bs
+    mc = h.mean[-1] if h.mean is not None else None
+    if mc is not None:
+        b = consistent(b, mc[1])                         # solvable pure-Neumann rhs
     x = np.zeros(N) if x0 is None else np.array(x0, np.float64)
     r = residual(F.n, F.bs, F.rp, F.col, F.val, x, b)
     beta0 = nrm2(r)
@@ -194,6 +242,8 @@ def gmres(h: MgHierarchy, b, x0=None, rtol=1e-10, restart=30, max_iter=200, prec
         beta = nrm2(r)
         if done or beta <= rtol * beta0:
             break
+    if mc is not None:
+        x = project_zero_mean(x, *mc)                    # the normalised solution int p = 0
     return x, its, hist, beta / beta0
 
 

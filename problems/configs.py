@@ -31,6 +31,8 @@ class LevelData:
     P: tuple | None = None       # (rp, col, w) prolongation from level-1, n x n_{l-1}
     wpe: int = 1                 # weights per P entry (1 or bs)
     keys: np.ndarray | None = None  # (n,) sorted Morton keys at the finest lattice level (partitioning)
+    mean_w: np.ndarray | None = None  # (n,) pure Neumann: lumped-mass weights H^T m of int p = 0
+    mean_k: np.ndarray | None = None  # (n,) pure Neumann: kernel vector (1 free, 0 hanging)
     mesh: M.Mesh | None = None
     nodes: M.NodeSet | None = None
 
@@ -112,7 +114,10 @@ def apply_HT(H, v: np.ndarray) -> np.ndarray:
 
 
 def make_problem(name, root, box, steps, op: F.Operator, *, seed_index=0, omega=0.8,
-                 nu=(2, 2), f=None, g_fun=None, keep_geometry=True) -> Problem:
+                 nu=(2, 2), f=None, g_fun=None, keep_geometry=True, neumann=False) -> Problem:
+    """neumann: no Dirichlet boundary (the pressure Poisson problem of the
+    projection step); every level then carries the kernel vector
+    and lumped-mass weights of the constraint int p = 0."""
     fine_mesh = build_mesh(root, steps)
     meshes = M.hierarchy(fine_mesh)
     R = fine_mesh.max_level
@@ -125,12 +130,17 @@ def make_problem(name, root, box, steps, op: F.Operator, *, seed_index=0, omega=
         H = F.hanging_matrix(nodes)
         n = len(nodes.keys)
         bnd = M.boundary_nodes(lm, nodes)
-        cmask = np.repeat((nodes.hanging | bnd)[:, None], bs, axis=1)
+        cmask = np.repeat(((nodes.hanging | bnd) if not neumann else nodes.hanging)[:, None], bs, axis=1)
         if vel_only:
             cmask[:, 0] = nodes.hanging
         rp, col, val = F.assemble(lm, nodes, op, box, H)
         lvl = LevelData(n, bs, rp, col, val, cmask, H, keys=nodes.keys, mesh=lm if keep_geometry else None,
                         nodes=nodes if keep_geometry else None)
+        if neumann:
+            lvl.mean_k = (~nodes.hanging).astype(np.float64)
+            m = apply_HT(H, load_vector(lm, nodes, box, lambda xp: np.ones(len(xp)), 1))[:, 0]
+            lvl.mean_w = np.where(nodes.hanging, 0.0, m)
+            bnd = np.zeros_like(bnd)
         lvl._bnd = bnd
         lvl._nodes = nodes
         lvl._mesh = lm
@@ -243,9 +253,25 @@ CONFIGS.update({
                F.Operator("stokes", 4, False, STOKES3), 0.6, 4),
 })
 
+# Pure-Neumann pressure Poisson of the projection step (Alg. 2 Step 2, P:618-636;
+# Table `ns` pres-solve) on the NS cavity domain (0,1)x(0,1)x(0,2), root
+# (4,4,8): "pres" = 3 uniform steps = 70,785 nodes (the paper's 32x32x64 mesh,
+# P:706), "pres_l5" = 5 steps = 4,293,249 nodes (bench size), "pres_mid" adds
+# hanging nodes (band refinement), "pres_small" for parity.
+NEUMANN = {"pres", "pres_small", "pres_mid", "pres_l5"}
+CONFIGS.update({
+    "pres": ((4, 4, 8), (1.0, 1.0, 2.0), [("uniform",)] * 3, F.Operator("poisson", 1, True), 0.8, 6),
+    "pres_l5": ((4, 4, 8), (1.0, 1.0, 2.0), [("uniform",)] * 5, F.Operator("poisson", 1, True), 0.8, 6),
+    "pres_small": ((2, 2, 4), (1.0, 1.0, 2.0), [("uniform",)] * 2, F.Operator("poisson", 1, True), 0.8, 6),
+    "pres_mid": ((2, 2, 4), (1.0, 1.0, 2.0), [("band", [2], 1)] * 2 + [("uniform",)],
+                 F.Operator("poisson", 1, True), 0.8, 6),
+})
+
 
 def build(name: str, **kw) -> Problem:
     root, box, steps, op, omega, si = CONFIGS[name]
     if op.name == "stokes" and "g_fun" not in kw:
         kw["g_fun"] = lid(len(root), op.bs)
+    if name in NEUMANN:
+        kw.setdefault("neumann", True)
     return make_problem(name, root, box, steps, op, seed_index=si, omega=omega, **kw)
