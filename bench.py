@@ -45,6 +45,9 @@ WORKLOADS = {
           "GMRES(30)+V(2,2) block-Jacobi omega=0.5, direct coarse solve",
     "c5": "C5: 3D NS-shaped generalised Stokes (PSPG, eps M_p), Q1 4x4 blocks (p,u,v,w), (0,1)^2x(0,2) cavity, "
           "128x128x256 cells, 6 levels, per-component transfers, GMRES(30)+V(2,2) omega=0.6",
+    "pres": "N2: pure-Neumann pressure Poisson of the projection step (Alg. 2 Step 2, P:618-636) on the NS cavity "
+            "(0,1)^2x(0,2), Q1, 128x128x256 cells (4,293,249 DOFs), 6 levels, int p = 0 imposed on every level "
+            "(P:158), GMRES(30)+V(2,2) Jacobi omega=0.8, regularised direct coarse solve",
 }
 
 
@@ -142,7 +145,7 @@ def vcycle_bytes(infos, bs, nu=(2, 2), zero=True, coarse_direct=True, vb=8):
 def build_problem(name):
     from problems import configs
     t = time.time()
-    P = configs.build({"e6": "e6_face_l5"}.get(name, name), keep_geometry=False)
+    P = configs.build({"e6": "e6_face_l5", "pres": "pres_l5"}.get(name, name), keep_geometry=False)
     log(f"[bench] generated {name}: {P.n_dof} DOFs, levels {[l.n for l in P.levels]} in {time.time() - t:.1f}s")
     return P
 
@@ -173,7 +176,8 @@ def oracle_vcycle_rate(P, n_cycles=1, warmup=0, threads=None):
             times.append(time.perf_counter() - t)
         return times, cores
     t = time.time()
-    h = oracle.MgHierarchy.from_arrays(P.levels, omega=P.omega, nu_pre=P.nu_pre, nu_post=P.nu_post)
+    mean = [(L.mean_w, L.mean_k) for L in P.levels] if P.fine.mean_w is not None else None
+    h = oracle.MgHierarchy.from_arrays(P.levels, omega=P.omega, nu_pre=P.nu_pre, nu_post=P.nu_post, mean=mean)
     _ORACLE_H[id(P)] = h
     log(f"[bench] oracle setup {time.time() - t:.1f}s on {cores} cores")
     L = len(P.levels) - 1

@@ -215,6 +215,31 @@ mg_status mg_set_smoother(mg_ctx ctx, int level, double omega, int nu_pre, int n
 mg_status mg_set_constraints(mg_ctx ctx, const int64_t *H_row_ptr, const int64_t *H_col,
                              const double *H_w, int64_t nnz, int mem);
 
+/* Global constraint w^T x = 0 on level `level` of a singular operator with
+ * kernel span{k}: the normalisation int_Omega p = 0 "on each grid level" of
+ * pure-Neumann problems (SPEC project_zero_mean S:452-460, S:474;
+ * reading Z25).  w, k: [n_rows * bs] level-local rows (host or device per
+ * `mem`, copied); w = lumped-mass weights (0 at identity rows), k = the kernel
+ * vector (1 at free DOFs, 0 at identity rows).  Collective on distributed
+ * levels; requires w^T k > 0 and k^T k > 0 (checked at setup, over all ranks).
+ * Effect on the V-cycle: restricted right-hand sides become consistent,
+ * d -= (k^T d / k^T k) k; after the coarse solve and after each level's
+ * post-smoothing, x -= (w^T x / w^T k) k.  A direct coarse solve inverts
+ * A_0 + alpha w w^T with alpha = max_i |(A_0)_ii| / max(w)^2 (nonsingular;
+ * for consistent d its solution solves A_0 y = d with w^T y = 0).  mg_solve
+ * makes b consistent (internal copy; b is not modified) and returns x with
+ * w^T x = 0.  mg_vcycle / mg_vcycle_zero expect a consistent b.  w == NULL
+ * removes the constraint.  MG_ERR_NONFINITE on non-finite entries. */
+mg_status mg_set_mean_constraint(mg_ctx ctx, int level, const double *w, const double *k, int mem);
+
+/* x <- x - (w^T x / w^T k) k on level `level` (zero weighted mean, SPEC
+ * project_zero_mean S:452-460).  Async; MG_ERR_STATE without a constraint. */
+mg_status mg_project_zero_mean(mg_ctx ctx, int level, double *x);
+
+/* b <- b - (k^T b / k^T k) k on level `level` (the consistent right-hand side
+ * of the singular system).  Async; MG_ERR_STATE without a constraint. */
+mg_status mg_make_consistent(mg_ctx ctx, int level, double *b);
+
 /* Finalise setup (R, D^-1, coarse inverse, work vectors).  Optional: the
  * first compute call finalises implicitly. */
 mg_status mg_setup(mg_ctx ctx);

@@ -79,6 +79,9 @@ _SIGS = {
     "mg_set_transfer": [_P, _I, _P, _P, _P, _I64, _I, _I],
     "mg_set_smoother": [_P, _I, _D, _I, _I, _P, _I],
     "mg_set_constraints": [_P, _P, _P, _P, _I64, _I],
+    "mg_set_mean_constraint": [_P, _I, _P, _P, _I],
+    "mg_project_zero_mean": [_P, _I, _P],
+    "mg_make_consistent": [_P, _I, _P],
     "mg_setup": [_P],
     "mg_destroy": [_P],
     "mg_vcycle": [_P, _P, _P],
@@ -227,6 +230,25 @@ def mg_set_constraints(ctx, row_ptr, col, w):
     mem = _same_mem(row_ptr, col, w)
     _check(_lib.mg_set_constraints(ctx, _ptr(row_ptr, np.int64)[0], _ptr(col, np.int64)[0],
                                    _ptr(w, np.float64)[0], int(col.shape[0]), mem), "mg_set_constraints")
+
+
+def mg_set_mean_constraint(ctx, level, w, k):
+    """Global constraint w^T x = 0 of a singular level operator with kernel
+    span{k} (int p = 0 on every level); w=None removes it."""
+    if w is None:
+        _check(_lib.mg_set_mean_constraint(ctx, level, None, None, MG_MEM_HOST), "mg_set_mean_constraint")
+        return
+    mem = _same_mem(w, k)
+    _check(_lib.mg_set_mean_constraint(ctx, level, _ptr(w, np.float64)[0], _ptr(k, np.float64)[0], mem),
+           "mg_set_mean_constraint")
+
+
+def mg_project_zero_mean(ctx, level, x):
+    _check(_lib.mg_project_zero_mean(ctx, level, _dptr(x)), "mg_project_zero_mean")
+
+
+def mg_make_consistent(ctx, level, b):
+    _check(_lib.mg_make_consistent(ctx, level, _dptr(b)), "mg_make_consistent")
 
 
 def mg_setup(ctx):

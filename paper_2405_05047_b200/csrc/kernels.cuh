@@ -853,4 +853,39 @@ __global__ void k_nonfinite(int64_t n, const double *__restrict__ a, int *flag) 
     if (!isfinite(a[i])) *flag = 1;
 }
 
+// ---------------------------------------------------------------------------
+// Global constraint w^T x = 0 on a level (int p = 0): the projections
+// x -= (a^T x / denom) k with the dot a^T x already reduced into *s.
+// ---------------------------------------------------------------------------
+__global__ void k_sub_mean(int64_t n, double *__restrict__ x, const double *__restrict__ k,
+                           const double *__restrict__ s, double denom) {
+  const double coef = *s / denom;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    x[i] = x[i] - coef * k[i];
+}
+
+// Coarse regularisation A_0 + alpha w w^T, alpha = max_i |a_ii| / w_max^2 (reading
+// Z25): one block finds the largest diagonal magnitude, then the rank-1 update.
+__global__ void k_diag_absmax(int64_t N, int64_t ld, const double *__restrict__ a, double *out) {
+  __shared__ double sh[1024];
+  double m = 0.0;
+  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) m = fmax(m, fabs(a[i * ld + i]));
+  sh[threadIdx.x] = m;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + st]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+__global__ void k_rank1_reg(int64_t N, int64_t ld, double *__restrict__ a, const double *__restrict__ w,
+                            const double *__restrict__ dmax, double wmax) {
+  const double alpha = *dmax / (wmax * wmax);
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < N * N; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = t / N, j = t % N;
+    a[i * ld + j] = a[i * ld + j] + alpha * (w[i] * w[j]);
+  }
+}
+
 }  // namespace mgk

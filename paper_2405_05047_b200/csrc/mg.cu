@@ -226,6 +226,10 @@ struct Level {
   std::vector<int64_t> ag_counts, ag_displs;
   int wpe = 1;
   int64_t nnz_p = 0;
+  // global constraint w^T x = 0: weights, kernel vector, w^T k, k^T k
+  bool mean = false;
+  DevArray<double> mean_w, mean_k;
+  double mean_wk = 0.0, mean_kk = 0.0, mean_wmax = 0.0;
   double omega = 0.0;
   int nu_pre = -1, nu_post = -1;
   DevArray<double> x, b, w;  // correction, restricted rhs, work (ping-pong / residual)
@@ -279,6 +283,7 @@ struct mg_ctx_s {
   int gm_m = 0;
   DevArray<double> gm_V, gm_Z, gm_state;
   DevArray<double> rich_z, rich_r;  // mixed-precision MG iteration (defect correction)
+  DevArray<double> mean_b;          // consistent copy of b (global constraint on the finest level)
   double *gm_host = nullptr;  // pinned
   mgk::GmresDev gm{};
   ~mg_ctx_s() {
@@ -703,6 +708,17 @@ __global__ void k_gj_unswap(int64_t N, int64_t ld, double *a, const int64_t *piv
 // in-place Gauss-Jordan inversion of the dense coarse matrix held in c->cinv
 mg_status coarse_gj(mg_ctx_s *c, int64_t N, int64_t ld);
 
+// A_0 += alpha w w^T when level 0 carries a global constraint (reading Z25)
+mg_status coarse_regularise(mg_ctx_s *c, int64_t N, int64_t ld) {
+  Level &L0 = c->lv[0];
+  if (!L0.mean || N == 0) return MG_OK;
+  if (!c->scal.p) TRY(c->scal.alloc(16));
+  mgk::k_diag_absmax<<<1, 1024, 0, c->stream>>>(N, ld, c->cinv.p, c->scal.p + 9);
+  const unsigned g = unsigned(std::min<int64_t>((N * N + 255) / 256, 16 * c->n_sm));
+  mgk::k_rank1_reg<<<g, 256, 0, c->stream>>>(N, ld, c->cinv.p, L0.mean_w.p, c->scal.p + 9, L0.mean_wmax);
+  return check_launch("coarse regularisation");
+}
+
 mg_status build_coarse_inverse(mg_ctx_s *c) {
   Level &L0 = c->lv[0];
   const int bs = c->bs();
@@ -713,6 +729,7 @@ mg_status build_coarse_inverse(mg_ctx_s *c) {
   std::vector<double> padded(size_t(N) * ld, 0.0);
   for (int64_t r = 0; r < N; ++r) std::memcpy(&padded[r * ld], &dense[r * N], N * sizeof(double));
   TRY(c->cinv.upload(padded.data(), padded.size()));
+  TRY(coarse_regularise(c, N, ld));
   return coarse_gj(c, N, ld);
 }
 
@@ -836,6 +853,8 @@ mg_status build_tail(mg_ctx_s *c) {
   const char *env = std::getenv("MGB200_TAIL");
   const char mode = env && *env ? env[0] : '0';
   if (mode != '1' && mode != 'c') return MG_OK;
+  for (const Level &L : c->lv)
+    if (L.mean) return MG_OK;  // the tail has no projection step
   c->tail_cluster = mode == 'c';
   const int64_t max_slices = env_i64("MGB200_TAIL_SLICES", c->tail_cluster ? 256 : 1024);
   int T = -1;
@@ -1008,13 +1027,27 @@ mg_status finalize(mg_ctx_s *c) {
       if (L.b.n < nv) TRY(L.b.alloc(nv));
     }
   }
-  if (c->cfg.coarse_mode == MG_COARSE_DIRECT && c->cN == 0) TRY(build_coarse_inverse(c));
-  TRY(build_tail(c));
   if (!c->red_part.p) {
     TRY(c->red_part.alloc(4 * c->n_sm + 8));
     TRY(c->ticket.alloc(1));
     CU(cudaMemset(c->ticket.p, 0, sizeof(unsigned)));
-    TRY(c->scal.alloc(16));
+  }
+  if (c->cfg.coarse_mode == MG_COARSE_DIRECT && c->cN == 0) TRY(build_coarse_inverse(c));
+  TRY(build_tail(c));
+  if (!c->scal.p) TRY(c->scal.alloc(16));
+  for (int l = 0; l <= c->L(); ++l) {
+    Level &L = c->lv[l];
+    if (!L.mean) continue;
+    const int64_t n = L.n * bs;
+    TRY(dev_dot(c, L.dist, n, L.mean_w.p, L.mean_k.p, c->scal.p + 10, false));
+    TRY(dev_dot(c, L.dist, n, L.mean_k.p, L.mean_k.p, c->scal.p + 11, false));
+    double h[2];
+    CU(cudaMemcpyAsync(h, c->scal.p + 10, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    if (!(h[0] > 0.0) || !(h[1] > 0.0))
+      return fail(MG_ERR_INVALID_ARG, "level %d: mean constraint needs w^T k > 0 and k^T k > 0", l);
+    L.mean_wk = h[0];
+    L.mean_kk = h[1];
   }
   c->finalized = true;
   return MG_OK;
@@ -1113,6 +1146,19 @@ mg_status smooth(mg_ctx_s *c, int l, double *x, const double *b, int k, bool zer
   return MG_OK;
 }
 
+// Global constraint: x -= (w^T x / w^T k) k, or with consist
+// b -= (k^T b / k^T k) k.  The dot goes to scal[8] (all-reduced if distributed).
+mg_status mean_project(mg_ctx_s *c, int l, double *x, bool consist) {
+  Level &L = c->lv[l];
+  const int64_t n = L.n * c->bs();
+  TRY(dev_dot(c, L.dist, n, consist ? L.mean_k.p : L.mean_w.p, x, c->scal.p + 8, false));
+  if (n == 0) return MG_OK;
+  const unsigned g = unsigned(std::min<int64_t>((n + 255) / 256, 8 * c->n_sm));
+  ++g_tally, mgk::k_sub_mean<<<g, 256, 0, c->stream>>>(n, x, L.mean_k.p, c->scal.p + 8,
+                                                       consist ? L.mean_kk : L.mean_wk);
+  return check_launch("mean projection");
+}
+
 mg_status coarse_solve(mg_ctx_s *c, const double *b, double *x) {
   if (c->cfg.coarse_mode == MG_COARSE_DIRECT) {
     const unsigned g = unsigned((c->cN + mgk::kWarpsPerCta - 1) / mgk::kWarpsPerCta);
@@ -1128,17 +1174,22 @@ mg_status vcycle_rec(mg_ctx_s *c, int l, double *x, const double *b, bool zero) 
   mark(c, l);
   if (l == c->tail_T && c->tail_nops > 0 && zero && x == c->lv[l].x.p && b == c->lv[l].b.p)
     return launch_tail(c);                   // GMG(T, 0, b_T), levels T..0 in one launch
-  if (l == 0) return coarse_solve(c, b, x);  // Step 0; ignores x (Z21)
+  if (l == 0) {                                      // Step 0; ignores x (Z21)
+    TRY(coarse_solve(c, b, x));
+    return c->lv[0].mean ? mean_project(c, 0, x, false) : MG_OK;
+  }
   Level &L = c->lv[l];
   Level &C = c->lv[l - 1];
   TRY(smooth(c, l, x, b, lv_nu_pre(c, L), zero));    // Step 1
   TRY(a_pass_resid(c, l, x, b, L.w.p));              // Step 2: r = b - A x
   TRY(do_restrict(c, l, L.w.p, C.b.p));              //         d = R r
+  if (C.mean) TRY(mean_project(c, l - 1, C.b.p, true));  //   consistent d
   TRY(vcycle_rec(c, l - 1, C.x.p, C.b.p, true));     // Step 3
   c->cur_level = l;
   mark(c, l);
   TRY(do_prolong(c, l, C.x.p, x));                   // Step 4
-  return smooth(c, l, x, b, lv_nu_post(c, L), false);  // Step 5
+  TRY(smooth(c, l, x, b, lv_nu_post(c, L), false));  // Step 5
+  return L.mean ? mean_project(c, l, x, false) : MG_OK;  // int x = 0 on this level
 }
 
 // Capture everything `body` enqueues on the context stream into a graph.
@@ -1792,6 +1843,61 @@ mg_status mg_apply_constraints(mg_ctx c, double *x) {
   return MG_OK;
 }
 
+mg_status mg_set_mean_constraint(mg_ctx c, int level, const double *w, const double *k, int mem) {
+  TRY(check_level(c, level));
+  DeviceGuard dg(c->device);
+  Level &L = c->lv[level];
+  const size_t n = size_t(L.n) * c->bs();
+  if (!w) {
+    L.mean = false;
+    L.mean_w = DevArray<double>();
+    L.mean_k = DevArray<double>();
+  } else {
+    if (n > 0 && !k) return fail(MG_ERR_INVALID_ARG, "k must be given with w");
+    std::vector<double> hw, hk;
+    TRY(fetch(hw, w, n, mem));
+    TRY(fetch(hk, k, n, mem));
+    double wmax = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+      if (!std::isfinite(hw[i]) || !std::isfinite(hk[i])) return fail(MG_ERR_NONFINITE, "non-finite w or k");
+      wmax = std::max(wmax, hw[i]);
+    }
+    if (!hw.empty()) {
+      TRY(L.mean_w.upload(hw.data(), n));
+      TRY(L.mean_k.upload(hk.data(), n));
+    } else {
+      TRY(L.mean_w.alloc(1));
+      TRY(L.mean_k.alloc(1));
+    }
+    if (level == 0 && !L.dist && !(wmax > 0.0)) return fail(MG_ERR_INVALID_ARG, "level 0: max(w) must be > 0");
+    L.mean = true;
+    L.mean_wmax = wmax;
+  }
+  if (level == 0) c->cN = 0;  // the coarse inverse includes alpha w w^T: rebuild
+  c->invalidate();
+  return MG_OK;
+}
+
+mg_status mg_project_zero_mean(mg_ctx c, int level, double *x) {
+  TRY(check_level(c, level));
+  if (c->lv[level].n > 0 && !x) return fail(MG_ERR_INVALID_ARG, "NULL vector");
+  if (!c->lv[level].mean) return fail(MG_ERR_STATE, "level %d has no mean constraint", level);
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  TRY(finalize(c));
+  return mean_project(c, level, x, false);
+}
+
+mg_status mg_make_consistent(mg_ctx c, int level, double *b) {
+  TRY(check_level(c, level));
+  if (c->lv[level].n > 0 && !b) return fail(MG_ERR_INVALID_ARG, "NULL vector");
+  if (!c->lv[level].mean) return fail(MG_ERR_STATE, "level %d has no mean constraint", level);
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  TRY(finalize(c));
+  return mean_project(c, level, b, true);
+}
+
 mg_status mg_update_matrix(mg_ctx c, int level, const double *vals, int mem) {
   TRY(check_level(c, level));
   if (!vals) return fail(MG_ERR_INVALID_ARG, "NULL values");
@@ -1835,6 +1941,7 @@ mg_status mg_update_matrix(mg_ctx c, int level, const double *vals, int mem) {
     mgk::k_dense_scatter<<<gd, 256, 0, c->stream>>>(nnzb, bs, L.ublk_row.p, L.ublk_col.p, dv,
                                                     c->cfg.precision == MG_PREC_MIXED ? 1 : 0, c->cld, c->cinv.p);
     TRY(check_launch("dense scatter"));
+    TRY(coarse_regularise(c, c->cN, c->cld));
     TRY(coarse_gj(c, c->cN, c->cld));
   }
   // graphs hold pointers only: they stay valid
@@ -1928,6 +2035,12 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
   if (!c->gm_host) CU(cudaMallocHost(&c->gm_host, 16 * sizeof(double)));
   double *hst = c->gm_host;
 
+  if (F.mean) {  // solvable right-hand side of the singular system: b - (k^T b / k^T k) k
+    if (c->mean_b.n < size_t(std::max<int64_t>(N, 1))) TRY(c->mean_b.alloc(size_t(std::max<int64_t>(N, 1))));
+    if (N) CU(cudaMemcpyAsync(c->mean_b.p, b, size_t(N) * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    TRY(mean_project(c, Lf, c->mean_b.p, true));
+    b = c->mean_b.p;
+  }
   const bool mixed = F.part[0].A64.set;
   if (opts->method == MG_RICHARDSON) {
     // mixed precision: defect correction x += GMG(L, 0, r), r = b - A x in fp64,
@@ -2040,6 +2153,10 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
     }
   } else {
     return fail(MG_ERR_INVALID_ARG, "unknown method %d", opts->method);
+  }
+  if (F.mean) {  // the normalised solution w^T x = 0
+    TRY(mean_project(c, Lf, x, false));
+    CU(cudaStreamSynchronize(c->stream));
   }
   if (info) {
     info->iterations = its;

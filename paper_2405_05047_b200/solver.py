@@ -3,7 +3,7 @@ operation is a call into libmgb200.so)."""
 from __future__ import annotations
 
 from . import (MG_COARSE_DIRECT, MG_GMRES, mg_apply_constraints, mg_create, mg_create_level, mg_destroy,
-               mg_set_constraints, mg_set_matrix, mg_set_smoother, mg_set_transfer, mg_setup, mg_solve,
+               mg_set_constraints, mg_set_matrix, mg_set_mean_constraint, mg_set_smoother, mg_set_transfer, mg_setup, mg_solve,
                mg_vcycle, mg_vcycle_zero)
 
 
@@ -11,7 +11,9 @@ class Multigrid:
     """levels: coarse -> fine sequence of objects with attributes
     n, row_ptr, col, val (BSR, val shaped (nnzb, bs, bs) or flat), and for
     l >= 1 P = (row_ptr, col, w) (n_l x n_{l-1}) and wpe.  H (optional):
-    (row_ptr, col, w) hanging matrix of the finest level.
+    (row_ptr, col, w) hanging matrix of the finest level.  Levels with
+    attributes mean_w / mean_k (not None) carry the global constraint
+    w^T x = 0 of a pure-Neumann operator.
     Multi-GPU: comm = (nranks, rank, id_bytes, transport) and levels carrying
     n_global, row_begin, row_end (this rank's rows; columns global), e.g. from
     problems.partition."""
@@ -37,6 +39,8 @@ class Multigrid:
                     mg_set_transfer(self.ctx, l, rp, col, w, getattr(L, "wpe", 1))
                 if omegas is not None:
                     mg_set_smoother(self.ctx, l, omegas[l])
+                if getattr(L, "mean_w", None) is not None:
+                    mg_set_mean_constraint(self.ctx, l, L.mean_w, L.mean_k)
             if H is not None:
                 mg_set_constraints(self.ctx, *H)
             mg_setup(self.ctx)

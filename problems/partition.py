@@ -32,6 +32,8 @@ class RankLevel:
     val: np.ndarray
     P: tuple | None = None
     wpe: int = 1
+    mean_w: np.ndarray | None = None   # owned rows of the level's constraint weights (pure Neumann)
+    mean_k: np.ndarray | None = None
 
     @property
     def replicated(self) -> bool:
@@ -93,6 +95,9 @@ def partition(problem, nranks, min_rows_per_rank=64, replicate_level0=True, only
                 RL.P = (np.ascontiguousarray(prp[r0:r1 + 1] - prp[r0]), np.ascontiguousarray(pcol[a:b]),
                         np.ascontiguousarray(pw[a * wpe:b * wpe]))
                 RL.wpe = wpe
+            if getattr(L, "mean_w", None) is not None:
+                RL.mean_w = np.ascontiguousarray(L.mean_w.reshape(-1, bs)[r0:r1].reshape(-1))
+                RL.mean_k = np.ascontiguousarray(L.mean_k.reshape(-1, bs)[r0:r1].reshape(-1))
             lv.append(RL)
         f0, f1 = ranges[-1][r]
         b_loc = np.ascontiguousarray(problem.b.reshape(-1, bs)[f0:f1].reshape(-1))
