@@ -5,7 +5,9 @@ Plain, slow, obviously-correct fp64 reference for the hot path of arXiv
 assembled block systems, with the block-Jacobi smoother, transfer
 matrices P and R = P^T, the coarse solve (P:127 / P:341), GMRES
 with modified Gram-Schmidt and Givens rotations and hanging-node
-interpolation x <- H x.
+interpolation x <- H x; the global constraint int p = 0 on every
+level; the explicit pressure-correction Navier-Stokes step of Alg. 2
+(P:618-636) in oracle/ns.py.
 
 Who may use it: only tests/, __graft_entry__.smoke() and bench.py's
 cpu_baseline / `--impl reference` leg.  The product (paper_2405_05047_b200)
