@@ -110,6 +110,10 @@ int mgi_assemble_routed_rows(int64_t m, const int64_t *J, const int64_t *i, cons
 typedef struct mg_ctx_s *mgi_ctx;
 int64_t mgi_launch_count(mgi_ctx ctx);
 
+/* The context's CUDA stream (as void*), device, level count and finest-level
+ * row count (libns: the NS step runs on the pressure solver's stream). */
+int mgi_stream_info(mgi_ctx ctx, void **stream, int *device, int *n_levels, int64_t *n_fine);
+
 /* One V-cycle (eager, not graph-launched) with CUDA events between its
  * phases: out[l] = ms spent on level l's kernels (both legs; level 0 = the
  * coarse solve), out[n_levels + l] = ms in level l's halo exchanges,

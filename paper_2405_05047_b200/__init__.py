@@ -113,7 +113,34 @@ _lib.mgi_vcycle_profile.argtypes = [_P, _P, _P, _I, _P, _I]
 _lib.mgi_level_info.restype = ctypes.c_int
 _lib.mgi_level_info.argtypes = [_P, _I] + [ctypes.POINTER(ctypes.c_int64)] * 6
 
-EXPORTED = sorted(list(_SIGS) + ["mg_last_error", "mg_version"])
+# --- Navier-Stokes step (include/ns.h) ---
+class ns_step_info(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int), ("rel_residual", ctypes.c_double), ("converged", ctypes.c_int),
+                ("ms", ctypes.c_double * 4)]
+
+
+_NS_SIGS = {
+    "ns_create": [ctypes.POINTER(_P), _P, _I64, _I64],
+    "ns_destroy": [_P],
+    "ns_set_momentum": [_P, _P, _P, _P, _I64, _I],
+    "ns_set_coupling": [_P, _P, _P, _P, _I64, _P, _P, _P, _I64, _I],
+    "ns_set_mass": [_P, _P, _P, _I],
+    "ns_set_dirichlet": [_P, _P, _P, _I64, _I],
+    "ns_set_force": [_P, _P, _I],
+    "ns_set_params": [_P, _D, _D, _D, _I, _I, _I],
+    "ns_set_state": [_P, _P, _P, _P, _I],
+    "ns_get_state": [_P, _P, _P, _P, _I],
+    "ns_step": [_P, ctypes.POINTER(ns_step_info)],
+    "ns_momentum": [_P, _P, _I],
+    "ns_get_divergence": [_P, _P, _I],
+}
+for _name, _args in _NS_SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+_lib.ns_launch_count.restype = ctypes.c_int64
+_lib.ns_launch_count.argtypes = [_P]
+
+EXPORTED = sorted(list(_SIGS) + list(_NS_SIGS) + ["mg_last_error", "mg_version", "ns_launch_count"])
 
 
 def lib():
@@ -339,3 +366,89 @@ def level_info(ctx, level) -> dict:
 
 
 from .solver import Multigrid  # noqa: E402,F401
+
+
+# ----------------------------------------------------------------------------
+# Navier-Stokes step (include/ns.h): same names, argument marshalling only
+# ----------------------------------------------------------------------------
+
+def ns_create(pressure_ctx, n_u, n_p):
+    h = _P()
+    _check(_lib.ns_create(ctypes.byref(h), pressure_ctx, int(n_u), int(n_p)), "ns_create")
+    return h
+
+
+def ns_destroy(ctx):
+    _check(_lib.ns_destroy(ctx), "ns_destroy")
+
+
+def ns_set_momentum(ctx, row_ptr, col, vals):
+    mem = _same_mem(row_ptr, col, vals)
+    _check(_lib.ns_set_momentum(ctx, _ptr(row_ptr, np.int64)[0], _ptr(col, np.int64)[0], _ptr(vals, np.float64)[0],
+                                int(col.shape[0]), mem), "ns_set_momentum")
+
+
+def ns_set_coupling(ctx, pi, g):
+    prp, pcol, pw = pi
+    grp, gcol, gv = g
+    mem = _same_mem(prp, pcol, pw, grp, gcol, gv)
+    _check(_lib.ns_set_coupling(ctx, _ptr(prp, np.int64)[0], _ptr(pcol, np.int64)[0], _ptr(pw, np.float64)[0],
+                                int(pcol.shape[0]), _ptr(grp, np.int64)[0], _ptr(gcol, np.int64)[0],
+                                _ptr(gv, np.float64)[0], int(gcol.shape[0]), mem), "ns_set_coupling")
+
+
+def ns_set_mass(ctx, m_u, m_p):
+    mem = _same_mem(m_u, m_p)
+    _check(_lib.ns_set_mass(ctx, _ptr(m_u, np.float64)[0], _ptr(m_p, np.float64)[0], mem), "ns_set_mass")
+
+
+def ns_set_dirichlet(ctx, rows, vals):
+    mem = _same_mem(rows, vals)
+    _check(_lib.ns_set_dirichlet(ctx, _ptr(rows, np.int64)[0], _ptr(vals, np.float64)[0], int(rows.shape[0]), mem),
+           "ns_set_dirichlet")
+
+
+def ns_set_force(ctx, F):
+    p, mem = _ptr(F, np.float64)
+    _check(_lib.ns_set_force(ctx, p, mem), "ns_set_force")
+
+
+def ns_set_params(ctx, nu, dt, rtol=1e-6, restart=30, max_iter=200, timing=False):
+    _check(_lib.ns_set_params(ctx, float(nu), float(dt), float(rtol), int(restart), int(max_iter), int(bool(timing))),
+           "ns_set_params")
+
+
+def ns_set_state(ctx, u, p, q):
+    mem = _same_mem(u, p, q)
+    _check(_lib.ns_set_state(ctx, _ptr(u, np.float64)[0], _ptr(p, np.float64)[0], _ptr(q, np.float64)[0], mem),
+           "ns_set_state")
+
+
+def ns_get_state(ctx, u, p, q):
+    """Fill u [n_u*3], p, q [n_p] (numpy arrays or CUDA tensors, same memory)."""
+    mem = _same_mem(u, p, q)
+    _check(_lib.ns_get_state(ctx, _ptr(u, np.float64)[0], _ptr(p, np.float64)[0], _ptr(q, np.float64)[0], mem),
+           "ns_get_state")
+
+
+def ns_step(ctx):
+    """One time step; returns (status, iterations, rel_residual, converged, ms[4])."""
+    info = ns_step_info()
+    st = _lib.ns_step(ctx, ctypes.byref(info))
+    _check(st, "ns_step", ok=(MG_OK, MG_NOT_CONVERGED))
+    return st, info.iterations, info.rel_residual, bool(info.converged), list(info.ms)
+
+
+def ns_momentum(ctx, u_new):
+    p, mem = _ptr(u_new, np.float64)
+    _check(_lib.ns_momentum(ctx, p, mem), "ns_momentum")
+
+
+def ns_get_divergence(ctx, d):
+    p, mem = _ptr(d, np.float64)
+    _check(_lib.ns_get_divergence(ctx, p, mem), "ns_get_divergence")
+
+
+def ns_launch_count(ctx) -> int:
+    return int(_lib.ns_launch_count(ctx))
+from .navier_stokes import NavierStokes  # noqa: E402,F401

@@ -22,14 +22,15 @@
 #include "../../include/mg.h"
 #include "../../include/mg_internal.h"
 #include "comm.h"
+#include "common.h"
 #include "kernels.cuh"
 
 #define MGB200_VERSION "mgb200 0.2 (sm_100a, fp64, SELL-32-sigma, multi-GPU halo)"
 
-namespace {
+namespace mgb {
 
 thread_local std::string g_err;
-thread_local int64_t g_tally = 0;  // kernel launches issued by this thread (bench accounting)
+thread_local int64_t g_tally = 0;
 
 mg_status vfail(mg_status st, const char *fmt, va_list ap) {
   char buf[512];
@@ -46,7 +47,9 @@ mg_status fail(mg_status st, const char *fmt, ...) {
   return st;
 }
 
-}  // namespace
+}  // namespace mgb
+
+using namespace mgb;
 
 namespace mgc {
 mg_status comm_fail(mg_status st, const char *fmt, ...) {
@@ -59,59 +62,6 @@ mg_status comm_fail(mg_status st, const char *fmt, ...) {
 }  // namespace mgc
 
 namespace {
-
-#define CU(x)                                                                                \
-  do {                                                                                       \
-    cudaError_t e_ = (x);                                                                    \
-    if (e_ != cudaSuccess) {                                                                 \
-      if (e_ == cudaErrorMemoryAllocation) return fail(MG_ERR_OOM, "%s: out of memory", #x); \
-      return fail(MG_ERR_CUDA, "%s: %s", #x, cudaGetErrorString(e_));                        \
-    }                                                                                        \
-  } while (0)
-#define TRY(x)                  \
-  do {                          \
-    mg_status s_ = (x);         \
-    if (s_ != MG_OK) return s_; \
-  } while (0)
-
-constexpr int kSigma = 4096;                       // sorting window of SELL-32-sigma
-constexpr size_t kStreamBytes = size_t(32) << 20;  // operators larger than this use evict-first loads
-
-template <class T>
-struct DevArray {
-  T *p = nullptr;
-  size_t n = 0;
-  DevArray() = default;
-  DevArray(const DevArray &) = delete;
-  DevArray &operator=(const DevArray &) = delete;
-  DevArray(DevArray &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
-  DevArray &operator=(DevArray &&o) noexcept {
-    if (this != &o) {
-      release();
-      p = o.p, n = o.n;
-      o.p = nullptr, o.n = 0;
-    }
-    return *this;
-  }
-  ~DevArray() { release(); }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-  }
-  mg_status alloc(size_t count) {
-    release();
-    if (count == 0) count = 1;
-    CU(cudaMalloc(&p, count * sizeof(T)));
-    n = count;
-    return MG_OK;
-  }
-  mg_status upload(const T *h, size_t count) {
-    TRY(alloc(count));
-    if (h && count) CU(cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice));
-    return MG_OK;
-  }
-};
 
 struct SellOp {
   DevArray<int64_t> slice_ptr;
@@ -1974,6 +1924,15 @@ mg_status mg_dot(mg_ctx c, int level, const double *a, const double *b, double *
 }
 
 int64_t mgi_launch_count(mgi_ctx c) { return c ? c->launches : -1; }
+
+int mgi_stream_info(mgi_ctx c, void **stream, int *device, int *n_levels, int64_t *n_fine) {
+  if (!c) return MG_ERR_INVALID_ARG;
+  if (stream) *stream = c->stream;
+  if (device) *device = c->device;
+  if (n_levels) *n_levels = c->cfg.n_levels;
+  if (n_fine) *n_fine = c->lv.empty() ? 0 : c->lv[c->L()].n * c->bs();
+  return MG_OK;
+}
 
 int mgi_vcycle_profile(mgi_ctx c, double *x, const double *b, int zero, double *out, int n_out) {
   if (!c || !x || !b || !out) return MG_ERR_INVALID_ARG;

@@ -14,7 +14,7 @@ from mgtest_util import ROOT, problem
 
 import oracle
 
-HDRS = [os.path.join(ROOT, "include", h) for h in ("mg.h", "mg_internal.h")]
+HDRS = [os.path.join(ROOT, "include", h) for h in ("mg.h", "mg_internal.h", "ns.h")]
 
 
 def _lib():
@@ -31,7 +31,7 @@ def declared_symbols():
     for h in HDRS:
         txt = open(h).read()
         txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-        for m in re.finditer(r"\b(mgi?_[a-z0-9_]+)\s*\(", txt):
+        for m in re.finditer(r"\b((?:mgi?|ns)_[a-z0-9_]+)\s*\(", txt):
             names.add(m.group(1))
     return sorted(names)
 
@@ -39,12 +39,12 @@ def declared_symbols():
 def test_library_exports_every_declared_symbol():
     import paper_2405_05047_b200 as m
     names = declared_symbols()
-    assert "mg_vcycle" in names and "mg_solve" in names and "mgi_sell_fill" in names
+    assert "mg_vcycle" in names and "mg_solve" in names and "mgi_sell_fill" in names and "ns_step" in names
     L = m.lib()
     for n in names:
         assert hasattr(L, n), f"{n} declared in include/ but not exported"
     # the python binding exposes the same names as the C ABI
-    for n in [x for x in names if x.startswith("mg_")]:
+    for n in [x for x in names if x.startswith(("mg_", "ns_"))]:
         assert hasattr(m, n), f"binding lacks {n}"
     assert m.mg_version().startswith("mgb200")
 
