@@ -3,7 +3,8 @@
 Thin ctypes binding over libmgb200.so (include/mg.h): the same names as the C
 ABI, argument marshalling only.  Every step of the solve runs in the CUDA
 library; there is no CPU fallback -- importing this package fails loudly if
-the extension has not been built (``python -m paper_2405_05047_b200.build``).
+the extension has not been built (``python paper_2405_05047_b200/build.py`` or
+``python __graft_entry__.py``).
 
 Vectors and arrays may be torch tensors (CUDA -> device pointer, CPU -> host
 pointer) or numpy arrays (host pointer).  Compute calls take CUDA tensors.
@@ -19,7 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmgb200.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2405_05047_b200.build` "
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_2405_05047_b200/build.py` "
                       "(there is no CPU fallback)")
 
 _lib = ctypes.CDLL(LIB_PATH)
