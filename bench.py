@@ -43,6 +43,13 @@ WORKLOADS = {
     "e6": "N4: the paper's 6-component elasticity system (u, v), backward Euler (P:441-445), 6x6 blocks, "
           "Table ndofs face mesh L5 (8^3 root, K=1 band toward x=0): 1,035,030 DOFs as in P:537, "
           "GMRES(30)+V(2,2) block-Jacobi omega=0.5, direct coarse solve",
+    "c4ns": "C4 (SURVEY §8(d)): 2D instationary Navier-Stokes flow around a cylinder (DFG 2D-2 channel, "
+            "Re 100, disk as Dirichlet obstacle), equal-order Q1 (PSPG + streamline diffusion), 3x3 blocks, "
+            "quadtree band-refined toward the cylinder (44x8 root, 2 uniform + 6 band steps), 9 levels, backward "
+            "Euler dt=0.01, Newton (CPU-assembled Jacobians re-uploaded every step) + GMRES(30)/V(2,2) omega=0.6",
+    "ns": "N2: the paper's explicit pressure-correction Navier-Stokes step (Alg. 2) on its 3D driven cavity "
+          "(0,1)^2x(0,2), graded 32x32x64 pressure mesh (Q1, 70,785 nodes) and Q1-iso-Q2 velocity (545,025 "
+          "nodes), Re 1000, dt 1e-4, pressure Poisson GMRES+MG with int p = 0 to rtol 1e-6",
     "c5": "C5: 3D NS-shaped generalised Stokes (PSPG, eps M_p), Q1 4x4 blocks (p,u,v,w), (0,1)^2x(0,2) cavity, "
           "128x128x256 cells, 6 levels, per-component transfers, GMRES(30)+V(2,2) omega=0.6",
     "pres": "N2: pure-Neumann pressure Poisson of the projection step (Alg. 2 Step 2, P:618-636) on the NS cavity "
@@ -498,6 +505,211 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def run_newton(args):
+    """C4 as SURVEY §8(d) states it (BASELINE config 4): flow around a cylinder,
+    backward Euler, Newton + GMRES(30)/V(2,2) per time step with every level's
+    Jacobian assembled on the CPU and re-uploaded value-only.  Step =
+    one time step through mg_newton (the public API): `value` = V-cycles/s of
+    the GPU linear solves (device time: CUDA events inside mg_newton), `e2e` =
+    the same V-cycles over the whole time step's wall time including the CPU
+    assembly and the host<->device copies."""
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1 and rank != 0:
+        return          # single-GPU workload: replicas only (DESIGN.md)
+    torch.cuda.set_device(local)
+    import paper_2405_05047_b200 as mg
+    from problems import channel as C
+    t = time.time()
+    P = C.build("c4ns")
+    log(f"[bench] generated c4ns: {P.n_dof} DOFs, levels {[L.data.n for L in P.levels]} in {time.time() - t:.1f}s")
+    stream = torch.cuda.current_stream()
+    u = C.initial_state(P)
+    solver = mg.Multigrid(C.with_values(P, C.jacobians(P, u, u)), 3, omega=P.omega, H=P.fine.H, device=local,
+                          stream=stream)
+    ctx = solver.ctx
+    L = len(P.levels) - 1
+    infos = [mg.level_info(ctx, l) for l in range(L + 1)]
+    x = torch.from_numpy(u.reshape(-1).copy()).cuda()
+
+    def time_step():
+        u_old = x.cpu().numpy().reshape(-1, 3)
+        t0 = time.perf_counter()
+        st, info = solver.newton(x, C.assemble_callback(P, u_old), max_newton=4, ntol=1e-8)
+        if not info["converged"]:
+            raise RuntimeError(f"Newton did not converge: {info}")
+        return time.perf_counter() - t0, info
+
+    for _ in range(args.warmup):
+        time_step()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    l0 = mg.launch_count(ctx)
+    wall, its, newton, upl, sol, asm, lin = 0.0, 0, 0, 0.0, 0.0, 0.0, []
+    for _ in range(args.steps):
+        w_s, info = time_step()
+        wall += w_s
+        its += info["gmres_its"]
+        newton += info["newton_its"]
+        upl += info["ms_upload"]
+        sol += info["ms_solve"]
+        asm += info["ms_assemble"]
+        lin.append(info["lin_its"])
+    launches = mg.launch_count(ctx) - l0
+    clocks = sampler.stop()
+    value = its / (sol / 1e3)
+    # dominant kernel: fine-level fused sweep of the current Jacobian
+    peak, peak_src = measured_peaks()
+    N = P.n_dof
+    xin = torch.randn(N, dtype=torch.float64, device="cuda")
+    bb = torch.randn(N, dtype=torch.float64, device="cuda")
+    xout = torch.empty_like(xin)
+    for _ in range(3):
+        mg.mg_sweep(ctx, L, xin, bb, xout)
+    ns = 20
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ns)]
+    torch.cuda.synchronize()
+    for a, c_ in evs:
+        a.record(stream)
+        mg.mg_sweep(ctx, L, xin, bb, xout)
+        c_.record(stream)
+    torch.cuda.synchronize()
+    sw_ms = sum(a.elapsed_time(c_) for a, c_ in evs) / ns
+    sweep_b, _, _ = level_bytes(infos[L], 3, False)
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle
+        cores = cpu_cores()
+        oracle.set_threads(cores)
+        h = oracle.MgHierarchy.from_arrays(C.with_values(P, C.jacobians(P, u, u)), omega=P.omega)
+        bh = np.random.default_rng(0).standard_normal(N)
+        t = time.perf_counter()
+        oracle.vcycle(h, L, np.zeros(N), bh)
+        dt_o = time.perf_counter() - t
+        cpu = {"value": 1.0 / dt_o, "unit": "V-cycles/s", "cores": cores, "kind": "oracle",
+               "sample": f"one oracle V(2,2) GMG(L,0,b) on the c4ns Jacobian hierarchy ({N} DOFs), {dt_o:.2f} s"}
+    line = {
+        "metric": "V-cycles/s", "value": value, "unit": "V-cycles/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS["c4ns"], "n_dof": N, "levels": L + 1,
+                   "level_rows": [i["n"] for i in infos], "nnzb_fine": infos[L]["nnzb"],
+                   "parallelism": "single GPU", "l2": "finest Jacobian 0.29 GB > L2 126 MB",
+                   "newton_per_step": newton / args.steps, "gmres_per_step": its / args.steps,
+                   "lin_its": lin},
+        "dof_cycles_per_s": value * N,
+        "time_step": {"wall_ms": 1e3 * wall / args.steps, "cpu_assembly_ms": asm / args.steps,
+                      "upload_device_ms": upl / args.steps, "solve_device_ms": sol / args.steps,
+                      "note": "CPU assembly of F and of 9 levels' Jacobians (numpy + C helper, the paper's CPU side)"},
+        "roofline": {"bound": "hbm", "kernel": "k_sell_apply<3,SWEEP> (fused block-Jacobi sweep), finest level",
+                     "achieved": sweep_b / (sw_ms / 1e3) / 1e9, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": sweep_b / (sw_ms / 1e3) / 1e9 / peak, "traffic": None, "alg_bytes_per_launch": sweep_b,
+                     "avg_launch_ms": sw_ms},
+        "cpu_baseline": cpu,
+        "e2e": {"value": its / wall, "unit": "V-cycles/s",
+                "h2d_bytes_per_step": int(newton / args.steps * (8 * N + sum(8 * 9 * i["nnzb"] for i in infos))),
+                "d2h_bytes_per_step": int((newton / args.steps + 1) * 8 * N)},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    solver.close()
+
+
+def run_ns(args):
+    """The paper's explicit pressure-correction NS step (Alg. 2; SURVEY
+    N2) on its 3D cavity (32x32x64 graded pressure mesh = 70,785 nodes,
+    velocity on the midpoint refinement = 545,025 nodes), from rest.  Step = one
+    ns_step (momentum kernel, divergence, pressure GMRES+MG with int q = 0,
+    pressure update).  value = time steps/s; the line carries the Table `ns`
+    split per step for context (the paper: H100 PCIe, its GPU column
+    sums to 1660 s over "40 000" steps = 41.5 ms per step; reading Z19)."""
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1 and rank != 0:
+        return
+    torch.cuda.set_device(local)
+    import paper_2405_05047_b200 as mg
+    from problems import ns as NSP
+    t = time.time()
+    P = NSP.build_ns("ns")
+    log(f"[bench] generated ns: n_u {P.n_u}, n_p {P.n_p}, pressure levels {[L.n for L in P.pres_levels]} "
+        f"in {time.time() - t:.1f}s")
+    g = mg.NavierStokes(P, rtol=1e-6, timing=True)
+    u, p, q = NSP.initial_state(P)
+    g.set_state(u, p, q)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        g.step()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    l0 = mg.ns_launch_count(g.ctx)   # includes the pressure solve (thread-local tally)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    comp = np.zeros(4)
+    its = 0
+    for _ in range(args.steps):
+        st, it, rel, conv, ms = g.step()
+        comp += np.array(ms)
+        its += it
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_ms = e0.elapsed_time(e1)
+    launches = mg.ns_launch_count(g.ctx) - l0
+    clocks = sampler.stop()
+    # e2e: the state from/to pinned host buffers around every step
+    uh, ph, qh = (np.ascontiguousarray(a) for a in g.get_state())
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        g.set_state(uh, ph, qh)
+        g.step()
+        uh, ph, qh = (np.ascontiguousarray(a) for a in g.get_state())
+    e2e_s = time.perf_counter() - t0
+    value = args.steps / (t_ms / 1e3)
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle
+        from oracle import ns as ons
+        cores = cpu_cores()
+        oracle.set_threads(cores)
+        ops = ons.NsOperators.from_arrays(P.n_u, P.n_p, P.mom_rp, P.mom_col, P.mom_val, P.G, P.m_u, P.m_p,
+                                          P.dir_rows, P.dir_vals, P.nu, P.dt)
+        h = oracle.MgHierarchy.from_arrays(P.pres_levels, omega=P.omega,
+                                           mean=[(L.mean_w, L.mean_k) for L in P.pres_levels])
+        t = time.perf_counter()
+        ons.step(ops, h, uh, ph, qh, rtol=1e-6)
+        dt_o = time.perf_counter() - t
+        cpu = {"value": 1.0 / dt_o, "unit": "time steps/s", "cores": cores, "kind": "oracle",
+               "sample": f"one oracle Alg. 2 step on the paper's cavity, {dt_o:.2f} s"}
+    n = args.steps
+    line = {
+        "metric": "NS time steps/s", "value": value, "unit": "time steps/s", "n_gpus": 1, "steps": n,
+        "warmup": args.warmup, "ms_per_step": t_ms / n, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS["ns"], "n_u": P.n_u, "n_p": P.n_p,
+                   "pressure_levels": [L.n for L in P.pres_levels], "pressure_gmres_per_step": its / n,
+                   "pressure_rtol": 1e-6, "parallelism": "single GPU",
+                   "l2": "per-step operators ~0.6 GB > L2 126 MB"},
+        "table_ns_split_ms_per_step": {"momentum": comp[0] / n, "pres-rhs": comp[1] / n, "pres-solve": comp[2] / n,
+                                       "pres-up": comp[3] / n},
+        "paper_context": {"gpu_ms_per_step_h100": 41.5, "split_ms_per_step_h100": {
+            "momentum": 5.78, "pres-rhs": 1.33, "pres-solve": 32.6, "pres-up": 1.81},
+            "note": "Table ns GPU column / 40 000 steps (P:757-790); other hardware and code: context only"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": n / e2e_s, "unit": "time steps/s", "h2d_bytes_per_step": 8 * (3 * P.n_u + 2 * P.n_p),
+                "d2h_bytes_per_step": 8 * (3 * P.n_u + 2 * P.n_p)},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    g.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -519,6 +731,10 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c4ns":
+        run_newton(args)
+    elif args.config == "ns":
+        run_ns(args)
     else:
         run_ours(args)
 

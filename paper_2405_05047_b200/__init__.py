@@ -98,6 +98,7 @@ _SIGS = {
     "mg_apply_constraints": [_P, _P],
     "mg_condense_rhs": [_P, _P, _P],
     "mg_dot": [_P, _I, _P, _P, ctypes.POINTER(_D)],
+    "mg_axpy": [_P, _I, _D, _P, _P],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -141,7 +142,29 @@ for _name, _args in _NS_SIGS.items():
 _lib.ns_launch_count.restype = ctypes.c_int64
 _lib.ns_launch_count.argtypes = [_P]
 
-EXPORTED = sorted(list(_SIGS) + list(_NS_SIGS) + ["mg_last_error", "mg_version", "ns_launch_count"])
+# --- Newton's method (include/newton.h) ---
+MG_NEWTON_MAX_HIST = 32
+
+
+class mg_newton_opts(ctypes.Structure):
+    _fields_ = [("max_newton", ctypes.c_int), ("ntol", ctypes.c_double), ("atol", ctypes.c_double),
+                ("reuse_rate", ctypes.c_double), ("lin", mg_solve_opts)]
+
+
+class mg_newton_info(ctypes.Structure):
+    _fields_ = [("newton_its", ctypes.c_int), ("gmres_its", ctypes.c_int), ("jacobians", ctypes.c_int),
+                ("converged", ctypes.c_int),
+                ("lin_its", ctypes.c_int * MG_NEWTON_MAX_HIST), ("res_norm", ctypes.c_double * (MG_NEWTON_MAX_HIST + 1)),
+                ("ms_assemble", ctypes.c_double), ("ms_upload", ctypes.c_double), ("ms_solve", ctypes.c_double)]
+
+
+MG_NEWTON_ASSEMBLE_FN = ctypes.CFUNCTYPE(ctypes.c_int, _P, ctypes.POINTER(_D), ctypes.POINTER(_D),
+                                         ctypes.POINTER(ctypes.POINTER(_D)))
+_lib.mg_newton.restype = ctypes.c_int
+_lib.mg_newton.argtypes = [_P, _P, MG_NEWTON_ASSEMBLE_FN, _P, ctypes.POINTER(mg_newton_opts),
+                           ctypes.POINTER(mg_newton_info)]
+
+EXPORTED = sorted(list(_SIGS) + list(_NS_SIGS) + ["mg_last_error", "mg_version", "ns_launch_count", "mg_newton"])
 
 
 def lib():
@@ -344,6 +367,46 @@ def mg_dot(ctx, level, a, b) -> float:
     out = _D()
     _check(_lib.mg_dot(ctx, level, _dptr(a), _dptr(b), ctypes.byref(out)), "mg_dot")
     return out.value
+
+
+def mg_axpy(ctx, level, alpha, x, y):
+    _check(_lib.mg_axpy(ctx, level, alpha, _dptr(x), _dptr(y)), "mg_axpy")
+
+
+def mg_newton(ctx, x, assemble, n_fine_dof, level_sizes, *, max_newton=3, ntol=1e-8, atol=0.0, reuse_rate=0.0,
+              method=MG_GMRES, restart=30, max_iter=200, rtol=1e-10):
+    """Newton's method on the device (include/newton.h).  assemble(w, F, vals)
+    is the caller's CPU assembly: w (n_fine_dof,) read-only view of the current
+    iterate; F (n_fine_dof,) to fill with F(w), or None; vals a list of
+    per-level views (level_sizes[l],) to fill with the Jacobian values, or
+    None.  level_sizes: nnzb_l*bs*bs per level.  Returns (status, info dict)."""
+    err = []
+
+    def cb(_user, w_p, F_p, vals_p):
+        try:
+            w = np.ctypeslib.as_array(w_p, shape=(n_fine_dof,))
+            F = np.ctypeslib.as_array(F_p, shape=(n_fine_dof,)) if bool(F_p) else None
+            vals = None
+            if bool(vals_p):
+                vals = [np.ctypeslib.as_array(vals_p[l], shape=(int(sz),)) for l, sz in enumerate(level_sizes)]
+            assemble(w, F, vals)
+            return MG_OK
+        except Exception as e:  # reported after the call returns
+            err.append(e)
+            return MG_ERR_INVALID_ARG
+
+    fn = MG_NEWTON_ASSEMBLE_FN(cb)
+    o = mg_newton_opts(max_newton, ntol, atol, reuse_rate, mg_solve_opts(method, restart, max_iter, rtol))
+    info = mg_newton_info()
+    st = _lib.mg_newton(ctx, _dptr(x), fn, None, ctypes.byref(o), ctypes.byref(info))
+    if err:
+        raise err[0]
+    _check(st, "mg_newton", ok=(MG_OK, MG_NOT_CONVERGED))
+    k = info.newton_its
+    return st, {"newton_its": k, "gmres_its": info.gmres_its, "jacobians": info.jacobians,
+                "converged": bool(info.converged), "lin_its": list(info.lin_its[:k]),
+                "res_norm": list(info.res_norm[:k + 1]), "ms_assemble": info.ms_assemble,
+                "ms_upload": info.ms_upload, "ms_solve": info.ms_solve}
 
 
 def launch_count(ctx) -> int:

@@ -10,9 +10,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmgb200.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("mg.cu", "ns.cu", "comm.cu", "host.cpp")]
+SOURCES = [os.path.join(CSRC, f) for f in ("mg.cu", "ns.cu", "newton.cu", "comm.cu", "host.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, "kernels.cuh"), os.path.join(CSRC, "comm.h"), os.path.join(CSRC, "common.h"),
-                  os.path.join(ROOT, "include", "mg.h"), os.path.join(ROOT, "include", "ns.h"),
+                  os.path.join(ROOT, "include", "mg.h"), os.path.join(ROOT, "include", "ns.h"), os.path.join(ROOT, "include", "newton.h"),
                   os.path.join(ROOT, "include", "mg_internal.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -842,6 +842,12 @@ __global__ void k_dense_scatter(int64_t nnzb, int bs, const int32_t *__restrict_
 }
 
 // x += z
+// y += alpha x (mg_axpy: the Newton update w + d).
+__global__ void k_axpy(int64_t n, double alpha, const double *__restrict__ x, double *__restrict__ y) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    y[i] = fma(alpha, x[i], y[i]);
+}
+
 __global__ void k_axpy1(int64_t n, const double *__restrict__ z, double *__restrict__ x) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     x[i] += z[i];

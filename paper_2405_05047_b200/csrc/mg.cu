@@ -21,6 +21,7 @@
 
 #include "../../include/mg.h"
 #include "../../include/mg_internal.h"
+#include "../../include/newton.h"
 #include "comm.h"
 #include "common.h"
 #include "kernels.cuh"
@@ -234,6 +235,7 @@ struct mg_ctx_s {
   DevArray<double> gm_V, gm_Z, gm_state;
   DevArray<double> rich_z, rich_r;  // mixed-precision MG iteration (defect correction)
   DevArray<double> mean_b;          // consistent copy of b (global constraint on the finest level)
+  DevArray<double> upd_stage;       // mg_update_matrix: staging buffer for host values (kept across calls)
   double *gm_host = nullptr;  // pinned
   mgk::GmresDev gm{};
   ~mg_ctx_s() {
@@ -1857,11 +1859,15 @@ mg_status mg_update_matrix(mg_ctx c, int level, const double *vals, int mem) {
   DeviceGuard dg(c->device);
   const int bs = c->bs(), V = bs * bs;
   const int64_t nnzb = L.nnzb;
-  DevArray<double> tmp;
   const double *dv = vals;
-  if (mem == MG_MEM_HOST) {
-    TRY(tmp.upload(vals, size_t(std::max<int64_t>(1, nnzb)) * V));
-    dv = tmp.p;
+  if (mem == MG_MEM_HOST) {  // stream-ordered copy into a staging buffer kept by the context
+    const size_t cnt = size_t(std::max<int64_t>(1, nnzb)) * V;
+    if (c->upd_stage.n < cnt) {
+      CU(cudaStreamSynchronize(c->stream));
+      TRY(c->upd_stage.alloc(cnt));
+    }
+    CU(cudaMemcpyAsync(c->upd_stage.p, vals, size_t(nnzb) * V * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    dv = c->upd_stage.p;
   }
   DevArray<int> flag;
   TRY(flag.alloc(1));
@@ -1909,6 +1915,19 @@ mg_status mg_condense_rhs(mg_ctx c, const double *b, double *b_bar) {
   TRY(halo_exchange(c, c->hht_halo, b));
   return launch_transfer(c->bs(), false, c->HT, In{b, c->hht_halo.active ? c->hht_halo.ghost.p : nullptr, int(F.n)},
                          b_bar, c->stream);
+}
+
+mg_status mg_axpy(mg_ctx c, int level, double alpha, const double *x, double *y) {
+  TRY(check_level(c, level));
+  const int64_t N = c->lv[level].n * c->bs();
+  if (N > 0 && (!x || !y)) return fail(MG_ERR_INVALID_ARG, "NULL vector");
+  if (!std::isfinite(alpha)) return fail(MG_ERR_NONFINITE, "non-finite alpha");
+  if (N == 0) return MG_OK;
+  DeviceGuard dg(c->device);
+  Tally tally(c);
+  const unsigned eg = unsigned(std::min<int64_t>(std::max<int64_t>(1, (N + 255) / 256), 8 * c->n_sm));
+  ++g_tally, mgk::k_axpy<<<eg, 256, 0, c->stream>>>(N, alpha, x, y);
+  return check_launch("axpy");
 }
 
 mg_status mg_dot(mg_ctx c, int level, const double *a, const double *b, double *out_host) {

@@ -2,7 +2,8 @@
 operation is a call into libmgb200.so)."""
 from __future__ import annotations
 
-from . import (MG_COARSE_DIRECT, MG_GMRES, mg_apply_constraints, mg_create, mg_create_level, mg_destroy,
+from . import (MG_COARSE_DIRECT, MG_GMRES, level_info, mg_apply_constraints, mg_create, mg_create_level, mg_destroy,
+               mg_newton,
                mg_set_constraints, mg_set_matrix, mg_set_mean_constraint, mg_set_smoother, mg_set_transfer, mg_setup, mg_solve,
                mg_vcycle, mg_vcycle_zero)
 
@@ -61,6 +62,15 @@ class Multigrid:
 
     def solve(self, x, b, method=MG_GMRES, restart=30, max_iter=200, rtol=1e-10):
         return mg_solve(self.ctx, x, b, method=method, restart=restart, max_iter=max_iter, rtol=rtol)
+
+    def newton(self, x, assemble, *, max_newton=3, ntol=1e-8, atol=0.0, reuse_rate=0.0, restart=30, max_iter=200,
+               rtol=1e-10):
+        """Newton's method with the caller's CPU assembly (include/newton.h):
+        assemble(w, F, vals) fills F(w) unless F is None and every level's
+        Jacobian values unless vals is None.  Returns (status, info)."""
+        sizes = [level_info(self.ctx, l)["nnzb"] * self.bs * self.bs for l in range(len(self.n))]
+        return mg_newton(self.ctx, x, assemble, self.n_dof, sizes, max_newton=max_newton, ntol=ntol, atol=atol,
+                         reuse_rate=reuse_rate, restart=restart, max_iter=max_iter, rtol=rtol)
 
     def apply_constraints(self, x):
         mg_apply_constraints(self.ctx, x)

@@ -286,11 +286,18 @@ def cell_sizes(mesh: M.Mesh, box) -> np.ndarray:
 def assemble(mesh: M.Mesh, nodes: M.NodeSet, op: Operator, box, H):
     """Condensed BSR  A_bar = H^T A H  (before Dirichlet / hanging identity rows).
     Returns row_ptr (n+1) int64, col (nnzb) int64, val (nnzb, bs, bs)."""
+    T, S = element_terms(op, mesh.dim, cell_sizes(mesh, box))
+    return assemble_terms(mesh, nodes, T, S, op.bs, op.symmetric, H)
+
+
+def assemble_terms(mesh: M.Mesh, nodes: M.NodeSet, T: np.ndarray, S: np.ndarray, bs: int, symmetric: bool, H):
+    """Condensed BSR of the element matrices A_e = sum_t S[e, t] T_t (T (n_terms,
+    nloc*bs, nloc*bs), S (n_e, n_terms)); the sparsity pattern depends on the
+    mesh connectivity only, never on the values."""
     N = len(nodes.keys)
-    dim = mesh.dim
-    nloc = 1 << dim
-    bs = op.bs
-    T, S = element_terms(op, dim, cell_sizes(mesh, box))
+    nloc = 1 << mesh.dim
+    T = np.ascontiguousarray(T, np.float64)
+    S = np.ascontiguousarray(S, np.float64)
     conn = np.ascontiguousarray(nodes.conn, np.int64)
     rp_h, col_h, w_h = (np.ascontiguousarray(a) for a in H)
     L = lib()
@@ -303,7 +310,7 @@ def assemble(mesh: M.Mesh, nodes: M.NodeSet, op: Operator, box, H):
     col = np.empty(nnzb, np.int64)
     val = np.empty((nnzb, bs, bs))
     rc = L.asm_condensed(N, bs, nloc, mesh.n_cells, ptr(conn), ptr(rp_h), ptr(col_h), ptr(w_h),
-                         T.shape[0], ptr(T), ptr(S), 1, int(op.symmetric), ptr(row_ptr), ptr(col), ptr(val))
+                         T.shape[0], ptr(T), ptr(S), 1, int(symmetric), ptr(row_ptr), ptr(col), ptr(val))
     if rc != 0:
         raise RuntimeError("assembly pass 1 failed")
     return row_ptr, col, val
@@ -338,6 +345,28 @@ def apply_constraints(row_ptr, col, val, cmask: np.ndarray, g: np.ndarray, b: np
     val[k] = vk
     if b is not None:
         b[cmask] = g[cmask]
+
+
+def constraint_plan(row_ptr, col, cmask: np.ndarray):
+    """The value-only part of apply_constraints (homogeneous g, no rhs) as a
+    reusable plan for repeated assemblies on one pattern (Newton Jacobians):
+    (entries touched, 0/1 keep mask per block entry, identity positions)."""
+    n, bs = cmask.shape
+    rows = row_of(row_ptr)
+    touch = cmask[rows].any(axis=1) | cmask[col].any(axis=1)
+    k = np.nonzero(touch)[0]
+    keep = (~cmask[rows[k]])[:, :, None] & (~cmask[col[k]])[:, None, :]
+    diag = np.nonzero(rows[k] == col[k])[0]
+    ident = [(k[diag[cmask[rows[k][diag], c]]], c) for c in range(bs)]
+    return k, keep.astype(np.float64), ident
+
+
+def apply_constraint_plan(val, plan):
+    """Same values as apply_constraints(..., g = 0, b = None)."""
+    k, keep, ident = plan
+    val[k] *= keep
+    for idx, c in ident:
+        val[idx, c, c] = 1.0
 
 
 # --------------------------------------------------------------------------

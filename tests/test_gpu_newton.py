@@ -1,0 +1,113 @@
+"""GPU parity of Newton's method around GMRES + MG (include/newton.h; the
+paper's hybrid workflow P:821) against oracle/newton.py on the
+same generated channel-flow problems and the same CPU assembly.
+
+Each Newton step re-uploads every level's Jacobian (mg_update_matrix), solves
+J d = -F with GMRES(30) + V(2,2) to rtol 1e-10 from 0 and applies w <- H(w + d)
+(mg_axpy + mg_apply_constraints) on the device.  Tolerances (reading Z11): the
+two sides' linear solves agree to ~kappa*1e-10, so residual norms agree to
+1e-8 ||F_0|| + 1e-6 ||F_k||, iterates to 1e-8 relative, GMRES counts +-1."""
+import functools
+
+import numpy as np
+import pytest
+
+from gpu_util import dev, host
+
+from oracle import newton as ON
+from problems import channel as C
+
+pytestmark = pytest.mark.gpu
+
+
+@functools.lru_cache(maxsize=None)
+def prob(name):
+    return C.build(name)
+
+
+def gpu_solver(P, u_old, w):
+    from paper_2405_05047_b200 import Multigrid
+    return Multigrid(C.with_values(P, C.jacobians(P, w, u_old)), 3, omega=P.omega, H=P.fine.H)
+
+
+def test_axpy_matches_definition():
+    import paper_2405_05047_b200 as m
+    P = prob("c4ns_small")
+    u = C.initial_state(P)
+    g = gpu_solver(P, u, u)
+    rng = np.random.default_rng(3)
+    x, y = rng.standard_normal(P.n_dof), rng.standard_normal(P.n_dof)
+    yd = dev(y)
+    m.mg_axpy(g.ctx, len(P.levels) - 1, -0.37, dev(x), yd)
+    exp = y + (-0.37) * x
+    assert np.max(np.abs(host(yd) - exp)) <= 1e-15 * np.max(np.abs(y) + 0.37 * np.abs(x))
+    g.close()
+
+
+@pytest.mark.parametrize("name", ["c4ns_small", "c4ns_mid"])
+def test_newton_time_steps_match_oracle(name):
+    P = prob(name)
+    u = C.initial_state(P)
+    g = gpu_solver(P, u, u)
+    x = dev(u.reshape(-1))
+    for step in range(3):
+        u_old = u.copy()
+        st, info = g.newton(x, C.assemble_callback(P, u_old), max_newton=4, ntol=1e-8)
+        u, hist = ON.newton_step(lambda v: C.with_values(P, v), lambda w: C.residual(P, w, u_old),
+                                 lambda w: C.jacobians(P, w, u_old), P.fine.H, u_old, omega=P.omega, max_newton=4)
+        assert info["converged"] and st == 0, info
+        F0 = hist[0][0]
+        assert len(info["res_norm"]) == len(hist), (info, hist)
+        for k, (nF, its) in enumerate(hist):
+            assert abs(info["res_norm"][k] - nF) <= 1e-8 * F0 + 1e-6 * nF, (step, k, info, hist)
+            if k < info["newton_its"]:
+                assert abs(info["lin_its"][k] - its) <= 1, (step, k, info, hist)
+        got = host(x).reshape(-1, 3)
+        assert np.linalg.norm(got - u) <= 1e-8 * np.linalg.norm(u), step
+        u = got   # continue both sides from the same state
+        x = dev(u.reshape(-1))
+    g.close()
+
+
+def test_newton_fullsize_c4ns():
+    """BASELINE config 4 at its full size (348,562 nodes = 1,045,686 DOFs, 9
+    levels): one time step from the impulsive start and one more; Newton must
+    reach 1e-8 within 4 steps with bounded GMRES counts (the oracle's own
+    counts: 13-20 on the mid mesh, 30 on the first full-size Newton step)."""
+    P = prob("c4ns")
+    assert P.n_dof == 1045686
+    u = C.initial_state(P)
+    g = gpu_solver(P, u, u)
+    x = dev(u.reshape(-1))
+    for step in range(2):
+        u_old = host(x).reshape(-1, 3)
+        st, info = g.newton(x, C.assemble_callback(P, u_old), max_newton=4, ntol=1e-8)
+        assert st == 0 and info["converged"], info
+        assert max(info["lin_its"]) <= 45, info
+        r = info["res_norm"]
+        assert all(r[k + 1] < r[k] for k in range(len(r) - 1)), info
+    # the final iterate's residual, recomputed by the CPU assembly, is the reported one
+    w = host(x).reshape(-1, 3)
+    nF = np.linalg.norm(C.residual(P, w, u_old))
+    assert abs(nF - info["res_norm"][-1]) <= 1e-6 * info["res_norm"][-1] + 1e-12 * info["res_norm"][0]
+    g.close()
+
+
+def test_inexact_newton_reuse_matches_oracle():
+    """reuse_rate > 0: the Jacobian is kept while ||F_k|| <= rate ||F_{k-1}||
+    (P:821); both sides take the same keep/rebuild decisions."""
+    P = prob("c4ns_mid")
+    u = C.initial_state(P)
+    g = gpu_solver(P, u, u)
+    x = dev(u.reshape(-1))
+    st, info = g.newton(x, C.assemble_callback(P, u), max_newton=10, ntol=1e-8, reuse_rate=0.3)
+    w, hist = ON.newton_step(lambda v: C.with_values(P, v), lambda w: C.residual(P, w, u),
+                             lambda w: C.jacobians(P, w, u), P.fine.H, u, omega=P.omega, max_newton=10,
+                             reuse_rate=0.3)
+    assert info["converged"] and len(info["res_norm"]) == len(hist), (info, hist)
+    assert info["jacobians"] < info["newton_its"], info          # at least one reuse happened
+    F0 = hist[0][0]
+    for k, (nF, its) in enumerate(hist):
+        assert abs(info["res_norm"][k] - nF) <= 1e-8 * F0 + 1e-6 * nF, (k, info, hist)
+    assert np.linalg.norm(host(x).reshape(-1, 3) - w) <= 1e-8 * np.linalg.norm(w)
+    g.close()

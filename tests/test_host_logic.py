@@ -14,7 +14,7 @@ from mgtest_util import ROOT, problem
 
 import oracle
 
-HDRS = [os.path.join(ROOT, "include", h) for h in ("mg.h", "mg_internal.h", "ns.h")]
+HDRS = [os.path.join(ROOT, "include", h) for h in ("mg.h", "mg_internal.h", "ns.h", "newton.h")]
 
 
 def _lib():
@@ -31,6 +31,7 @@ def declared_symbols():
     for h in HDRS:
         txt = open(h).read()
         txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+        txt = re.sub(r"typedef[^;]*;", "", txt)            # function-pointer types are not symbols
         for m in re.finditer(r"\b((?:mgi?|ns)_[a-z0-9_]+)\s*\(", txt):
             names.add(m.group(1))
     return sorted(names)
