@@ -525,8 +525,9 @@ def run_newton(args):
     log(f"[bench] generated c4ns: {P.n_dof} DOFs, levels {[L.data.n for L in P.levels]} in {time.time() - t:.1f}s")
     stream = torch.cuda.current_stream()
     u = C.initial_state(P)
-    solver = mg.Multigrid(C.with_values(P, C.jacobians(P, u, u)), 3, omega=P.omega, H=P.fine.H, device=local,
-                          stream=stream)
+    omega = args.omega if args.omega else (1.0 if args.vanka else P.omega)
+    solver = mg.Multigrid(C.with_values(P, C.jacobians(P, u, u)), 3, omega=omega, H=P.fine.H, device=local,
+                          stream=stream, vanka=args.vanka)
     ctx = solver.ctx
     L = len(P.levels) - 1
     infos = [mg.level_info(ctx, l) for l in range(L + 1)]
@@ -597,6 +598,8 @@ def run_newton(args):
         "config": {"workload": WORKLOADS["c4ns"], "n_dof": N, "levels": L + 1,
                    "level_rows": [i["n"] for i in infos], "nnzb_fine": infos[L]["nnzb"],
                    "parallelism": "single GPU", "l2": "finest Jacobian 0.29 GB > L2 126 MB",
+                   "smoother": ("Vanka (cell patches, mg_set_vanka)" if args.vanka else "block-Jacobi")
+                   + f", omega {omega}",
                    "newton_per_step": newton / args.steps, "gmres_per_step": its / args.steps,
                    "lin_its": lin},
         "dof_cycles_per_s": value * N,
@@ -723,6 +726,8 @@ def main():
     ap.add_argument("--no-mixed", action="store_true", help="skip the mixed-precision side measurement")
     ap.add_argument("--precision", choices=["fp64", "mixed"], default="fp64",
                     help="mixed: fp32-stored V-cycle operators inside fp64 GMRES (SURVEY N1)")
+    ap.add_argument("--vanka", action="store_true", help="c4ns: Vanka-type cell-patch smoother (P:822)")
+    ap.add_argument("--omega", type=float, default=0.0, help="c4ns: smoother damping (0: config default)")
     ap.add_argument("--min-rows-per-rank", type=int, default=16384,
                     help="multi-GPU: levels with fewer rows per rank are replicated (agglomerated)")
     args = ap.parse_args()

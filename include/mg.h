@@ -210,6 +210,24 @@ mg_status mg_set_transfer(mg_ctx ctx, int fine_level, const int64_t *row_ptr, co
 mg_status mg_set_smoother(mg_ctx ctx, int level, double omega, int nu_pre, int nu_post,
                           const double *dinv, int mem);
 
+/* Vanka-type smoother on one level ("a Vanka smoother can be easily
+ * implemented with custom kernels"): patch-wise additive Schwarz
+ *   x <- x + omega sum_p R_p^T W_p A_pp^{-1} R_p (b - A x),
+ * replacing the block-Jacobi sweep of that level in every smoothing step
+ * (mg_smooth, mg_sweep, the V-cycle, the smoothing coarse solve).
+ * patch_nodes [n_patches * nloc]: the level's rows (local ids, distinct within
+ * a patch; e.g. the 2^d nodes of each mesh cell); every row must lie in at
+ * least one patch; W = diag(1 / number of patches holding the row), so
+ * overlapping patches average.  A_pp (nloc*bs square, blocks of A between the
+ * patch's nodes, absent blocks 0; the V-cycle operator's values, i.e. fp32-
+ * rounded in mixed precision) is inverted on the device by Gauss-Jordan with
+ * partial pivoting at setup and after mg_update_matrix.  Constraints:
+ * nloc * block_size <= 32, level not distributed, mg_set_matrix first.
+ * n_patches = 0 switches the level back to block-Jacobi.  Errors:
+ * MG_ERR_STRUCTURE (node out of range / repeated / uncovered row),
+ * MG_ERR_SINGULAR (singular A_pp, reported at setup), MG_ERR_STATE. */
+mg_status mg_set_vanka(mg_ctx ctx, int level, int64_t n_patches, int nloc, const int64_t *patch_nodes, int mem);
+
 /* Hanging-node matrix H of the finest level (n x n CSR, weights_per_entry 1;
  * identity rows at regular nodes, master weights at hanging nodes). */
 mg_status mg_set_constraints(mg_ctx ctx, const int64_t *H_row_ptr, const int64_t *H_col,

@@ -30,6 +30,7 @@ class MgLevel:
     wpe: int = 1
     dinv: np.ndarray | None = None
     R: tuple | None = None        # R_{l-1} = P_{l-1}^T (built here)
+    vanka: tuple | None = None    # (patches, A_pp^{-1}, W) of the Vanka smoother, or None
 
 
 @dataclass
@@ -46,7 +47,7 @@ class MgHierarchy:
 
     @classmethod
     def from_arrays(cls, levels, omega=0.8, nu_pre=2, nu_post=2, coarse="direct", coarse_sweeps=20, H=None,
-                    mean=None):
+                    mean=None, vanka=False):
         """levels: list (coarse -> fine) of objects with n, bs, row_ptr, col, val,
         P (or None), wpe.  mean: per level (w, k) or None -- the global
         constraint int_Omega p = w^T x = 0 imposed on every level of a
@@ -57,6 +58,8 @@ class MgHierarchy:
             lv = MgLevel(L.n, L.bs, np.asarray(L.row_ptr, np.int64), np.asarray(L.col, np.int64),
                          np.asarray(L.val, np.float64), L.P if l > 0 else None, getattr(L, "wpe", 1))
             lv.dinv = block_diag_inverse(lv.n, lv.bs, lv.rp, lv.col, lv.val)
+            if vanka and getattr(L, "patches", None) is not None:
+                lv.vanka = vanka_setup(lv, L.patches)
             if l > 0:
                 prp, pcol, pw = lv.P
                 lv.R = csr_transpose(lv.n, out[-1].n, prp, pcol, pw, lv.wpe)
@@ -79,8 +82,11 @@ class MgHierarchy:
         return spmv(L.n, L.bs, L.rp, L.col, L.val, x)
 
     def smooth(self, l, x, b):
-        """S_l(x, b): one damped block-Jacobi step x + omega D^{-1}(b - A x)."""
+        """S_l(x, b): one damped block-Jacobi step x + omega D^{-1}(b - A x),
+        or a Vanka patch step on levels with patches."""
         L = self.levels[l]
+        if getattr(L, "vanka", None) is not None:
+            return vanka_sweep(L, L.vanka, self.omega, x, b)
         return jacobi_sweep(L.n, L.bs, L.rp, L.col, L.val, L.dinv, self.omega, x, b)
 
     def restrict(self, l, r):
@@ -103,6 +109,39 @@ class MgHierarchy:
         for _ in range(self.coarse_sweeps):
             x = self.smooth(0, x, b)
         return x
+
+
+def vanka_setup(L, patches):
+    """Vanka-type smoother data: for every patch p (rows patches[p]) the
+    dense inverse of A_pp -- the blocks of A between the patch's nodes, absent
+    blocks zero -- by LAPACK (numpy.linalg.inv, a library primitive), and the
+    weights W = 1 / (number of patches holding the row)."""
+    patches = np.asarray(patches, np.int64)
+    npch, nl = patches.shape
+    bs, n = L.bs, L.n
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(L.rp))
+    keys = rows * n + L.col                                   # ascending (CSR, sorted columns)
+    q = (patches[:, :, None] * n + patches[:, None, :]).ravel()
+    pos = np.minimum(np.searchsorted(keys, q), len(keys) - 1)
+    hit = keys[pos] == q
+    blk = np.where(hit[:, None, None], L.val.reshape(-1, bs, bs)[pos], 0.0).reshape(npch, nl, nl, bs, bs)
+    A_pp = blk.transpose(0, 1, 3, 2, 4).reshape(npch, nl * bs, nl * bs)
+    mult = np.bincount(patches.ravel(), minlength=n)
+    if np.any(mult == 0):
+        raise ValueError("row in no patch")
+    return patches, np.linalg.inv(A_pp), 1.0 / mult
+
+
+def vanka_sweep(L, vk, omega, x, b):
+    """One Vanka step x + omega sum_p R_p^T W A_pp^{-1} R_p (b - A x)."""
+    patches, inv, w = vk
+    bs = L.bs
+    r = residual(L.n, bs, L.rp, L.col, L.val, x, b).reshape(-1, bs)
+    rp = r[patches].reshape(len(patches), -1)                  # R_p r
+    c = np.einsum("pij,pj->pi", inv, rp).reshape(len(patches), -1, bs)
+    acc = np.zeros_like(r)
+    np.add.at(acc, patches.ravel(), c.reshape(-1, bs))
+    return np.asarray(x, np.float64) + omega * (w[:, None] * acc).reshape(-1)
 
 
 def project_zero_mean(x, w, k=None):

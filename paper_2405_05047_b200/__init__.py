@@ -79,6 +79,7 @@ _SIGS = {
     "mg_update_matrix": [_P, _I, _P, _I],
     "mg_set_transfer": [_P, _I, _P, _P, _P, _I64, _I, _I],
     "mg_set_smoother": [_P, _I, _D, _I, _I, _P, _I],
+    "mg_set_vanka": [_P, _I, _I64, _I, _P, _I],
     "mg_set_constraints": [_P, _P, _P, _P, _I64, _I],
     "mg_set_mean_constraint": [_P, _I, _P, _P, _I],
     "mg_project_zero_mean": [_P, _I, _P],
@@ -275,6 +276,15 @@ def mg_set_transfer(ctx, fine_level, row_ptr, col, w, weights_per_entry=1):
 def mg_set_smoother(ctx, level, omega=0.0, nu_pre=-1, nu_post=-1, dinv=None):
     p, mem = _ptr(dinv, np.float64)
     _check(_lib.mg_set_smoother(ctx, level, omega, nu_pre, nu_post, p, mem), "mg_set_smoother")
+
+
+def mg_set_vanka(ctx, level, patch_nodes):
+    """patch_nodes: (n_patches, nloc) int64 rows of the level (None / empty: block-Jacobi)."""
+    if patch_nodes is None or len(patch_nodes) == 0:
+        _check(_lib.mg_set_vanka(ctx, level, 0, 1, None, MG_MEM_HOST), "mg_set_vanka")
+        return
+    pn = np.ascontiguousarray(patch_nodes, dtype=np.int64)
+    _check(_lib.mg_set_vanka(ctx, level, pn.shape[0], pn.shape[1], pn.ctypes.data, MG_MEM_HOST), "mg_set_vanka")
 
 
 def mg_set_constraints(ctx, row_ptr, col, w):

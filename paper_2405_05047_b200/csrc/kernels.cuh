@@ -894,4 +894,141 @@ __global__ void k_rank1_reg(int64_t N, int64_t ld, double *__restrict__ a, const
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Vanka-type patch smoother:
+//   x <- x + omega sum_p R_p^T W_p A_pp^{-1} R_p (b - A x),
+// patches of nl nodes (e.g. the 2^d nodes of a mesh cell), m = nl*BS <= 32
+// unknowns, W = diag(1/multiplicity).  Deterministic: a patch pass writes
+// c_p = A_pp^{-1} r_p per patch, a node pass gathers sum_p c_p through the
+// node -> (patch, corner) list in a fixed order (no atomics).
+// ---------------------------------------------------------------------------
+constexpr int kVankaWarps = 2;  // warps per CTA of the build kernel (2 x 16.9 KB shared)
+
+// ent[(p*nl + a)*nl + b] = SELL entry of block (node_a, node_b) of patch p, -1 if absent.
+__global__ void k_vanka_find(int64_t np, int nl, const int32_t *__restrict__ nodes,
+                             const int64_t *__restrict__ slice_ptr, const int32_t *__restrict__ col,
+                             const int32_t *__restrict__ row_pos, int64_t *__restrict__ ent) {
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < np * nl; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t p = t / nl;
+    int64_t *out = ent + t * nl;
+    for (int b = 0; b < nl; ++b) out[b] = -1;
+    const int i = nodes[t];
+    const int pos = row_pos[i];
+    const int s = pos >> 5, lane = pos & 31;
+    const int64_t e0 = slice_ptr[s], len = (slice_ptr[s + 1] - e0) >> 5;
+    for (int64_t k = 0; k < len; ++k) {
+      const int64_t e = e0 + 32 * k + lane;
+      const int cj = col[e];
+      for (int b = 0; b < nl; ++b)  // first match: padding repeats the last real column
+        if (out[b] < 0 && nodes[p * nl + b] == cj) out[b] = e;
+    }
+  }
+}
+
+// Dense inverse of every patch matrix A_pp (Gauss-Jordan, partial pivoting,
+// ties -> lowest row), stored column-major: inv[p*m*m + c*m + r].  Warp per
+// patch, lane = row.  flag |= 2 on a singular patch.
+template <int BS>
+__global__ void __launch_bounds__(32 * kVankaWarps) k_vanka_build(int64_t np, int nl, const int64_t *__restrict__ ent,
+                                                                 const double *__restrict__ val64,
+                                                                 const float *__restrict__ val32,
+                                                                 double *__restrict__ inv, int *flag) {
+  __shared__ double sA[kVankaWarps][32][33], sI[kVankaWarps][32][33];
+  const int w = threadIdx.x >> 5, r = threadIdx.x & 31;
+  const int64_t p = int64_t(blockIdx.x) * kVankaWarps + w;
+  if (p >= np) return;
+  const int m = nl * BS;
+  constexpr int V = BS * BS;
+  double(*A)[33] = sA[w];
+  double(*I)[33] = sI[w];
+  if (r < m) {
+    const int a = r / BS, rr = r % BS;
+    for (int c = 0; c < m; ++c) {
+      const int64_t e = ent[(p * nl + a) * nl + c / BS];
+      const int j = rr * BS + c % BS;
+      A[r][c] = e < 0 ? 0.0 : (val32 ? double(val32[sell_off32(e, V, j)]) : val64[sell_off64(e, V, j)]);
+      I[r][c] = r == c ? 1.0 : 0.0;
+    }
+  }
+  __syncwarp();
+  bool ok = true;
+  for (int k = 0; k < m; ++k) {
+    int piv = k;
+    double best = fabs(A[k][k]);
+    for (int q = k + 1; q < m; ++q) {
+      const double v = fabs(A[q][k]);
+      if (v > best) best = v, piv = q;
+    }
+    if (!(best > 0.0)) {
+      ok = false;
+      break;
+    }
+    if (piv != k && r < m) {  // lane r swaps column r of rows k and piv
+      double t = A[k][r];
+      A[k][r] = A[piv][r];
+      A[piv][r] = t;
+      t = I[k][r];
+      I[k][r] = I[piv][r];
+      I[piv][r] = t;
+    }
+    __syncwarp();
+    const double d = A[k][k];
+    __syncwarp();
+    if (r < m) {
+      A[k][r] = __ddiv_rn(A[k][r], d);
+      I[k][r] = __ddiv_rn(I[k][r], d);
+    }
+    __syncwarp();
+    if (r < m && r != k) {
+      const double f = A[r][k];
+      for (int c = 0; c < m; ++c) {
+        A[r][c] = A[r][c] - f * A[k][c];
+        I[r][c] = I[r][c] - f * I[k][c];
+      }
+    }
+    __syncwarp();
+  }
+  if (!ok) {
+    if (r == 0) atomicOr(flag, 2);
+    return;
+  }
+  if (r < m)
+    for (int c = 0; c < m; ++c) inv[p * m * m + int64_t(c) * m + r] = I[r][c];
+}
+
+// c_p = A_pp^{-1} r_p (r = b - A x, or b itself for a zero start).  Warp per patch.
+template <int BS>
+__global__ void __launch_bounds__(kCta) k_vanka_patch(int64_t np, int nl, const int32_t *__restrict__ nodes,
+                                                     const double *__restrict__ inv, const double *__restrict__ r,
+                                                     double *__restrict__ cbuf) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p = int64_t(blockIdx.x) * kWarpsPerCta + (threadIdx.x >> 5);
+  if (p >= np) return;
+  const int m = nl * BS;
+  const double rl = lane < m ? __ldg(r + int64_t(nodes[p * nl + lane / BS]) * BS + lane % BS) : 0.0;
+  const double *ip = inv + p * m * m;
+  double acc = 0.0;
+  for (int j = 0; j < m; ++j) {
+    const double rj = __shfl_sync(0xffffffffu, rl, j);
+    if (lane < m) acc = fma(__ldcs(ip + int64_t(j) * m + lane), rj, acc);
+  }
+  if (lane < m) cbuf[p * m + lane] = acc;
+}
+
+// x_i = (assign ? 0 : x_i) + omega w_i sum_{(p, a) in list(i)} c_p[a*BS + comp]; thread per DOF.
+__global__ void k_vanka_update(int64_t n, int bs, int m, const int64_t *__restrict__ nptr,
+                               const int64_t *__restrict__ nlist, const double *__restrict__ wgt,
+                               const double *__restrict__ cbuf, double omega, int assign, double *__restrict__ x) {
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n * bs; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = t / bs;
+    const int comp = int(t % bs);
+    double s = 0.0;
+    for (int64_t q = nptr[i]; q < nptr[i + 1]; ++q) s += __ldg(cbuf + nlist[q] + comp);
+    const double upd = omega * (wgt[i] * s);
+    x[t] = assign ? upd : x[t] + upd;
+  }
+  (void)m;
+}
+
 }  // namespace mgk

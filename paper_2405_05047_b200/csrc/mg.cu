@@ -184,6 +184,18 @@ struct Level {
   double omega = 0.0;
   int nu_pre = -1, nu_post = -1;
   DevArray<double> x, b, w;  // correction, restricted rhs, work (ping-pong / residual)
+  // Vanka-type patch smoother (mg_set_vanka): replaces block-Jacobi on this level
+  struct Vanka {
+    bool on = false, ready = false;
+    int64_t np = 0;
+    int nl = 0, m = 0;
+    DevArray<int32_t> nodes;          // [np*nl] patch nodes (local rows)
+    DevArray<int64_t> ent;            // [np*nl*nl] SELL entry of each block of A_pp (-1: absent)
+    DevArray<double> inv;             // [np*m*m] A_pp^{-1}, column-major per patch
+    DevArray<int64_t> nptr, nlist;    // node -> p*m + a*bs (CSR, ascending patch order)
+    DevArray<double> wgt;             // 1 / multiplicity
+    DevArray<double> cbuf;            // [np*m] patch corrections
+  } vk;
 };
 
 struct GraphExec {
@@ -769,6 +781,49 @@ mg_status device_dinv(mg_ctx_s *c, int l) {
   return MG_OK;
 }
 
+// Vanka patch inverses from the V-cycle operator's values (fp32-rounded in
+// mixed precision), on the device.  Synchronises.
+mg_status vanka_build(mg_ctx_s *c, int l) {
+  Level &L = c->lv[l];
+  Level::Vanka &V = L.vk;
+  Level::Part &Pt = L.part[0];
+  const int bs = c->bs();
+  if (V.np == 0) {
+    V.ready = true;
+    return MG_OK;
+  }
+  if (V.ent.n < size_t(V.np) * V.nl * V.nl) {
+    TRY(V.ent.alloc(size_t(V.np) * V.nl * V.nl));
+    const unsigned g = unsigned(std::min<int64_t>((V.np * V.nl + 255) / 256, 16 * c->n_sm));
+    ++g_tally, mgk::k_vanka_find<<<g, 256, 0, c->stream>>>(V.np, V.nl, V.nodes.p, Pt.A.slice_ptr.p, Pt.A.col.p,
+                                                           Pt.upos.p, V.ent.p);
+    TRY(check_launch("vanka find"));
+  }
+  DevArray<int> flag;
+  TRY(flag.alloc(1));
+  CU(cudaMemsetAsync(flag.p, 0, sizeof(int), c->stream));
+  const unsigned g = unsigned((V.np + mgk::kVankaWarps - 1) / mgk::kVankaWarps);
+  const double *v64 = Pt.A.f32 ? nullptr : Pt.A.val.p;
+  const float *v32 = Pt.A.f32 ? Pt.A.valf.p : nullptr;
+  switch (bs) {
+    case 1: ++g_tally, mgk::k_vanka_build<1><<<g, 32 * mgk::kVankaWarps, 0, c->stream>>>(V.np, V.nl, V.ent.p, v64, v32, V.inv.p, flag.p); break;
+    case 2: ++g_tally, mgk::k_vanka_build<2><<<g, 32 * mgk::kVankaWarps, 0, c->stream>>>(V.np, V.nl, V.ent.p, v64, v32, V.inv.p, flag.p); break;
+    case 3: ++g_tally, mgk::k_vanka_build<3><<<g, 32 * mgk::kVankaWarps, 0, c->stream>>>(V.np, V.nl, V.ent.p, v64, v32, V.inv.p, flag.p); break;
+    case 4: ++g_tally, mgk::k_vanka_build<4><<<g, 32 * mgk::kVankaWarps, 0, c->stream>>>(V.np, V.nl, V.ent.p, v64, v32, V.inv.p, flag.p); break;
+    default: ++g_tally, mgk::k_vanka_build<6><<<g, 32 * mgk::kVankaWarps, 0, c->stream>>>(V.np, V.nl, V.ent.p, v64, v32, V.inv.p, flag.p); break;
+  }
+  TRY(check_launch("vanka build"));
+  int f = 0;
+  CU(cudaMemcpyAsync(&f, flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (f & 2) return fail(MG_ERR_SINGULAR, "level %d: singular Vanka patch matrix", l);
+  V.ready = true;
+  return MG_OK;
+}
+
+// One Vanka sweep x <- x + omega sum_p R_p^T W A_pp^{-1} R_p (b - A x); zero: x enters as 0.
+mg_status vanka_sweep(mg_ctx_s *c, int l, double *x, const double *b, bool zero);
+
 double lv_omega(const mg_ctx_s *c, const Level &L) { return L.omega > 0.0 ? L.omega : c->cfg.omega; }
 int lv_nu_pre(const mg_ctx_s *c, const Level &L) { return L.nu_pre >= 0 ? L.nu_pre : c->cfg.nu_pre; }
 int lv_nu_post(const mg_ctx_s *c, const Level &L) { return L.nu_post >= 0 ? L.nu_post : c->cfg.nu_post; }
@@ -806,7 +861,7 @@ mg_status build_tail(mg_ctx_s *c) {
   const char mode = env && *env ? env[0] : '0';
   if (mode != '1' && mode != 'c') return MG_OK;
   for (const Level &L : c->lv)
-    if (L.mean) return MG_OK;  // the tail has no projection step
+    if (L.mean || L.vk.on) return MG_OK;  // the tail has no projection / Vanka step
   c->tail_cluster = mode == 'c';
   const int64_t max_slices = env_i64("MGB200_TAIL_SLICES", c->tail_cluster ? 256 : 1024);
   int T = -1;
@@ -972,6 +1027,7 @@ mg_status finalize(mg_ctx_s *c) {
       if (!L.dinv_host.empty()) TRY(upload_dinv(L, bs, L.dinv_host));
       else TRY(device_dinv(c, l));
     }
+    if (L.vk.on && !L.vk.ready) TRY(vanka_build(c, l));
     const size_t nv = size_t(std::max<int64_t>(1, L.n)) * bs;
     if (L.w.n < nv) TRY(L.w.alloc(nv));
     if (l < c->L()) {
@@ -1077,12 +1133,43 @@ mg_status do_prolong(mg_ctx_s *c, int l, const double *y, double *x) {
   return launch_transfer(c->bs(), true, L.P, In{y, L.hp.active ? L.hp.ghost.p : nullptr, int(C.n)}, x, c->stream);
 }
 
+mg_status vanka_sweep(mg_ctx_s *c, int l, double *x, const double *b, bool zero) {
+  Level &L = c->lv[l];
+  Level::Vanka &V = L.vk;
+  const int bs = c->bs();
+  const double *r = b;
+  if (!zero) {
+    TRY(a_pass_resid(c, l, x, b, L.w.p));
+    r = L.w.p;
+  }
+  if (V.np) {
+    const unsigned g = unsigned((V.np + mgk::kWarpsPerCta - 1) / mgk::kWarpsPerCta);
+    switch (bs) {
+      case 1: ++g_tally, mgk::k_vanka_patch<1><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
+      case 2: ++g_tally, mgk::k_vanka_patch<2><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
+      case 3: ++g_tally, mgk::k_vanka_patch<3><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
+      case 4: ++g_tally, mgk::k_vanka_patch<4><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
+      default: ++g_tally, mgk::k_vanka_patch<6><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
+    }
+    TRY(check_launch("vanka patch"));
+  }
+  if (L.n == 0) return MG_OK;
+  const unsigned g = unsigned(std::min<int64_t>((L.n * bs + 255) / 256, 16 * c->n_sm));
+  ++g_tally, mgk::k_vanka_update<<<g, 256, 0, c->stream>>>(L.n, bs, V.m, V.nptr.p, V.nlist.p, V.wgt.p, V.cbuf.p,
+                                                            lv_omega(c, L), zero ? 1 : 0, x);
+  return check_launch("vanka update");
+}
+
 mg_status smooth(mg_ctx_s *c, int l, double *x, const double *b, int k, bool zero) {
   Level &L = c->lv[l];
   const int bs = c->bs();
   const double om = lv_omega(c, L);
   if (k <= 0) {
     if (zero) CU(cudaMemsetAsync(x, 0, size_t(L.n) * bs * sizeof(double), c->stream));
+    return MG_OK;
+  }
+  if (L.vk.on) {
+    for (int i = 0; i < k; ++i) TRY(vanka_sweep(c, l, x, b, zero && i == 0));
     return MG_OK;
   }
   if (zero) {
@@ -1425,6 +1512,8 @@ mg_status mg_set_matrix(mg_ctx c, int level, const int64_t *row_ptr, const int64
   std::vector<int64_t> rp, cl;
   std::vector<double> v;
   TRY(fetch_csr(c, L.n, L.n_global, row_ptr, col, vals, nnzb, V, mem, true, L.row_begin, rp, cl, v, "matrix"));
+  L.vk.ready = false;  // a Vanka smoother on this level re-locates its blocks in the new layout
+  L.vk.ent.release();
   const bool mixed = c->cfg.precision == MG_PREC_MIXED;
   std::vector<double> v64;
   if (mixed) {
@@ -1644,6 +1733,60 @@ mg_status mg_set_smoother(mg_ctx c, int level, double omega, int nu_pre, int nu_
   return MG_OK;
 }
 
+mg_status mg_set_vanka(mg_ctx c, int level, int64_t n_patches, int nloc, const int64_t *patch_nodes, int mem) {
+  TRY(check_level(c, level));
+  DeviceGuard dg(c->device);
+  Level &L = c->lv[level];
+  Level::Vanka &V = L.vk;
+  const int bs = c->bs();
+  if (n_patches < 0 || nloc < 1 || (n_patches > 0 && !patch_nodes))
+    return fail(MG_ERR_INVALID_ARG, "bad patch arguments");
+  if (n_patches == 0) {  // switch back to block-Jacobi
+    V = Level::Vanka{};
+    c->invalidate();
+    return MG_OK;
+  }
+  if (nloc * bs > 32) return fail(MG_ERR_INVALID_ARG, "patch of %d unknowns: nloc * block_size must be <= 32", nloc * bs);
+  if (!L.part[0].A.set) return fail(MG_ERR_STATE, "level %d: call mg_set_matrix before mg_set_vanka", level);
+  if (L.dist || L.nparts != 1) return fail(MG_ERR_STATE, "level %d: Vanka needs a non-distributed level", level);
+  std::vector<int64_t> pn;
+  TRY(fetch(pn, patch_nodes, size_t(n_patches) * nloc, mem));
+  std::vector<int64_t> cnt(L.n + 1, 0);
+  for (int64_t p = 0; p < n_patches; ++p)
+    for (int a = 0; a < nloc; ++a) {
+      const int64_t i = pn[p * nloc + a];
+      if (i < 0 || i >= L.n) return fail(MG_ERR_STRUCTURE, "patch %lld: node %lld out of range", (long long)p, (long long)i);
+      for (int b2 = 0; b2 < a; ++b2)
+        if (pn[p * nloc + b2] == i) return fail(MG_ERR_STRUCTURE, "patch %lld: repeated node", (long long)p);
+      ++cnt[i + 1];
+    }
+  std::vector<double> wgt(L.n);
+  for (int64_t i = 0; i < L.n; ++i) {
+    if (cnt[i + 1] == 0) return fail(MG_ERR_STRUCTURE, "level %d: row %lld in no patch", level, (long long)i);
+    wgt[i] = 1.0 / double(cnt[i + 1]);
+  }
+  for (int64_t i = 0; i < L.n; ++i) cnt[i + 1] += cnt[i];
+  std::vector<int64_t> list(cnt[L.n]), fill(cnt.begin(), cnt.end() - 1);
+  const int m = nloc * bs;
+  for (int64_t p = 0; p < n_patches; ++p)  // ascending patch order per node: fixed summation order
+    for (int a = 0; a < nloc; ++a) list[fill[pn[p * nloc + a]]++] = p * m + int64_t(a) * bs;
+  std::vector<int32_t> nodes32(pn.begin(), pn.end());
+  Level::Vanka nv;
+  nv.on = true;
+  nv.np = n_patches;
+  nv.nl = nloc;
+  nv.m = m;
+  TRY(nv.nodes.upload(nodes32.data(), nodes32.size()));
+  TRY(nv.nptr.upload(cnt.data(), cnt.size()));
+  TRY(nv.nlist.upload(list.data(), list.size()));
+  TRY(nv.wgt.upload(wgt.data(), wgt.size()));
+  TRY(nv.inv.alloc(size_t(n_patches) * m * m));
+  TRY(nv.cbuf.alloc(size_t(n_patches) * m));
+  V = std::move(nv);
+  c->invalidate();
+  return MG_OK;
+}
+
 mg_status mg_set_constraints(mg_ctx c, const int64_t *H_row_ptr, const int64_t *H_col, const double *H_w, int64_t nnz,
                              int mem) {
   TRY(check_ctx(c));
@@ -1729,6 +1872,11 @@ mg_status mg_sweep(mg_ctx c, int level, const double *x, const double *b, double
   DeviceGuard dg(c->device);
   Tally tally(c);
   TRY(finalize(c));
+  if (c->lv[level].vk.on) {
+    const size_t n = size_t(c->lv[level].n) * c->bs();
+    if (n) CU(cudaMemcpyAsync(x_out, x, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    return vanka_sweep(c, level, x_out, b, false);
+  }
   return a_pass_sweep(c, level, x, b, x_out);
 }
 
@@ -1891,6 +2039,7 @@ mg_status mg_update_matrix(mg_ctx c, int level, const double *vals, int mem) {
   CU(cudaStreamSynchronize(c->stream));
   if (f & 1) return fail(MG_ERR_NONFINITE, "level %d: non-finite matrix value", level);
   if (L.dinv_host.empty()) TRY(device_dinv(c, level));  // a user-supplied D^-1 is kept
+  if (L.vk.on) TRY(vanka_build(c, level));
   if (level == 0 && c->cfg.coarse_mode == MG_COARSE_DIRECT && !L.dist && c->cN > 0) {
     CU(cudaMemsetAsync(c->cinv.p, 0, c->cinv.n * sizeof(double), c->stream));
     const unsigned gd = unsigned(std::min<int64_t>(std::max<int64_t>(1, (nnzb * V + 255) / 256), 16 * c->n_sm));

@@ -4,7 +4,7 @@ from __future__ import annotations
 
 from . import (MG_COARSE_DIRECT, MG_GMRES, level_info, mg_apply_constraints, mg_create, mg_create_level, mg_destroy,
                mg_newton,
-               mg_set_constraints, mg_set_matrix, mg_set_mean_constraint, mg_set_smoother, mg_set_transfer, mg_setup, mg_solve,
+               mg_set_constraints, mg_set_matrix, mg_set_vanka, mg_set_mean_constraint, mg_set_smoother, mg_set_transfer, mg_setup, mg_solve,
                mg_vcycle, mg_vcycle_zero)
 
 
@@ -17,11 +17,14 @@ class Multigrid:
     w^T x = 0 of a pure-Neumann operator.
     Multi-GPU: comm = (nranks, rank, id_bytes, transport) and levels carrying
     n_global, row_begin, row_end (this rank's rows; columns global), e.g. from
-    problems.partition."""
+    problems.partition.
+    vanka: levels carrying `patches` ((n_patches, nloc) rows, e.g. mesh cells)
+    use the Vanka-type patch smoother (mg_set_vanka) instead of
+    block-Jacobi."""
 
     def __init__(self, levels, bs, *, omega=0.8, nu_pre=2, nu_post=2, coarse_mode=MG_COARSE_DIRECT,
                  coarse_sweeps=20, use_graphs=True, device=0, stream=None, H=None, omegas=None, comm=None,
-                 precision=0):
+                 precision=0, vanka=False):
         self.bs = bs
         self.n = [int(L.n) for L in levels]
         self.ctx = mg_create(len(levels), bs, nu_pre=nu_pre, nu_post=nu_post, omega=omega,
@@ -40,6 +43,8 @@ class Multigrid:
                     mg_set_transfer(self.ctx, l, rp, col, w, getattr(L, "wpe", 1))
                 if omegas is not None:
                     mg_set_smoother(self.ctx, l, omegas[l])
+                if vanka and getattr(L, "patches", None) is not None:
+                    mg_set_vanka(self.ctx, l, L.patches)
                 if getattr(L, "mean_w", None) is not None:
                     mg_set_mean_constraint(self.ctx, l, L.mean_w, L.mean_k)
             if H is not None:

@@ -301,7 +301,8 @@ def with_values(P: ChannelProblem, vals) -> list:
     out = []
     for CL, v in zip(P.levels, vals):
         d = CL.data
-        out.append(LevelData(d.n, 3, d.row_ptr, d.col, v, d.cmask, d.H, P=d.P, wpe=d.wpe, keys=d.keys))
+        out.append(LevelData(d.n, 3, d.row_ptr, d.col, v, d.cmask, d.H, P=d.P, wpe=d.wpe, keys=d.keys,
+                             patches=CL.conn))
     return out
 
 

@@ -35,6 +35,7 @@ class LevelData:
     mean_k: np.ndarray | None = None  # (n,) pure Neumann: kernel vector (1 free, 0 hanging)
     mesh: M.Mesh | None = None
     nodes: M.NodeSet | None = None
+    patches: np.ndarray | None = None  # (n_cells, 2^d) node ids of each mesh cell (Vanka patches)
 
     @property
     def nnzb(self) -> int:
@@ -135,7 +136,7 @@ def make_problem(name, root, box, steps, op: F.Operator, *, seed_index=0, omega=
             cmask[:, 0] = nodes.hanging
         rp, col, val = F.assemble(lm, nodes, op, box, H)
         lvl = LevelData(n, bs, rp, col, val, cmask, H, keys=nodes.keys, mesh=lm if keep_geometry else None,
-                        nodes=nodes if keep_geometry else None)
+                        nodes=nodes if keep_geometry else None, patches=np.ascontiguousarray(nodes.conn, np.int64))
         if neumann:
             lvl.mean_k = (~nodes.hanging).astype(np.float64)
             m = apply_HT(H, load_vector(lm, nodes, box, lambda xp: np.ones(len(xp)), 1))[:, 0]
