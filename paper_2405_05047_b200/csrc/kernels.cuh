@@ -926,13 +926,21 @@ __global__ void k_vanka_find(int64_t np, int nl, const int32_t *__restrict__ nod
   }
 }
 
+// Inverse layout: patches in groups of ppw = 32 / m (the patches one warp of
+// k_vanka_patch serves); column c of the group's patches is contiguous, so the
+// warp reads ppw*m consecutive doubles per column:
+//   element (r, c) of patch p at ((p / ppw) * m + c) * (ppw * m) + (p % ppw) * m + r.
+__device__ __forceinline__ int64_t vk_off(int64_t p, int m, int ppw, int r, int c) {
+  return ((p / ppw) * m + c) * int64_t(ppw * m) + (p % ppw) * m + r;
+}
+
 // Dense inverse of every patch matrix A_pp (Gauss-Jordan, partial pivoting,
-// ties -> lowest row), stored column-major: inv[p*m*m + c*m + r].  Warp per
-// patch, lane = row.  flag |= 2 on a singular patch.
+// ties -> lowest row), in the vk_off layout.  Warp per patch, lane = row.
+// flag |= 2 on a singular patch.
 template <int BS>
 __global__ void __launch_bounds__(32 * kVankaWarps) k_vanka_build(int64_t np, int nl, const int64_t *__restrict__ ent,
                                                                  const double *__restrict__ val64,
-                                                                 const float *__restrict__ val32,
+                                                                 const float *__restrict__ val32, int ppw,
                                                                  double *__restrict__ inv, int *flag) {
   __shared__ double sA[kVankaWarps][32][33], sI[kVankaWarps][32][33];
   const int w = threadIdx.x >> 5, r = threadIdx.x & 31;
@@ -994,26 +1002,40 @@ __global__ void __launch_bounds__(32 * kVankaWarps) k_vanka_build(int64_t np, in
     return;
   }
   if (r < m)
-    for (int c = 0; c < m; ++c) inv[p * m * m + int64_t(c) * m + r] = I[r][c];
+    for (int c = 0; c < m; ++c) inv[vk_off(p, m, ppw, r, c)] = I[r][c];
 }
 
-// c_p = A_pp^{-1} r_p (r = b - A x, or b itself for a zero start).  Warp per patch.
+// c_p = A_pp^{-1} r_p (r = b - A x, or b itself for a zero start).  ppw =
+// 32 / m patches per warp (lane = sub * m + row), columns read as ppw*m
+// contiguous doubles, four columns' loads in flight before their use.
 template <int BS>
-__global__ void __launch_bounds__(kCta) k_vanka_patch(int64_t np, int nl, const int32_t *__restrict__ nodes,
+__global__ void __launch_bounds__(kCta) k_vanka_patch(int64_t np, int nl, int ppw, const int32_t *__restrict__ nodes,
                                                      const double *__restrict__ inv, const double *__restrict__ r,
                                                      double *__restrict__ cbuf) {
   const int lane = threadIdx.x & 31;
-  const int64_t p = int64_t(blockIdx.x) * kWarpsPerCta + (threadIdx.x >> 5);
-  if (p >= np) return;
   const int m = nl * BS;
-  const double rl = lane < m ? __ldg(r + int64_t(nodes[p * nl + lane / BS]) * BS + lane % BS) : 0.0;
-  const double *ip = inv + p * m * m;
+  const int sub = lane / m, row = lane - sub * m;
+  const int64_t p = (int64_t(blockIdx.x) * kWarpsPerCta + (threadIdx.x >> 5)) * ppw + sub;
+  const bool act = sub < ppw && p < np;
+  if ((int64_t(blockIdx.x) * kWarpsPerCta + (threadIdx.x >> 5)) * ppw >= np) return;
+  const double rl = act ? __ldg(r + int64_t(nodes[p * nl + row / BS]) * BS + row % BS) : 0.0;
+  const int base = sub * m;
+  const double *ip = inv + (act ? vk_off(p, m, ppw, row, 0) : 0);
+  const int64_t cs = int64_t(ppw) * m;  // column stride
   double acc = 0.0;
-  for (int j = 0; j < m; ++j) {
-    const double rj = __shfl_sync(0xffffffffu, rl, j);
-    if (lane < m) acc = fma(__ldcs(ip + int64_t(j) * m + lane), rj, acc);
+  int j = 0;
+  for (; j + 4 <= m; j += 4) {
+    double a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = act ? __ldcs(ip + (j + u) * cs) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc = fma(a[u], __shfl_sync(0xffffffffu, rl, (base + j + u) & 31), acc);
   }
-  if (lane < m) cbuf[p * m + lane] = acc;
+  for (; j < m; ++j) {
+    const double a = act ? __ldcs(ip + j * cs) : 0.0;
+    acc = fma(a, __shfl_sync(0xffffffffu, rl, (base + j) & 31), acc);
+  }
+  if (act) cbuf[p * m + row] = acc;
 }
 
 // x_i = (assign ? 0 : x_i) + omega w_i sum_{(p, a) in list(i)} c_p[a*BS + comp]; thread per DOF.

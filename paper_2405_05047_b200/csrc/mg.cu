@@ -188,7 +188,7 @@ struct Level {
   struct Vanka {
     bool on = false, ready = false;
     int64_t np = 0;
-    int nl = 0, m = 0;
+    int nl = 0, m = 0, ppw = 1;       // ppw = 32 / m patches per warp (inverse layout, mgk::vk_off)
     DevArray<int32_t> nodes;          // [np*nl] patch nodes (local rows)
     DevArray<int64_t> ent;            // [np*nl*nl] SELL entry of each block of A_pp (-1: absent)
     DevArray<double> inv;             // [np*m*m] A_pp^{-1}, column-major per patch
@@ -806,11 +806,11 @@ mg_status vanka_build(mg_ctx_s *c, int l) {
   const double *v64 = Pt.A.f32 ? nullptr : Pt.A.val.p;
   const float *v32 = Pt.A.f32 ? Pt.A.valf.p : nullptr;
   switch (bs) {
-    case 1: ++g_tally, mgk::k_vanka_build<1><<<g, 32 * mgk::kVankaWarps, 0, c->stream>>>(V.np, V.nl, V.ent.p, v64, v32, V.inv.p, flag.p); break;
-    case 2: ++g_tally, mgk::k_vanka_build<2><<<g, 32 * mgk::kVankaWarps, 0, c->stream>>>(V.np, V.nl, V.ent.p, v64, v32, V.inv.p, flag.p); break;
-    case 3: ++g_tally, mgk::k_vanka_build<3><<<g, 32 * mgk::kVankaWarps, 0, c->stream>>>(V.np, V.nl, V.ent.p, v64, v32, V.inv.p, flag.p); break;
-    case 4: ++g_tally, mgk::k_vanka_build<4><<<g, 32 * mgk::kVankaWarps, 0, c->stream>>>(V.np, V.nl, V.ent.p, v64, v32, V.inv.p, flag.p); break;
-    default: ++g_tally, mgk::k_vanka_build<6><<<g, 32 * mgk::kVankaWarps, 0, c->stream>>>(V.np, V.nl, V.ent.p, v64, v32, V.inv.p, flag.p); break;
+    case 1: ++g_tally, mgk::k_vanka_build<1><<<g, 32 * mgk::kVankaWarps, 0, c->stream>>>(V.np, V.nl, V.ent.p, v64, v32, V.ppw, V.inv.p, flag.p); break;
+    case 2: ++g_tally, mgk::k_vanka_build<2><<<g, 32 * mgk::kVankaWarps, 0, c->stream>>>(V.np, V.nl, V.ent.p, v64, v32, V.ppw, V.inv.p, flag.p); break;
+    case 3: ++g_tally, mgk::k_vanka_build<3><<<g, 32 * mgk::kVankaWarps, 0, c->stream>>>(V.np, V.nl, V.ent.p, v64, v32, V.ppw, V.inv.p, flag.p); break;
+    case 4: ++g_tally, mgk::k_vanka_build<4><<<g, 32 * mgk::kVankaWarps, 0, c->stream>>>(V.np, V.nl, V.ent.p, v64, v32, V.ppw, V.inv.p, flag.p); break;
+    default: ++g_tally, mgk::k_vanka_build<6><<<g, 32 * mgk::kVankaWarps, 0, c->stream>>>(V.np, V.nl, V.ent.p, v64, v32, V.ppw, V.inv.p, flag.p); break;
   }
   TRY(check_launch("vanka build"));
   int f = 0;
@@ -1143,13 +1143,14 @@ mg_status vanka_sweep(mg_ctx_s *c, int l, double *x, const double *b, bool zero)
     r = L.w.p;
   }
   if (V.np) {
-    const unsigned g = unsigned((V.np + mgk::kWarpsPerCta - 1) / mgk::kWarpsPerCta);
+    const int64_t warps = (V.np + V.ppw - 1) / V.ppw;
+    const unsigned g = unsigned((warps + mgk::kWarpsPerCta - 1) / mgk::kWarpsPerCta);
     switch (bs) {
-      case 1: ++g_tally, mgk::k_vanka_patch<1><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
-      case 2: ++g_tally, mgk::k_vanka_patch<2><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
-      case 3: ++g_tally, mgk::k_vanka_patch<3><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
-      case 4: ++g_tally, mgk::k_vanka_patch<4><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
-      default: ++g_tally, mgk::k_vanka_patch<6><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
+      case 1: ++g_tally, mgk::k_vanka_patch<1><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.ppw, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
+      case 2: ++g_tally, mgk::k_vanka_patch<2><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.ppw, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
+      case 3: ++g_tally, mgk::k_vanka_patch<3><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.ppw, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
+      case 4: ++g_tally, mgk::k_vanka_patch<4><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.ppw, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
+      default: ++g_tally, mgk::k_vanka_patch<6><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.ppw, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
     }
     TRY(check_launch("vanka patch"));
   }
@@ -1776,11 +1777,12 @@ mg_status mg_set_vanka(mg_ctx c, int level, int64_t n_patches, int nloc, const i
   nv.np = n_patches;
   nv.nl = nloc;
   nv.m = m;
+  nv.ppw = 32 / m;
   TRY(nv.nodes.upload(nodes32.data(), nodes32.size()));
   TRY(nv.nptr.upload(cnt.data(), cnt.size()));
   TRY(nv.nlist.upload(list.data(), list.size()));
   TRY(nv.wgt.upload(wgt.data(), wgt.size()));
-  TRY(nv.inv.alloc(size_t(n_patches) * m * m));
+  TRY(nv.inv.alloc(size_t((n_patches + nv.ppw - 1) / nv.ppw) * nv.ppw * m * m));  // whole groups (vk_off)
   TRY(nv.cbuf.alloc(size_t(n_patches) * m));
   V = std::move(nv);
   c->invalidate();
