@@ -640,7 +640,7 @@ def run_ns(args):
     P = NSP.build_ns("ns")
     log(f"[bench] generated ns: n_u {P.n_u}, n_p {P.n_p}, pressure levels {[L.n for L in P.pres_levels]} "
         f"in {time.time() - t:.1f}s")
-    g = mg.NavierStokes(P, rtol=1e-6, timing=True)
+    g = mg.NavierStokes(P, rtol=1e-6, timing=True, vanka=args.vanka, omega=args.omega or None)
     u, p, q = NSP.initial_state(P)
     g.set_state(u, p, q)
     stream = torch.cuda.current_stream()
@@ -674,6 +674,30 @@ def run_ns(args):
         uh, ph, qh = (np.ascontiguousarray(a) for a in g.get_state())
     e2e_s = time.perf_counter() - t0
     value = args.steps / (t_ms / 1e3)
+    # the same steps with the Vanka-type cell-patch smoother in the pressure MG
+    vk = None
+    if not args.vanka:
+        gv = mg.NavierStokes(P, rtol=1e-6, timing=True, vanka=True, omega=0.8)
+        gv.set_state(u, p, q)
+        for _ in range(args.warmup):
+            gv.step()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        vcomp, vits = np.zeros(4), 0
+        for _ in range(args.steps):
+            st, it, rel, conv, ms = gv.step()
+            vcomp += np.array(ms)
+            vits += it
+        e1.record(stream)
+        torch.cuda.synchronize()
+        v_ms = e0.elapsed_time(e1)
+        vk = {"value": args.steps / (v_ms / 1e3), "unit": "time steps/s", "ms_per_step": v_ms / args.steps,
+              "pressure_gmres_per_step": vits / args.steps,
+              "split_ms_per_step": dict(zip(("momentum", "pres-rhs", "pres-solve", "pres-up"),
+                                            (vcomp / args.steps).tolist())),
+              "note": "pressure MG smoothed by mg_set_vanka on the mesh cells, omega 0.8 (point Jacobi needs "
+                      "omega 0.4 on the graded mesh, reading Z27)"}
+        gv.close()
     cpu = None
     if not args.no_cpu_baseline:
         import oracle
@@ -697,9 +721,12 @@ def run_ns(args):
         "config": {"workload": WORKLOADS["ns"], "n_u": P.n_u, "n_p": P.n_p,
                    "pressure_levels": [L.n for L in P.pres_levels], "pressure_gmres_per_step": its / n,
                    "pressure_rtol": 1e-6, "parallelism": "single GPU",
+                   "pressure_smoother": ("Vanka (cell patches)" if args.vanka else "point Jacobi")
+                   + f", omega {args.omega or P.omega}",
                    "l2": "per-step operators ~0.6 GB > L2 126 MB"},
         "table_ns_split_ms_per_step": {"momentum": comp[0] / n, "pres-rhs": comp[1] / n, "pres-solve": comp[2] / n,
                                        "pres-up": comp[3] / n},
+        "vanka_pressure": vk,
         "paper_context": {"gpu_ms_per_step_h100": 41.5, "split_ms_per_step_h100": {
             "momentum": 5.78, "pres-rhs": 1.33, "pres-solve": 32.6, "pres-up": 1.81},
             "note": "Table ns GPU column / 40 000 steps (P:757-790); other hardware and code: context only"},
@@ -726,8 +753,8 @@ def main():
     ap.add_argument("--no-mixed", action="store_true", help="skip the mixed-precision side measurement")
     ap.add_argument("--precision", choices=["fp64", "mixed"], default="fp64",
                     help="mixed: fp32-stored V-cycle operators inside fp64 GMRES (SURVEY N1)")
-    ap.add_argument("--vanka", action="store_true", help="c4ns: Vanka-type cell-patch smoother (P:822)")
-    ap.add_argument("--omega", type=float, default=0.0, help="c4ns: smoother damping (0: config default)")
+    ap.add_argument("--vanka", action="store_true", help="c4ns / ns: Vanka-type cell-patch smoother (P:822)")
+    ap.add_argument("--omega", type=float, default=0.0, help="c4ns / ns: smoother damping (0: config default)")
     ap.add_argument("--min-rows-per-rank", type=int, default=16384,
                     help="multi-GPU: levels with fewer rows per rank are replicated (agglomerated)")
     args = ap.parse_args()

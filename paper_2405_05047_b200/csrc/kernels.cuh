@@ -870,6 +870,30 @@ __global__ void k_sub_mean(int64_t n, double *__restrict__ x, const double *__re
     x[i] = x[i] - coef * k[i];
 }
 
+// Small vectors (one CTA): x -= ((d^T x) / denom) k in a single launch -- the
+// global constraint's projection on coarse levels, where the two-kernel
+// path (grid reduction + update) is pure launch latency.  Fixed summation order.
+__global__ void __launch_bounds__(1024) k_mean_project_small(int64_t n, double *__restrict__ x,
+                                                            const double *__restrict__ d,
+                                                            const double *__restrict__ k, double denom) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(d[i], x[i], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) sh[0] = t;
+  }
+  __syncthreads();
+  const double coef = sh[0] / denom;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = x[i] - coef * k[i];
+}
+
 // Coarse regularisation A_0 + alpha w w^T, alpha = max_i |a_ii| / w_max^2 (reading
 // Z25): one block finds the largest diagonal magnitude, then the rank-1 update.
 __global__ void k_diag_absmax(int64_t N, int64_t ld, const double *__restrict__ a, double *out) {

@@ -1191,6 +1191,11 @@ mg_status smooth(mg_ctx_s *c, int l, double *x, const double *b, int k, bool zer
 mg_status mean_project(mg_ctx_s *c, int l, double *x, bool consist) {
   Level &L = c->lv[l];
   const int64_t n = L.n * c->bs();
+  if (!L.dist && n > 0 && n <= 16384) {  // one launch instead of dot + update
+    ++g_tally, mgk::k_mean_project_small<<<1, 1024, 0, c->stream>>>(n, x, consist ? L.mean_k.p : L.mean_w.p, L.mean_k.p,
+                                                                    consist ? L.mean_kk : L.mean_wk);
+    return check_launch("mean projection");
+  }
   TRY(dev_dot(c, L.dist, n, consist ? L.mean_k.p : L.mean_w.p, x, c->scal.p + 8, false));
   if (n == 0) return MG_OK;
   const unsigned g = unsigned(std::min<int64_t>((n + 255) / 256, 8 * c->n_sm));

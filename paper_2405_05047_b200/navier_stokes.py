@@ -15,9 +15,11 @@ class NavierStokes:
     Pi, G, m_u, m_p, dir_rows, dir_vals, nu, dt (e.g. problems.ns.NsProblem)."""
 
     def __init__(self, P, *, rtol=1e-6, restart=30, max_iter=200, timing=False, precision=0, use_graphs=True,
-                 device=0):
-        self.pressure = Multigrid(P.pres_levels, 1, omega=P.omega, coarse_mode=MG_COARSE_DIRECT, precision=precision,
-                                  use_graphs=use_graphs, device=device)
+                 device=0, vanka=False, omega=None):
+        """vanka: the pressure levels' cell patches (pres_levels[l].patches) smooth
+        with the Vanka-type patch smoother (mg_set_vanka) instead of Jacobi."""
+        self.pressure = Multigrid(P.pres_levels, 1, omega=omega if omega else P.omega, coarse_mode=MG_COARSE_DIRECT,
+                                  precision=precision, use_graphs=use_graphs, device=device, vanka=vanka)
         self.n_u, self.n_p = P.n_u, P.n_p
         self.ctx = ns_create(self.pressure.ctx, P.n_u, P.n_p)
         try:

@@ -218,6 +218,12 @@ def _pressure_level(xs, prev_xs):
     L.mean_w = np.kron(lumped1d(Mz), np.kron(lumped1d(My), lumped1d(Mx)))
     L.mean_k = np.ones(n)
     L.coords = xs
+    # cells of the tensor-product mesh (Vanka patches): 8 nodes, lexicographic ids
+    nx, ny, nz = (len(x) for x in xs)
+    I, J, K = np.meshgrid(np.arange(nx - 1), np.arange(ny - 1), np.arange(nz - 1), indexing="ij")
+    base = ((K * ny + J) * nx + I).ravel()
+    L.patches = np.stack([base + o for o in (0, 1, nx, nx + 1, nx * ny, nx * ny + 1, nx * ny + nx,
+                                             nx * ny + nx + 1)], axis=1).astype(np.int64)
     if prev_xs is not None:
         Pz, Py, Px = (interp1d(xs[a], prev_xs[a]) for a in (2, 1, 0))
         L.P = _csr(kron3(Pz, Py, Px))
