@@ -91,6 +91,8 @@ class ChannelLevel:
     mesh: M.Mesh = None
     nodes: M.NodeSet = None
     plan: tuple = None           # cached constraint plan of the level's pattern
+    static_val: np.ndarray = None  # cached values of the w-independent Stokes part
+    mass_val: np.ndarray = None    # finest level: cached velocity mass / dt
 
 
 @dataclass
@@ -202,20 +204,24 @@ def build_channel(name: str, uniform: int, band: int, K: int, *, omega=0.6, seed
 # --------------------------------------------------------------------------
 
 
-def _field_terms(P: ChannelProblem, CL: ChannelLevel, w_nodes: np.ndarray, newton: bool, lag_nodes=None):
-    """Element scales of the convection (and Newton) terms for the nodal velocity
-    field w_nodes (n, 2) of the level; streamline diffusion with the lagged
-    (previous time step) field lag_nodes: linear in w, so J stays the exact
-    derivative of F."""
+def _field_terms(P: ChannelProblem, CL: ChannelLevel, w_nodes: np.ndarray, newton: bool, lag_nodes=None,
+                 static: bool = True, convection: bool = True):
+    """Element terms (T, S) of the level operator for the nodal velocity field
+    w_nodes (n, 2): the static Stokes part (static), the Galerkin convection
+    (convection), streamline diffusion with the lagged (previous time step)
+    field lag_nodes -- linear in w, so J stays the exact derivative of F -- and
+    the Newton term (newton)."""
     vol = np.prod(CL.hsz, axis=1)
     we = w_nodes[CL.conn]                     # (n_e, 4, 2)
-    Sc = np.concatenate([we[:, :, a] * (vol / CL.hsz[:, a])[:, None] for a in range(2)], axis=1)
-    T = [CL.T_static, P.T_conv]
-    S = [CL.S_static, Sc]
+    T, S = [], []
+    if static:
+        T.append(CL.T_static)
+        S.append(CL.S_static)
+    if convection:
+        T.append(P.T_conv)
+        S.append(np.concatenate([we[:, :, a] * (vol / CL.hsz[:, a])[:, None] for a in range(2)], axis=1))
     if P.sd > 0.0 and lag_nodes is not None:
-        wb = lag_nodes[CL.conn].mean(axis=1)  # (n_e, 2) element mean of the lagged field
-        hT = CL.hsz.max(axis=1)
-        delta = P.sd / (1.0 / P.dt + np.hypot(wb[:, 0], wb[:, 1]) / hT + P.nu / hT ** 2)
+        wb, delta = _sd_delta(P, CL, lag_nodes)
         Ss = np.stack([delta * wb[:, a] * wb[:, b] * vol / (CL.hsz[:, a] * CL.hsz[:, b])
                        for a in range(2) for b in range(2)], axis=1)
         T.append(P.T_sd)
@@ -230,8 +236,7 @@ def _field_terms(P: ChannelProblem, CL: ChannelLevel, w_nodes: np.ndarray, newto
 
 def _assemble(CL: ChannelLevel, T, S):
     d = CL.data
-    rp, col, val = F.assemble_terms(CL.mesh, CL.nodes, T, S, 3, False, d.H)
-    assert np.array_equal(rp, d.row_ptr) and np.array_equal(col, d.col)
+    rp, col, val = F.assemble_terms(CL.mesh, CL.nodes, T, S, 3, False, d.H, row_ptr=d.row_ptr)
     return val
 
 
@@ -249,27 +254,74 @@ def full_field(P: ChannelProblem, w: np.ndarray) -> np.ndarray:
     return out
 
 
-def residual(P: ChannelProblem, w: np.ndarray, u_old: np.ndarray) -> np.ndarray:
-    """F(w) = A(w) w - M u_old/dt on the finest level (condensed), constrained rows 0.
-    w, u_old: (n, 3) full fields (hanging values interpolated, Dirichlet data imposed)."""
+def step_cache(P: ChannelProblem, u_old: np.ndarray) -> dict:
+    """What stays fixed within one time step: the w-independent Stokes part of
+    every level (assembled once per problem) and M u_old / dt on the finest level."""
+    for CL in P.levels:
+        if CL.static_val is None:
+            CL.static_val = _assemble(CL, CL.T_static, CL.S_static)
+            if CL is P.levels[-1]:
+                CL.mass_val = _assemble(CL, CL.T_mass, CL.S_mass)
     CL = P.levels[-1]
-    T, S = _field_terms(P, CL, w[:, 1:], newton=False, lag_nodes=u_old[:, 1:])
-    A = _assemble(CL, T, S)
-    Mv = _assemble(CL, CL.T_mass, CL.S_mass)
-    Fv = _bsr_mv(CL.data, A, w) - _bsr_mv(CL.data, Mv, u_old)
+    return {"Mu": _bsr_mv(CL.data, CL.mass_val, u_old), "u_old": u_old}
+
+
+def _sd_delta(P: ChannelProblem, CL: ChannelLevel, lag_nodes: np.ndarray):
+    wb = lag_nodes[CL.conn].mean(axis=1)      # (n_e, 2) element mean of the lagged field
+    hT = CL.hsz.max(axis=1)
+    return wb, P.sd / (1.0 / P.dt + np.hypot(wb[:, 0], wb[:, 1]) / hT + P.nu / hT ** 2)
+
+
+def _field_vector(P: ChannelProblem, w: np.ndarray, u_old: np.ndarray) -> np.ndarray:
+    """H^T [c(w; w, .) + sd(u_old; w, .)] on the finest level, element by element:
+    ((w . grad) w_c, phi_i) and sum_T delta_T (wb . grad w_c, wb . grad phi_i)_T with
+    the same integrals as the T_conv / T_sd terms."""
+    CL = P.levels[-1]
+    vol = np.prod(CL.hsz, axis=1)
+    we = w[CL.conn][:, :, 1:]                                      # (n_e, 4, 2)
+    ne = len(we)
+    C3 = conv_tensor()                                             # [a, k, i, j]
+    coef = we * (vol[:, None, None] / CL.hsz[:, None, :])          # w_{k,a} vol / h_a
+    Me = (coef.transpose(0, 2, 1).reshape(ne, 8) @ C3.reshape(8, 16)).reshape(ne, 4, 4)
+    if P.sd > 0.0:
+        _, G, _ = F.reference_tensors(2)
+        wb, delta = _sd_delta(P, CL, u_old[:, 1:])
+        cs = np.stack([delta * wb[:, a] * wb[:, b] * vol / (CL.hsz[:, a] * CL.hsz[:, b])
+                       for a in range(2) for b in range(2)], axis=1)
+        Me = Me + (cs @ G.reshape(4, 16)).reshape(ne, 4, 4)
+    loc = Me @ we                                                  # (n_e, 4, 2)
+    n = CL.data.n
+    full = np.stack([np.bincount(CL.conn.ravel(), loc[:, :, c].ravel(), minlength=n) for c in range(2)], 1)
+    rp, col, wt = CL.data.H
+    rows = F.row_of(rp)
+    cond = np.stack([np.bincount(col, wt * full[rows, c], minlength=n) for c in range(2)], 1)
+    out = np.zeros((n, 3))
+    out[:, 1:] = cond
+    return out
+
+
+def residual(P: ChannelProblem, w: np.ndarray, u_old: np.ndarray, cache: dict | None = None) -> np.ndarray:
+    """F(w) = A(w) w - M u_old/dt on the finest level (condensed), constrained rows 0:
+    the cached Stokes part times w plus the element-wise convection and
+    streamline-diffusion vector.
+    w, u_old: (n, 3) full fields (hanging values interpolated, Dirichlet data imposed)."""
+    cache = cache if cache is not None else step_cache(P, u_old)
+    CL = P.levels[-1]
+    Fv = _bsr_mv(CL.data, CL.static_val, w) + _field_vector(P, w, u_old).reshape(-1) - cache["Mu"]
     Fv = Fv.reshape(-1, 3)
     Fv[CL.data.cmask] = 0.0
     return Fv.reshape(-1)
 
 
-def jacobians(P: ChannelProblem, w: np.ndarray, u_old: np.ndarray, newton: bool = True):
+def jacobians(P: ChannelProblem, w: np.ndarray, u_old: np.ndarray, newton: bool = True, cache: dict | None = None):
     """Per level (coarse -> fine) the BSR values (nnzb, 3, 3) of J(w_l) (Newton) or
     A(w_l) (Picard), w_l = w injected, constraints applied (identity rows and
     eliminated columns, homogeneous: the Newton correction vanishes there)."""
+    cache = cache if cache is not None else step_cache(P, u_old)
     out = []
-    for CL in P.levels:
-        T, S = _field_terms(P, CL, w[CL.inject, 1:], newton, lag_nodes=u_old[CL.inject, 1:])
-        val = _assemble(CL, T, S)
+    for l, CL in enumerate(P.levels):
+        T, S = _field_terms(P, CL, w[CL.inject, 1:], newton, lag_nodes=u_old[CL.inject, 1:], static=False)
+        val = _assemble(CL, T, S) + CL.static_val
         if CL.plan is None:
             d = CL.data
             CL.plan = F.constraint_plan(d.row_ptr, d.col, d.cmask)
@@ -286,12 +338,14 @@ def initial_state(P: ChannelProblem) -> np.ndarray:
 def assemble_callback(P: ChannelProblem, u_old: np.ndarray):
     """The CPU side of one time step for the library's Newton driver
     (include/newton.h): fills F(w) and every level's Jacobian values."""
+    cache = step_cache(P, u_old)
+
     def asm(w, F, vals):
         W = np.asarray(w).reshape(-1, 3)
         if F is not None:
-            F[:] = residual(P, W, u_old)
+            F[:] = residual(P, W, u_old, cache)
         if vals is not None:
-            for l, v in enumerate(jacobians(P, W, u_old)):
+            for l, v in enumerate(jacobians(P, W, u_old, cache=cache)):
                 vals[l][:] = v.reshape(-1)
     return asm
 

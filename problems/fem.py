@@ -290,10 +290,12 @@ def assemble(mesh: M.Mesh, nodes: M.NodeSet, op: Operator, box, H):
     return assemble_terms(mesh, nodes, T, S, op.bs, op.symmetric, H)
 
 
-def assemble_terms(mesh: M.Mesh, nodes: M.NodeSet, T: np.ndarray, S: np.ndarray, bs: int, symmetric: bool, H):
+def assemble_terms(mesh: M.Mesh, nodes: M.NodeSet, T: np.ndarray, S: np.ndarray, bs: int, symmetric: bool, H,
+                   row_ptr=None):
     """Condensed BSR of the element matrices A_e = sum_t S[e, t] T_t (T (n_terms,
     nloc*bs, nloc*bs), S (n_e, n_terms)); the sparsity pattern depends on the
-    mesh connectivity only, never on the values."""
+    mesh connectivity only, never on the values (row_ptr: a known pattern's row
+    pointer skips the counting pass)."""
     N = len(nodes.keys)
     nloc = 1 << mesh.dim
     T = np.ascontiguousarray(T, np.float64)
@@ -301,11 +303,14 @@ def assemble_terms(mesh: M.Mesh, nodes: M.NodeSet, T: np.ndarray, S: np.ndarray,
     conn = np.ascontiguousarray(nodes.conn, np.int64)
     rp_h, col_h, w_h = (np.ascontiguousarray(a) for a in H)
     L = lib()
-    row_ptr = np.zeros(N + 1, np.int64)
-    rc = L.asm_condensed(N, bs, nloc, mesh.n_cells, ptr(conn), ptr(rp_h), ptr(col_h), ptr(w_h),
-                         T.shape[0], ptr(T), ptr(S), 0, 0, ptr(row_ptr), None, None)
-    if rc != 0:
-        raise RuntimeError("assembly pass 0 failed")
+    if row_ptr is None:
+        row_ptr = np.zeros(N + 1, np.int64)
+        rc = L.asm_condensed(N, bs, nloc, mesh.n_cells, ptr(conn), ptr(rp_h), ptr(col_h), ptr(w_h),
+                             T.shape[0], ptr(T), ptr(S), 0, 0, ptr(row_ptr), None, None)
+        if rc != 0:
+            raise RuntimeError("assembly pass 0 failed")
+    else:
+        row_ptr = np.array(row_ptr, np.int64)
     nnzb = int(row_ptr[-1])
     col = np.empty(nnzb, np.int64)
     val = np.empty((nnzb, bs, bs))

@@ -113,3 +113,69 @@ def test_inexact_newton_reuse_matches_oracle():
         assert abs(info["res_norm"][k] - nF) <= 1e-8 * F0 + 1e-6 * nF, (k, info, hist)
     assert np.linalg.norm(host(x).reshape(-1, 3) - w) <= 1e-8 * np.linalg.norm(w)
     g.close()
+
+
+def test_newton_distributed_local_ranks():
+    """mg_newton is collective: 2 LOCAL ranks (row partition, halo exchanges,
+    all-reduced norms) each assemble their own rows of F and of every level's
+    Jacobian (from the gathered iterate) and reach the oracle's Newton history."""
+    import os
+    import threading
+
+    import paper_2405_05047_b200 as m
+    from types import SimpleNamespace
+
+    from problems.partition import partition
+    P = prob("c4ns_mid")
+    u = C.initial_state(P)
+    levels0 = C.with_values(P, C.jacobians(P, u, u))
+    prob_ns = SimpleNamespace(levels=levels0, bs=3, b=np.zeros(P.n_dof), fine=levels0[-1])
+    parts, extras, ranges = partition(prob_ns, 2, min_rows_per_rank=64)
+    assert any(not L.replicated for L in parts[0])
+    key = os.urandom(16)
+    W = np.zeros((P.fine.n, 3))
+    bar = threading.Barrier(2, timeout=120)
+    out, errs = [None, None], []
+
+    def work(r):
+        import torch
+        torch.cuda.set_device(0)
+        try:
+            g = m.Multigrid(parts[r], 3, omega=P.omega, H=extras[r][1], comm=(2, r, key, m.MG_TRANSPORT_LOCAL))
+            f0, f1 = ranges[-1][r]
+
+            def asm(w, F, vals):
+                W[f0:f1] = np.asarray(w).reshape(-1, 3)
+                bar.wait()
+                if F is not None:
+                    F[:] = C.residual(P, W, u).reshape(-1, 3)[f0:f1].reshape(-1)
+                if vals is not None:
+                    for l, v in enumerate(C.jacobians(P, W, u)):
+                        a0, a1 = ranges[l][r]
+                        rp = P.levels[l].data.row_ptr
+                        vals[l][:] = v[rp[a0]:rp[a1]].reshape(-1)
+                bar.wait()
+
+            x = dev(u[f0:f1].reshape(-1))
+            st, info = g.newton(x, asm, max_newton=4, ntol=1e-8)
+            out[r] = (host(x).reshape(-1, 3), info)
+            g.close()
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+            bar.abort()
+    th = [threading.Thread(target=work, args=(r,)) for r in range(2)]
+    [t.start() for t in th]
+    [t.join(timeout=600) for t in th]
+    if errs:
+        raise errs[0]
+    w_o, hist = ON.newton_step(lambda v: C.with_values(P, v), lambda w: C.residual(P, w, u),
+                               lambda w: C.jacobians(P, w, u), P.fine.H, u, omega=P.omega, max_newton=4)
+    i0, i1 = out[0][1], out[1][1]
+    assert i0["converged"] and i0["res_norm"] == i1["res_norm"] and i0["lin_its"] == i1["lin_its"]
+    F0 = hist[0][0]
+    for k, (nF, its) in enumerate(hist):
+        assert abs(i0["res_norm"][k] - nF) <= 1e-8 * F0 + 1e-6 * nF, (k, i0, hist)
+        if k < i0["newton_its"]:
+            assert abs(i0["lin_its"][k] - its) <= 1, (k, i0, hist)
+    w = np.concatenate([out[0][0], out[1][0]])
+    assert np.linalg.norm(w - w_o) <= 1e-8 * np.linalg.norm(w_o)

@@ -150,3 +150,17 @@ def test_mesh_invariants():
     g = P.g
     inflow = P.xyz[:, 0] == 0.0
     assert np.isclose(g[inflow, 1].max(), C.U_MAX * (1 - (2 * np.min(np.abs(P.xyz[inflow, 1] - C.BOX[1] / 2)) / C.BOX[1]) ** 2))
+
+
+def test_elementwise_field_vector_equals_assembled_operator():
+    """The residual's element-wise vector H^T [c(w; w, .) + sd(u_old; w, .)] equals
+    the assembled convection + streamline-diffusion terms (condensed) times w."""
+    P = prob("c4ns_mid")
+    u_old, _ = perturbed_state(P, seed=4)
+    _, w = perturbed_state(P, seed=3)
+    CL = P.levels[-1]
+    T1, S1 = C._field_terms(P, CL, w[:, 1:], newton=False, lag_nodes=u_old[:, 1:], static=False)
+    A1 = bsr(CL.data, C._assemble(CL, T1, S1))
+    got = C._field_vector(P, w, u_old).reshape(-1)
+    exp = A1 @ w.reshape(-1)
+    assert np.abs(got - exp).max() <= 1e-13 * np.abs(exp).max()
