@@ -164,3 +164,25 @@ def test_elementwise_field_vector_equals_assembled_operator():
     got = C._field_vector(P, w, u_old).reshape(-1)
     exp = A1 @ w.reshape(-1)
     assert np.abs(got - exp).max() <= 1e-13 * np.abs(exp).max()
+
+
+def test_inexact_newton_reaches_the_same_solution():
+    """Jacobian reuse changes the path, not the fixed point F(w) = 0:
+    with reuse_rate 0.3 at least one Jacobian is kept, more Newton steps are
+    taken, and both iterations end at the same w."""
+    P = prob("c4ns_small")
+    u = C.initial_state(P)
+    built = []
+
+    def jac(w):
+        built.append(1)
+        return C.jacobians(P, w, u)
+    run = lambda r: ON.newton_step(lambda v: C.with_values(P, v), lambda w: C.residual(P, w, u), jac,  # noqa: E731
+                                   P.fine.H, u, omega=P.omega, max_newton=12, reuse_rate=r, ntol=1e-10)
+    w0, h0 = run(0.0)
+    n0 = len(built)
+    w1, h1 = run(0.3)
+    n1 = len(built) - n0
+    assert h0[-1][0] <= 1e-10 * h0[0][0] and h1[-1][0] <= 1e-10 * h1[0][0]
+    assert n1 < len(h1) - 1 and len(h1) >= len(h0)
+    assert np.linalg.norm(w1 - w0) <= 1e-8 * np.linalg.norm(w0)
