@@ -1155,7 +1155,7 @@ mg_status vanka_sweep(mg_ctx_s *c, int l, double *x, const double *b, bool zero)
     TRY(check_launch("vanka patch"));
   }
   if (L.n == 0) return MG_OK;
-  const unsigned g = unsigned(std::min<int64_t>((L.n * bs + 255) / 256, 16 * c->n_sm));
+  const unsigned g = unsigned(std::min<int64_t>((L.n + 255) / 256, 16 * c->n_sm));
   ++g_tally, mgk::k_vanka_update<<<g, 256, 0, c->stream>>>(L.n, bs, V.m, V.nptr.p, V.nlist.p, V.wgt.p, V.cbuf.p,
                                                             lv_omega(c, L), zero ? 1 : 0, x);
   return check_launch("vanka update");
@@ -1173,11 +1173,14 @@ mg_status smooth(mg_ctx_s *c, int l, double *x, const double *b, int k, bool zer
     for (int i = 0; i < k; ++i) TRY(vanka_sweep(c, l, x, b, zero && i == 0));
     return MG_OK;
   }
-  if (zero) {
-    for (int pi = 0; pi < L.nparts; ++pi) TRY(launch_sweep0(bs, L.part[pi].A, L.part[pi].dinv.p, b, x, om, c->stream));
-    --k;
-  }
   double *src = x, *dst = L.w.p;
+  if (zero) {
+    // the A-free first sweep lands where the remaining k-1 ping-pong sweeps end in x
+    // (no copy back)
+    --k;
+    if (k % 2) std::swap(src, dst);
+    for (int pi = 0; pi < L.nparts; ++pi) TRY(launch_sweep0(bs, L.part[pi].A, L.part[pi].dinv.p, b, src, om, c->stream));
+  }
   for (int i = 0; i < k; ++i) {
     TRY(a_pass_sweep(c, l, src, b, dst));
     std::swap(src, dst);

@@ -128,12 +128,31 @@ __global__ void __launch_bounds__(256) k_ns_div(int64_t n_p, const int64_t *__re
   const int64_t j = (int64_t(blockIdx.x) * 256 + threadIdx.x) >> 5;
   if (j >= n_p) return;
   double acc = 0.0;
-  for (int64_t e = rp[j] + lane; e < rp[j + 1]; e += 32) {
-    const int64_t c = __ldcs(col + e);
-    const double b0 = __ldcs(bv + 3 * e), b1 = __ldcs(bv + 3 * e + 1), b2 = __ldcs(bv + 3 * e + 2);
-    const double2 uv = ldg2(U + 4 * c);
-    const double u3 = __ldg(U + 4 * c + 2);
-    acc = fma(b2, u3, fma(b1, uv.y, fma(b0, uv.x, acc)));
+  const int64_t e1 = rp[j + 1];
+  int64_t e = rp[j] + lane;
+  constexpr int UB = 4;  // a row holds ~125 entries: all four strides' loads in flight at once
+  for (; e < e1; e += 32 * UB) {
+    int64_t c[UB];
+    double b0[UB], b1[UB], b2[UB];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const bool ok = e + 32 * u < e1;
+      const int64_t eu = ok ? e + 32 * u : e;  // clamped: every load stays inside the row
+      c[u] = __ldcs(col + eu);
+      const double z = ok ? 1.0 : 0.0;
+      b0[u] = z * __ldcs(bv + 3 * eu);
+      b1[u] = z * __ldcs(bv + 3 * eu + 1);
+      b2[u] = z * __ldcs(bv + 3 * eu + 2);
+    }
+    double2 uv[UB];
+    double u3[UB];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      uv[u] = ldg2(U + 4 * c[u]);
+      u3[u] = __ldg(U + 4 * c[u] + 2);
+    }
+#pragma unroll
+    for (int u = 0; u < UB; ++u) acc = fma(b2[u], u3[u], fma(b1[u], uv[u].y, fma(b0[u], uv[u].x, acc)));
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
