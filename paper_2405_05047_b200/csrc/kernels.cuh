@@ -1052,34 +1052,29 @@ __global__ void __launch_bounds__(kCta) k_vanka_patch(int64_t np, int nl, int pp
   const double *ip = inv + vk_off(pc, m, ppw, rc, 0);
   const int64_t cs = int64_t(ppw) * m;  // column stride
   double acc = 0.0;
-  for (int j = 0; j < m; j += 8) {  // eight columns' loads in flight per lane
-    double a[8];
+  int j = 0;
+  for (; j + 4 <= m; j += 4) {  // four columns' loads in flight per lane
+    double a[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) a[u] = __ldcs(ip + (j + u < m ? j + u : m - 1) * cs);
+    for (int u = 0; u < 4; ++u) a[u] = __ldcs(ip + (j + u) * cs);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const double rj = __shfl_sync(0xffffffffu, rl, (base + j + u) & 31);
-      if (j + u < m) acc = fma(a[u], rj, acc);
-    }
+    for (int u = 0; u < 4; ++u) acc = fma(a[u], __shfl_sync(0xffffffffu, rl, (base + j + u) & 31), acc);
   }
+  for (; j < m; ++j) acc = fma(__ldcs(ip + j * cs), __shfl_sync(0xffffffffu, rl, (base + j) & 31), acc);
   if (act) cbuf[p * m + row] = acc;
 }
 
-// x_i = (assign ? 0 : x_i) + omega w_i sum_{(p, a) in list(i)} c_p[a*bs .. a*bs+bs-1];
-// thread per node (the list is read once for all bs components).
+// x_i = (assign ? 0 : x_i) + omega w_i sum_{(p, a) in list(i)} c_p[a*BS + comp]; thread per DOF.
 __global__ void k_vanka_update(int64_t n, int bs, int m, const int64_t *__restrict__ nptr,
                                const int64_t *__restrict__ nlist, const double *__restrict__ wgt,
                                const double *__restrict__ cbuf, double omega, int assign, double *__restrict__ x) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    double s[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    const int64_t q1 = nptr[i + 1];
-    for (int64_t q = nptr[i]; q < q1; ++q) {
-      const double *cp = cbuf + __ldg(nlist + q);
-      for (int c = 0; c < bs; ++c) s[c] += __ldg(cp + c);
-    }
-    const double f = omega * wgt[i];
-    double *xi = x + i * bs;
-    for (int c = 0; c < bs; ++c) xi[c] = assign ? f * s[c] : xi[c] + f * s[c];
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n * bs; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = t / bs;
+    const int comp = int(t % bs);
+    double s = 0.0;
+    for (int64_t q = nptr[i]; q < nptr[i + 1]; ++q) s += __ldg(cbuf + nlist[q] + comp);
+    const double upd = omega * (wgt[i] * s);
+    x[t] = assign ? upd : x[t] + upd;
   }
   (void)m;
 }

@@ -1155,7 +1155,7 @@ mg_status vanka_sweep(mg_ctx_s *c, int l, double *x, const double *b, bool zero)
     TRY(check_launch("vanka patch"));
   }
   if (L.n == 0) return MG_OK;
-  const unsigned g = unsigned(std::min<int64_t>((L.n + 255) / 256, 16 * c->n_sm));
+  const unsigned g = unsigned(std::min<int64_t>((L.n * bs + 255) / 256, 16 * c->n_sm));
   ++g_tally, mgk::k_vanka_update<<<g, 256, 0, c->stream>>>(L.n, bs, V.m, V.nptr.p, V.nlist.p, V.wgt.p, V.cbuf.p,
                                                             lv_omega(c, L), zero ? 1 : 0, x);
   return check_launch("vanka update");
