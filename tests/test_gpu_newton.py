@@ -179,3 +179,28 @@ def test_newton_distributed_local_ranks():
             assert abs(i0["lin_its"][k] - its) <= 1, (k, i0, hist)
     w = np.concatenate([out[0][0], out[1][0]])
     assert np.linalg.norm(w - w_o) <= 1e-8 * np.linalg.norm(w_o)
+
+
+def test_newton_edge_cases():
+    """max_newton = 0 only evaluates ||F_0||; an exception in the callback aborts
+    the iteration and is re-raised; bad options are rejected."""
+    import paper_2405_05047_b200 as m
+    P = prob("c4ns_small")
+    u = C.initial_state(P)
+    g = gpu_solver(P, u, u)
+    x = dev(u.reshape(-1))
+    st, info = g.newton(x, C.assemble_callback(P, u), max_newton=0)
+    assert st == m.MG_NOT_CONVERGED and info["newton_its"] == 0
+    assert abs(info["res_norm"][0] - np.linalg.norm(C.residual(P, u, u))) <= 1e-12 * info["res_norm"][0]
+    assert np.array_equal(host(x), u.reshape(-1))                      # untouched
+
+    def bad(w, F, vals):
+        raise ValueError("assembly failed")
+    with pytest.raises(ValueError):
+        g.newton(x, bad)
+    with pytest.raises(m.MgError):
+        g.newton(x, C.assemble_callback(P, u), max_newton=-1)
+    # the context is still usable afterwards
+    st, info = g.newton(x, C.assemble_callback(P, u), max_newton=4)
+    assert info["converged"]
+    g.close()
