@@ -470,6 +470,13 @@ def run_ours(args):
         cpu["threads_scan_vcycles_per_s"] = scan
         import oracle
         oracle.set_threads(cores)
+        # time-to-1e-10 of the oracle's GMRES(30) + V(2,2) on the same system
+        if not args.no_cpu_solve:
+            h = _ORACLE_H[id(P)]
+            t = time.perf_counter()
+            _, o_its, _, o_rel = oracle.gmres(h, P.b, rtol=args.rtol)
+            cpu["solve"] = {"seconds": time.perf_counter() - t, "iterations": o_its, "rel_residual": o_rel,
+                            "dofs_per_s": P.n_dof / (time.perf_counter() - t)}
 
     if rank == 0:
         line = {
@@ -768,6 +775,7 @@ def main():
     ap.add_argument("--config", choices=sorted(WORKLOADS), default="c3")
     ap.add_argument("--rtol", type=float, default=1e-10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-solve", action="store_true", help="skip the oracle's full GMRES solve in cpu_baseline")
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--no-mixed", action="store_true", help="skip the mixed-precision side measurement")
     ap.add_argument("--precision", choices=["fp64", "mixed"], default="fp64",

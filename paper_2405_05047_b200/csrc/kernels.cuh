@@ -1029,6 +1029,17 @@ __global__ void __launch_bounds__(32 * kVankaWarps) k_vanka_build(int64_t np, in
     for (int c = 0; c < m; ++c) inv[vk_off(p, m, ppw, r, c)] = I[r][c];
 }
 
+// Predicated evict-first load: lanes with !pred issue no access at all (volatile
+// asm with an explicit predicate: the compiler cannot if-convert it into an
+// unconditional load) and return 0.
+__device__ __forceinline__ double ldcs_if(const double *p, bool pred) {
+  double v = 0.0;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.cs.f64 %0, [%1];\n\t}"
+               : "+d"(v)
+               : "l"(p), "r"(int(pred)));
+  return v;
+}
+
 // c_p = A_pp^{-1} r_p (r = b - A x, or b itself for a zero start).  ppw =
 // 32 / m patches per warp (lane = sub * m + row), columns read as ppw*m
 // contiguous doubles, four columns' loads in flight before their use.
@@ -1043,11 +1054,11 @@ __global__ void __launch_bounds__(kCta) k_vanka_patch(int64_t np, int nl, int pp
   const bool act = sub < ppw && p < np;
   const int64_t p0 = (int64_t(blockIdx.x) * kWarpsPerCta + (threadIdx.x >> 5)) * ppw;
   if (p0 >= np) return;
-  // Inactive lanes work on the warp's first patch / row 0 (clamped indices, results
-  // discarded): every load is in bounds even if the compiler if-converts them.
+  // Inactive lanes use the warp's first patch / row 0 for their (never issued)
+  // addresses; their loads are predicated off.
   const int64_t pc = act ? p : p0;
   const int rc = act ? row : 0;
-  const double rl = __ldg(r + int64_t(nodes[pc * nl + rc / BS]) * BS + rc % BS);
+  const double rl = act ? __ldg(r + int64_t(nodes[pc * nl + rc / BS]) * BS + rc % BS) : 0.0;
   const int base = sub * m;
   const double *ip = inv + vk_off(pc, m, ppw, rc, 0);
   const int64_t cs = int64_t(ppw) * m;  // column stride
@@ -1056,11 +1067,11 @@ __global__ void __launch_bounds__(kCta) k_vanka_patch(int64_t np, int nl, int pp
   for (; j + 4 <= m; j += 4) {  // four columns' loads in flight per lane
     double a[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) a[u] = __ldcs(ip + (j + u) * cs);
+    for (int u = 0; u < 4; ++u) a[u] = ldcs_if(ip + (j + u) * cs, act);
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc = fma(a[u], __shfl_sync(0xffffffffu, rl, (base + j + u) & 31), acc);
   }
-  for (; j < m; ++j) acc = fma(__ldcs(ip + j * cs), __shfl_sync(0xffffffffu, rl, (base + j) & 31), acc);
+  for (; j < m; ++j) acc = fma(ldcs_if(ip + j * cs, act), __shfl_sync(0xffffffffu, rl, (base + j) & 31), acc);
   if (act) cbuf[p * m + row] = acc;
 }
 
