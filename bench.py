@@ -50,6 +50,9 @@ WORKLOADS = {
     "ns": "N2: the paper's explicit pressure-correction Navier-Stokes step (Alg. 2) on its 3D driven cavity "
           "(0,1)^2x(0,2), graded 32x32x64 pressure mesh (Q1, 70,785 nodes) and Q1-iso-Q2 velocity (545,025 "
           "nodes), Re 1000, dt 1e-4, pressure Poisson GMRES+MG with int p = 0 to rtol 1e-6",
+    "td_l10": "the paper's transport-diffusion case L10 (P:402-405): uniform 1024x1024 Q1 mesh of the unit square, "
+              "1,050,625 DOFs, M^l/dt + lambda K + B (lambda 0.01, b = (0,-1), dt 0.02), 9 levels, GMRES(30)+V(2,2) "
+              "Jacobi omega 0.8, direct coarse solve",
     "c5": "C5: 3D NS-shaped generalised Stokes (PSPG, eps M_p), Q1 4x4 blocks (p,u,v,w), (0,1)^2x(0,2) cavity, "
           "128x128x256 cells, 6 levels, per-component transfers, GMRES(30)+V(2,2) omega=0.6",
     "pres": "N2: pure-Neumann pressure Poisson of the projection step (Alg. 2 Step 2, P:618-636) on the NS cavity "
@@ -67,6 +70,15 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+# the paper's own numbers for the same workload (other hardware and code: context)
+PAPER_CONTEXT = {
+    "td_l10": {"gpu_ms_per_solve_h100": 90.0, "cpu_ms_per_solve_8threads": 3047.5,
+               "source": "P:405: 9.0 s (GPU) / 304.75 s (CPU) per 100 time steps = 100 linear solves"},
+    "e6": {"gpu_ms_per_solve_h100": 1225.7, "cpu_ms_per_solve_8threads": 44319.4,
+           "source": "P:537: 122.57 s (GPU) / 4431.94 s (CPU) per 100 time steps"},
+}
 
 
 def measured_peaks():
@@ -505,6 +517,7 @@ def run_ours(args):
                               + prof["agglomeration_ms"],
                               "halo_ms": prof["halo_ms"], "agglomeration_ms": prof["agglomeration_ms"],
                               "note": "one eager V(2,2) from zero, CUDA events between phases"},
+            "paper_context": PAPER_CONTEXT.get(args.config),
             "mixed_precision": mixed,
             "update_matrix": upd,
             "vcycle_only": {"ms": vc_ms, "per_s": 1e3 / vc_ms, "batch_ms": batches,

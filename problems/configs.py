@@ -219,6 +219,10 @@ CONFIGS = {
     # name: (root, box, steps, operator, omega, seed index)
     "c1": ((4, 4), (1.0, 1.0), [("uniform",)] * 3, F.Operator("td", 1, False, TD), 0.8, 0),
     "c1_poisson": ((4, 4), (1.0, 1.0), [("uniform",)] * 3, F.Operator("poisson", 1, True), 0.8, 0),
+    # the paper's transport-diffusion table: uniform Q1 meshes L7..L10 of the unit
+    # square, (2^L + 1)^2 nodes; td_l10 = 1,050,625 DOFs (the "about 34x" case)
+    "td_l7": ((4, 4), (1.0, 1.0), [("uniform",)] * 5, F.Operator("td", 1, False, TD), 0.8, 8),
+    "td_l10": ((4, 4), (1.0, 1.0), [("uniform",)] * 8, F.Operator("td", 1, False, TD), 0.8, 8),
     "c2": ((32, 32), (1.0, 1.0), [("band", [1], 20)] * 7, F.Operator("td", 1, False, TD), 0.8, 1),
     "c3": ((9, 9, 9), (1.0, 1.0, 1.0), [("band", [0], 1)] * 6,
            F.Operator("elasticity", 3, True, ELAST), 0.5, 2),
