@@ -79,6 +79,16 @@ struct SellOp {
   mgk::Sell view() const { return mgk::Sell{slice_ptr.p, perm.p, col.p, val.p, n_slices, valf.p}; }
 };
 
+// Operators above this size are read with evict-first loads (MGB200_STREAM_MB overrides
+// the default kStreamBytes; experiment knob for L2 residency of mid-sized operators).
+size_t stream_bytes() {
+  static const size_t v = [] {
+    const char *e = std::getenv("MGB200_STREAM_MB");
+    return e && *e ? size_t(std::atoll(e)) << 20 : kStreamBytes;
+  }();
+  return v;
+}
+
 // Build SELL-32-sigma on the host and upload it (col: LOCAL column indices);
 // f32: values rounded to fp32 in the fp32 chunk layout.
 mg_status build_sell(SellOp &op, int64_t n, const int64_t *rp, const int64_t *col, const double *val, int vpe,
@@ -114,7 +124,7 @@ mg_status build_sell(SellOp &op, int64_t n, const int64_t *rp, const int64_t *co
   op.n_entries = ne;
   op.vpe = vpe;
   op.f32 = f32;
-  op.stream = size_t(ne) * ((f32 ? 4 : 8) * vpe + 4) > kStreamBytes;
+  op.stream = size_t(ne) * ((f32 ? 4 : 8) * vpe + 4) > stream_bytes();
   op.set = true;
   return MG_OK;
 }
