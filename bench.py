@@ -50,6 +50,10 @@ WORKLOADS = {
     "ns": "N2: the paper's explicit pressure-correction Navier-Stokes step (Alg. 2) on its 3D driven cavity "
           "(0,1)^2x(0,2), graded 32x32x64 pressure mesh (Q1, 70,785 nodes) and Q1-iso-Q2 velocity (545,025 "
           "nodes), Re 1000, dt 1e-4, pressure Poisson GMRES+MG with int p = 0 to rtol 1e-6",
+    "e6_edge": "N4: the paper's 6-component elasticity (u, v) on Table ndofs edge mesh L6 (8^3 root, K=1 band toward "
+               "x=y=0): 209,910 DOFs as in P:554, GMRES(30)+V(2,2) block-Jacobi omega=0.5",
+    "e6_vertex": "N4: the paper's 6-component elasticity (u, v) on Table ndofs vertex mesh L6 (band toward the vertex "
+                 "0): 22,494 DOFs as in P:571, GMRES(30)+V(2,2) block-Jacobi omega=0.5",
     "td_l10": "the paper's transport-diffusion case L10 (P:402-405): uniform 1024x1024 Q1 mesh of the unit square, "
               "1,050,625 DOFs, M^l/dt + lambda K + B (lambda 0.01, b = (0,-1), dt 0.02), 9 levels, GMRES(30)+V(2,2) "
               "Jacobi omega 0.8, direct coarse solve",
@@ -76,6 +80,10 @@ def dist_env():
 PAPER_CONTEXT = {
     "td_l10": {"gpu_ms_per_solve_h100": 90.0, "cpu_ms_per_solve_8threads": 3047.5,
                "source": "P:405: 9.0 s (GPU) / 304.75 s (CPU) per 100 time steps = 100 linear solves"},
+    "e6_edge": {"gpu_ms_per_solve_h100": 147.0, "cpu_ms_per_solve_8threads": 3055.8,
+                "source": "P:554: 14.7 s (GPU) / 305.58 s (CPU) per 100 time steps"},
+    "e6_vertex": {"gpu_ms_per_solve_h100": 79.0, "cpu_ms_per_solve_8threads": 282.1,
+                  "source": "P:571: 7.9 s (GPU) / 28.21 s (CPU) per 100 time steps"},
     "e6": {"gpu_ms_per_solve_h100": 1225.7, "cpu_ms_per_solve_8threads": 44319.4,
            "source": "P:537: 122.57 s (GPU) / 4431.94 s (CPU) per 100 time steps"},
 }
@@ -164,7 +172,8 @@ def vcycle_bytes(infos, bs, nu=(2, 2), zero=True, coarse_direct=True, vb=8):
 def build_problem(name):
     from problems import configs
     t = time.time()
-    P = configs.build({"e6": "e6_face_l5", "pres": "pres_l5"}.get(name, name), keep_geometry=False)
+    P = configs.build({"e6": "e6_face_l5", "e6_edge": "e6_edge_l6", "e6_vertex": "e6_vertex_l6",
+                       "pres": "pres_l5"}.get(name, name), keep_geometry=False)
     log(f"[bench] generated {name}: {P.n_dof} DOFs, levels {[l.n for l in P.levels]} in {time.time() - t:.1f}s")
     return P
 

@@ -246,6 +246,12 @@ CONFIGS.update({
                    F.Operator("elasticity6", 6, False, ELAST), 0.5, 5),
     "e6_face_l5": ((8, 8, 8), (1.0, 1.0, 1.0), [("band", [0], 1)] * 4,
                    F.Operator("elasticity6", 6, False, ELAST), 0.5, 5),
+    # Table `ndofs` edge and vertex patterns, L6: band toward the edge x = y = 0 /
+    # the vertex 0 (reading Z16): 34,985 / 3,749 nodes = 209,910 / 22,494 DOFs
+    "e6_edge_l6": ((8, 8, 8), (1.0, 1.0, 1.0), [("band", [0, 1], 1)] * 5,
+                   F.Operator("elasticity6", 6, False, ELAST), 0.5, 5),
+    "e6_vertex_l6": ((8, 8, 8), (1.0, 1.0, 1.0), [("band", [0, 1, 2], 1)] * 5,
+                     F.Operator("elasticity6", 6, False, ELAST), 0.5, 5),
     # C4: 2D NS-shaped generalised Stokes, 3x3 blocks (p, u, v), lid cavity, band toward the lid
     "c4": ((32, 32), (1.0, 1.0), [("band", [1], 20)] * 6, F.Operator("stokes", 3, False, STOKES2), 0.8, 3),
     "c4_small": ((8, 8), (1.0, 1.0), [("band", [1], 2)] * 3, F.Operator("stokes", 3, False, STOKES2), 0.8, 3),

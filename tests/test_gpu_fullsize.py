@@ -141,7 +141,7 @@ def test_fullsize_gmres_converges(name):
     assert rn <= 2e-10 * np.linalg.norm(P.b)
 
 
-@pytest.mark.parametrize("name", ["c2", "c4", "td_l10"])
+@pytest.mark.parametrize("name", ["c2", "c4", "td_l10", "e6_edge_l6", "e6_vertex_l6"])
 def test_fullsize_gmres_iterations_match_oracle(name):
     import paper_2405_05047_b200 as m
     P, mg = full(name)

@@ -14,10 +14,11 @@ from problems import mesh as M
 import oracle
 
 
-@pytest.mark.parametrize("name,dofs", [("e6_face_l2", 17550), ("e6_face_l3", 67686)])
+@pytest.mark.parametrize("name,dofs", [("e6_face_l2", 17550), ("e6_face_l3", 67686), ("e6_edge_l6", 209910),
+                                       ("e6_vertex_l6", 22494)])
 def test_dof_counts_match_paper_table(name, dofs):
     P = configs.build(name)
-    assert P.n_dof == dofs and P.bs == 6            # P:534, P:535
+    assert P.n_dof == dofs and P.bs == 6            # P:534, P:535, P:554, P:571
 
 
 def test_face_l5_dof_count_matches_paper():
