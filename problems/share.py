@@ -76,30 +76,42 @@ def remove(directory: str) -> None:
     shutil.rmtree(directory, ignore_errors=True)
 
 
+def _nbytes(obj) -> int:
+    arrays: list = []
+    _strip(obj, arrays, {})
+    return sum(a.nbytes for a in arrays)
+
+
 def shared_build(build, tag: str, rank: int, barrier, broadcast_token, base: str | None = None):
     """build(): the generator call (rank 0 only).  barrier(): a collective barrier;
     broadcast_token(tok or None) -> tok: a collective broadcast of a small string
-    from rank 0.  Returns (problem, cleanup) -- call cleanup() collectively once
-    every rank has taken what it needs."""
-    base = base or ("/dev/shm" if os.path.isdir("/dev/shm") and os.access("/dev/shm", os.W_OK) else None)
+    from rank 0.  Rank 0 writes to the first of (base, /dev/shm, the temp dir) with
+    room for the arrays; if none has room every rank builds its own copy.
+    Returns (problem, cleanup) -- call cleanup() collectively once every rank has
+    taken what it needs."""
     import tempfile
-    base = base or tempfile.gettempdir()
-    tok = broadcast_token(f"{tag}-{os.getpid()}-{os.urandom(4).hex()}" if rank == 0 else None)
-    directory = os.path.join(base, f"mgb200_{tok}")
+    directory = None
     if rank == 0:
         P = build()
-        try:
-            dump(P, directory)
-            ok = "ok"
-        except OSError as e:  # no space: every rank builds its own copy
-            remove(directory)
-            ok = f"fail:{e}"
-    status = broadcast_token(ok if rank == 0 else None)
+        need = _nbytes(P) + (64 << 20)
+        for cand in (base, "/dev/shm", tempfile.gettempdir()):
+            if not cand or not os.path.isdir(cand) or not os.access(cand, os.W_OK):
+                continue
+            if shutil.disk_usage(cand).free < need:
+                continue
+            directory = os.path.join(cand, f"mgb200_{tag}_{os.getpid()}_{os.urandom(4).hex()}")
+            try:
+                dump(P, directory)
+                break
+            except OSError:
+                remove(directory)
+                directory = None
+    directory = broadcast_token(directory if rank == 0 else None)
     if rank != 0:
-        P = load(directory) if status == "ok" else build()
+        P = load(directory) if directory else build()
 
     def cleanup():
         barrier()
-        if rank == 0:
+        if rank == 0 and directory:
             remove(directory)
     return P, cleanup
