@@ -141,7 +141,6 @@ def build_channel(name: str, uniform: int, band: int, K: int, *, omega=0.6, seed
     Mref, G, _ = F.reference_tensors(2)
     T_sd = np.stack([sum(_blk(G[a, b], 1 + c, 1 + c) for c in range(2)) for a in range(2) for b in range(2)])
     T_mass = np.stack([sum(_blk(Mref, c, c) for c in range(1, 3))])
-    fine_nodes = None
     levels = []
     prev = None
     scale = np.array([BOX[a] / (ROOT[a] << R) for a in range(2)])
