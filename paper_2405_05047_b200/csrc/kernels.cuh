@@ -1042,36 +1042,50 @@ __device__ __forceinline__ double ldcs_if(const double *p, bool pred) {
 
 // c_p = A_pp^{-1} r_p (r = b - A x, or b itself for a zero start).  ppw =
 // 32 / m patches per warp (lane = sub * m + row), columns read as ppw*m
-// contiguous doubles, four columns' loads in flight before their use.
-template <int BS>
-__global__ void __launch_bounds__(kCta) k_vanka_patch(int64_t np, int nl, int ppw, const int32_t *__restrict__ nodes,
+// contiguous doubles.  NL > 0: patch size known at compile time -> all m
+// column loads of a lane in flight before the first use (the kernel is
+// latency bound otherwise); NL = 0: runtime nl, four columns at a time.
+template <int BS, int NL>
+__global__ void __launch_bounds__(kCta) k_vanka_patch(int64_t np, int nl_rt, int ppw, const int32_t *__restrict__ nodes,
                                                      const double *__restrict__ inv, const double *__restrict__ r,
                                                      double *__restrict__ cbuf) {
   const int lane = threadIdx.x & 31;
+  const int nl = NL > 0 ? NL : nl_rt;
   const int m = nl * BS;
   const int sub = lane / m, row = lane - sub * m;
-  const int64_t p = (int64_t(blockIdx.x) * kWarpsPerCta + (threadIdx.x >> 5)) * ppw + sub;
-  const bool act = sub < ppw && p < np;
   const int64_t p0 = (int64_t(blockIdx.x) * kWarpsPerCta + (threadIdx.x >> 5)) * ppw;
+  const int64_t p = p0 + sub;
+  const bool act = sub < ppw && p < np;
   if (p0 >= np) return;
   // Inactive lanes use the warp's first patch / row 0 for their (never issued)
   // addresses; their loads are predicated off.
   const int64_t pc = act ? p : p0;
   const int rc = act ? row : 0;
-  const double rl = act ? __ldg(r + int64_t(nodes[pc * nl + rc / BS]) * BS + rc % BS) : 0.0;
-  const int base = sub * m;
   const double *ip = inv + vk_off(pc, m, ppw, rc, 0);
   const int64_t cs = int64_t(ppw) * m;  // column stride
   double acc = 0.0;
-  int j = 0;
-  for (; j + 4 <= m; j += 4) {  // four columns' loads in flight per lane
-    double a[4];
+  if constexpr (NL > 0) {
+    constexpr int M = NL * BS;
+    double a[M];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) a[u] = ldcs_if(ip + (j + u) * cs, act);
+    for (int j = 0; j < M; ++j) a[j] = ldcs_if(ip + j * cs, act);
+    const double rl = act ? __ldg(r + int64_t(nodes[pc * NL + rc / BS]) * BS + rc % BS) : 0.0;
+    const int base = sub * M;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc = fma(a[u], __shfl_sync(0xffffffffu, rl, (base + j + u) & 31), acc);
+    for (int j = 0; j < M; ++j) acc = fma(a[j], __shfl_sync(0xffffffffu, rl, (base + j) & 31), acc);
+  } else {
+    const double rl = act ? __ldg(r + int64_t(nodes[pc * nl + rc / BS]) * BS + rc % BS) : 0.0;
+    const int base = sub * m;
+    int j = 0;
+    for (; j + 4 <= m; j += 4) {  // four columns' loads in flight per lane
+      double a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = ldcs_if(ip + (j + u) * cs, act);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc = fma(a[u], __shfl_sync(0xffffffffu, rl, (base + j + u) & 31), acc);
+    }
+    for (; j < m; ++j) acc = fma(ldcs_if(ip + j * cs, act), __shfl_sync(0xffffffffu, rl, (base + j) & 31), acc);
   }
-  for (; j < m; ++j) acc = fma(ldcs_if(ip + j * cs, act), __shfl_sync(0xffffffffu, rl, (base + j) & 31), acc);
   if (act) cbuf[p * m + row] = acc;
 }
 

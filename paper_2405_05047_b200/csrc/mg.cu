@@ -1155,13 +1155,29 @@ mg_status vanka_sweep(mg_ctx_s *c, int l, double *x, const double *b, bool zero)
   if (V.np) {
     const int64_t warps = (V.np + V.ppw - 1) / V.ppw;
     const unsigned g = unsigned((warps + mgk::kWarpsPerCta - 1) / mgk::kWarpsPerCta);
-    switch (bs) {
-      case 1: ++g_tally, mgk::k_vanka_patch<1><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.ppw, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
-      case 2: ++g_tally, mgk::k_vanka_patch<2><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.ppw, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
-      case 3: ++g_tally, mgk::k_vanka_patch<3><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.ppw, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
-      case 4: ++g_tally, mgk::k_vanka_patch<4><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.ppw, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
-      default: ++g_tally, mgk::k_vanka_patch<6><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.ppw, V.nodes.p, V.inv.p, r, V.cbuf.p); break;
+#define VK_PATCH(B, N) mgk::k_vanka_patch<B, N><<<g, mgk::kCta, 0, c->stream>>>(V.np, V.nl, V.ppw, V.nodes.p, V.inv.p, r, V.cbuf.p)
+    const int key = bs * 100 + V.nl;  // compile-time patch sizes for mesh cells (4 / 8 nodes)
+    ++g_tally;
+    switch (key) {
+      case 104: VK_PATCH(1, 4); break;
+      case 108: VK_PATCH(1, 8); break;
+      case 204: VK_PATCH(2, 4); break;
+      case 208: VK_PATCH(2, 8); break;
+      case 304: VK_PATCH(3, 4); break;
+      case 308: VK_PATCH(3, 8); break;
+      case 404: VK_PATCH(4, 4); break;
+      case 408: VK_PATCH(4, 8); break;
+      case 604: VK_PATCH(6, 4); break;
+      default:
+        switch (bs) {
+          case 1: VK_PATCH(1, 0); break;
+          case 2: VK_PATCH(2, 0); break;
+          case 3: VK_PATCH(3, 0); break;
+          case 4: VK_PATCH(4, 0); break;
+          default: VK_PATCH(6, 0); break;
+        }
     }
+#undef VK_PATCH
     TRY(check_launch("vanka patch"));
   }
   if (L.n == 0) return MG_OK;
