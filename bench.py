@@ -350,16 +350,41 @@ def run_ours(args):
     value = total_its / (t_ms / 1e3)
 
     # ---------------- e2e: host buffers through the public API -----------------
-    x_host = torch.empty(N, dtype=torch.float64).pin_memory()
+    # Every step copies its rhs host -> device and its solution device -> host
+    # (pinned buffers).  Double-buffered: step k+1's upload and step k's download
+    # run on a copy stream while step k / k+1 solve.
+    xs = [x, torch.zeros_like(x)]
+    bd = [b, torch.empty_like(b)]
+    x_hosts = [torch.empty(N, dtype=torch.float64).pin_memory() for _ in range(2)]
+    cs = torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
+    bd[1].copy_(b)
+    step(xs[1], bd[1])        # warm the second buffer pair (its CUDA graphs are captured here)
     barrier()
     torch.cuda.synchronize()
     e0.record(stream)
     e2e_its = 0
-    for _ in range(args.steps):
-        b.copy_(b_host, non_blocking=True)
-        its, _ = step(x, b)
-        x_host.copy_(x, non_blocking=True)
+    with torch.cuda.stream(cs):
+        bd[0].copy_(b_host, non_blocking=True)
+        ev_in[0].record(cs)
+    for k in range(args.steps):
+        cur, nxt = k % 2, (k + 1) % 2
+        if k + 1 < args.steps:
+            with torch.cuda.stream(cs):
+                bd[nxt].copy_(b_host, non_blocking=True)   # step k-1 (its user) has finished
+                ev_in[nxt].record(cs)
+        stream.wait_event(ev_in[cur])
+        if k >= 2:
+            stream.wait_event(ev_out[cur])                  # x_hosts[cur]'s download of step k-2 done
+        its, _ = step(xs[cur], bd[cur])
+        ev_out[cur].record(stream)
+        with torch.cuda.stream(cs):
+            cs.wait_event(ev_out[cur])
+            x_hosts[cur].copy_(xs[cur], non_blocking=True)
+            ev_out[cur].record(cs)
         e2e_its += its
+    stream.wait_stream(cs)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
