@@ -51,3 +51,25 @@ def test_shared_problem_two_ranks():
         out = man.dict()
         mp.spawn(_worker, args=(ws, _port(), out), nprocs=ws, join=True)
         assert out.get(0) and out.get(1), dict(out)
+
+
+def test_shared_build_roundtrip_and_fallback(tmp_path, monkeypatch):
+    """Single process: dump/load round trip of a problem (arrays memory-mapped,
+    identical), and the no-room fallback (every rank builds its own copy)."""
+    from problems import configs
+    from problems import share
+    P = configs.build("c2_small", keep_geometry=False)
+    share.dump(P, str(tmp_path / "p"))
+    Q = share.load(str(tmp_path / "p"))
+    assert Q.n_dof == P.n_dof and Q.omega == P.omega and np.array_equal(Q.b, P.b)
+    for a, b in zip(P.levels, Q.levels):
+        assert np.array_equal(a.row_ptr, b.row_ptr) and np.array_equal(a.val, b.val)
+        assert isinstance(b.val, np.memmap)
+    built = []
+    monkeypatch.setattr(share.shutil, "disk_usage", lambda p: type("U", (), {"free": 0})())
+    P2, cleanup = share.shared_build(lambda: built.append(1) or P, "t", 0, lambda: None, lambda tok: tok)
+    cleanup()
+    assert P2 is P and built == [1]
+    P3, cleanup = share.shared_build(lambda: built.append(2) or P, "t", 1, lambda: None, lambda tok: None)
+    cleanup()
+    assert P3 is P and built == [1, 2]        # rank 1 saw no directory: built its own
