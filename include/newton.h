@@ -74,7 +74,10 @@ typedef struct {
 mg_status mg_newton(mg_ctx ctx, double *x, mg_newton_assemble_fn assemble, void *user, const mg_newton_opts *opts,
                     mg_newton_info *info);
 
-/* y <- y + alpha x on this rank's rows of level `level` (device pointers). */
+/* y <- y + alpha x on this rank's rows of level `level` (n_l * bs doubles, device
+ * pointers, caller-owned; x and y must not overlap partially).  Asynchronous on
+ * the context's stream.  Errors: MG_ERR_INVALID_ARG (bad level, NULL vector with
+ * rows), MG_ERR_NONFINITE (alpha not finite).  The Newton update w + d. */
 mg_status mg_axpy(mg_ctx ctx, int level, double alpha, const double *x, double *y);
 
 #ifdef __cplusplus
