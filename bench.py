@@ -65,6 +65,9 @@ WORKLOADS = {
 }
 
 
+WEAK_CONFIGS = {"c5"}
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -230,7 +233,8 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "V-cycles/s", "value": val, "unit": "V-cycles/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak" if args.config in WEAK_CONFIGS else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": {"workload": WORKLOADS[args.config], "n_dof": P.n_dof, "levels": len(P.levels)},
         "cpu_baseline": {"value": val, "unit": "V-cycles/s", "cores": cores, "kind": "oracle",
                          "sample": f"each step = one oracle V(2,2) GMG(L,0,b) on the full {args.config} "
@@ -241,16 +245,48 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def init_dist(ws, local):
+    """One process per rank.  One GPU per rank: torch.distributed over NCCL for
+    the plumbing and the library's NCCL transport.  Fewer GPUs than ranks
+    (e.g. the one-GPU build box; NCCL refuses two ranks on one device): gloo
+    for the plumbing and the library's IPC transport (CUDA IPC mailboxes,
+    inter-process events, shared-memory barrier).  MGB200_TRANSPORT=ipc forces
+    the IPC transport.  Returns (device, transport, reduction device)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2405_05047_b200 as mg
+    ngpu = torch.cuda.device_count()
+    ipc = ngpu < ws or os.environ.get("MGB200_TRANSPORT", "").lower() == "ipc"
+    dev = local % max(ngpu, 1)
+    torch.cuda.set_device(dev)
+    if ipc:
+        dist.init_process_group("gloo")
+        return dev, mg.MG_TRANSPORT_IPC, "cpu"
+    dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    return dev, mg.MG_TRANSPORT_NCCL, "cuda"
+
+
+def group_key(transport):
+    """128-byte group key from rank 0: an NCCL unique id, or random bytes naming
+    the IPC transport's shared-memory segment."""
+    import torch
+    import paper_2405_05047_b200 as mg
+    rank = torch.distributed.get_rank()
+    box = [None]
+    if rank == 0:
+        box[0] = mg.mg_get_unique_id() if transport == mg.MG_TRANSPORT_NCCL else os.urandom(128)
+    torch.distributed.broadcast_object_list(box, src=0)
+    return box[0]
+
+
 def run_ours(args):
     import torch
     ws, rank, local = dist_env()
+    dev, transport, red = local, None, "cuda"
     if ws > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dev, transport, red = init_dist(ws, local)
         # host threads per rank for the generator's OpenMP helper
         os.environ["OMP_NUM_THREADS"] = str(max(1, cpu_cores() // ws))
-    dev = local
     torch.cuda.set_device(dev)
     import paper_2405_05047_b200 as mg
 
@@ -277,19 +313,19 @@ def run_ours(args):
         # level; levels with < 16k rows per rank are replicated (agglomerated)
         from problems.partition import partition
         parts, extras, ranges = partition(P, ws, min_rows_per_rank=args.min_rows_per_rank, only_rank=rank)
-        uid = [mg.mg_get_unique_id() if rank == 0 else None]
-        torch.distributed.broadcast_object_list(uid, src=0)
+        uid = group_key(transport)
         levels, (b_np, H) = parts[rank], extras[rank]
         del parts, extras
         cleanup()
         solver = mg.Multigrid(levels, bs, omega=P.omega, nu_pre=P.nu_pre, nu_post=P.nu_post, H=H, device=dev,
                               stream=stream, use_graphs=not args.no_graphs, precision=prec,
-                              comm=(ws, rank, uid[0], mg.MG_TRANSPORT_NCCL))
+                              comm=(ws, rank, uid, transport))
         n_global = P.n_dof
         level_kinds = ["replicated" if all(r == (0, P.levels[l].n) for r in ranges[l]) else "distributed"
                        for l in range(len(P.levels))]
     else:
-        solver = mg.Multigrid(P.levels, bs, omega=P.omega, nu_pre=P.nu_pre, nu_post=P.nu_post, H=P.fine.H,
+        H = P.fine.H
+        solver = mg.Multigrid(P.levels, bs, omega=P.omega, nu_pre=P.nu_pre, nu_post=P.nu_post, H=H,
                               device=dev, stream=stream, use_graphs=not args.no_graphs, precision=prec)
         b_np = P.b
         n_global = P.n_dof
@@ -310,7 +346,8 @@ def run_ours(args):
         st, its, rel, conv = solver.solve(xv, bv, **opts)
         if not conv:
             raise RuntimeError(f"solve did not converge: {its} its, rel {rel:.3e}")
-        solver.apply_constraints(xv)
+        if H is not None:
+            solver.apply_constraints(xv)
         return its, rel
 
     def barrier():
@@ -340,7 +377,7 @@ def run_ours(args):
     launches = mg.launch_count(ctx) - l0
     clocks = sampler.stop()
     if ws > 1:
-        tt = torch.tensor([t_ms, float(launches)], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([t_ms, float(launches)], dtype=torch.float64, device=red)
         tmax = tt[:1].clone()
         torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
         torch.distributed.all_reduce(tt[1:], op=torch.distributed.ReduceOp.SUM)
@@ -348,6 +385,9 @@ def run_ours(args):
     # every rank takes part in the same global V-cycles (strong scaling):
     # units = global V-cycles of the whole job
     value = total_its / (t_ms / 1e3)
+    # a fixed global problem (C2/C3/...) is strong scaling at every N; C5's
+    # per-rank generated rows are weak scaling
+    scaling = "weak" if args.config in WEAK_CONFIGS else "strong"
 
     # ---------------- e2e: host buffers through the public API -----------------
     # Every step copies its rhs host -> device and its solution device -> host
@@ -390,7 +430,7 @@ def run_ours(args):
     barrier()
     e2e_ms = e0.elapsed_time(e1)
     if ws > 1:
-        tt = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=red)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(tt[0])
     e2e_val = e2e_its / (e2e_ms / 1e3)
@@ -528,12 +568,15 @@ def run_ours(args):
         line = {
             "metric": "V-cycles/s", "value": value, "unit": "V-cycles/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config], "n_dof": n_global, "n_dof_per_gpu": N,
                        "levels": len(P.levels), "level_rows_rank0": [i["n"] for i in infos],
                        "level_kinds": level_kinds,
                        "nnzb_fine_rank0": infos[L]["nnzb"],
-                       "parallelism": f"row-partition x{ws} (NCCL halos, allreduce dots, agglomeration)"
+                       "parallelism": (f"row-partition x{ws} ({'NCCL' if transport == mg.MG_TRANSPORT_NCCL else 'IPC'}"
+                                       f" transport: halos, allreduce dots, agglomeration"
+                                       + (f"; {ws} ranks share {torch.cuda.device_count()} GPU(s)"
+                                          if torch.cuda.device_count() < ws else "") + ")")
                        if ws > 1 else "single GPU",
                        "solver": "GMRES(30) + V(2,2) block-Jacobi, rtol 1e-10, x0 = 0, then x <- Hx",
                        "precision": ("fp64" if vb == 8 else

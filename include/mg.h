@@ -78,7 +78,7 @@ typedef enum {
 } mg_status;
 
 enum { MG_MEM_HOST = 0, MG_MEM_DEVICE = 1 };
-enum { MG_TRANSPORT_NCCL = 0, MG_TRANSPORT_LOCAL = 1 };
+enum { MG_TRANSPORT_NCCL = 0, MG_TRANSPORT_LOCAL = 1, MG_TRANSPORT_IPC = 2 };
 enum { MG_COARSE_DIRECT = 0, MG_COARSE_SMOOTH = 1 };
 enum { MG_GMRES = 0, MG_RICHARDSON = 1 };
 enum { MG_PREC_FP64 = 0, MG_PREC_MIXED = 1 };
@@ -119,6 +119,16 @@ typedef struct {
  * transport = MG_TRANSPORT_LOCAL: all ranks are host threads of ONE process
  *   sharing one device (a test transport: the full distributed algorithm on a
  *   single GPU); nccl_id is any 128-byte group key shared by the ranks.
+ * transport = MG_TRANSPORT_IPC: one PROCESS per rank on one node, any mix of
+ *   devices (several ranks may share one GPU, which NCCL refuses: "Duplicate
+ *   GPU detected").  Device data moves through per-rank mailbox buffers
+ *   exported with CUDA IPC memory handles (peer loads over NVLink between
+ *   GPUs), ordered by inter-process CUDA events; the ranks meet at a host
+ *   barrier in a POSIX shared-memory segment named after the first 16 bytes
+ *   of nccl_id (any 128-byte key, e.g. random bytes from rank 0, broadcast
+ *   by the caller).  Host barriers make it not graph-capturable: contexts on
+ *   it run eagerly.  A rank that does not arrive within 300 s turns every
+ *   barrier into MG_ERR_STATE instead of a hang.
  * With nranks > 1 every mg_* call below is collective: all ranks call it, in
  * the same order, with their own rows. */
 typedef struct {

@@ -114,6 +114,14 @@ int64_t mgi_launch_count(mgi_ctx ctx);
  * row count (libns: the NS step runs on the pressure solver's stream). */
 int mgi_stream_info(mgi_ctx ctx, void **stream, int *device, int *n_levels, int64_t *n_fine);
 
+/* Agree on a status over all ranks of the context (collective; host-side
+ * all-gather through the transport): *agreed = the status of the lowest rank
+ * whose status is not MG_OK, else MG_OK.  Single GPU: *agreed = status.  Lets
+ * a rank-local failure (e.g. a Newton assembly callback) fail every rank
+ * together instead of leaving the others in a collective.  Returns an
+ * mg_status of the agreement itself. */
+int mgi_agree(mgi_ctx ctx, int status, int *agreed);
+
 /* One V-cycle (eager, not graph-launched) with CUDA events between its
  * phases: out[l] = ms spent on level l's kernels (both legs; level 0 = the
  * coarse solve), out[n_levels + l] = ms in level l's halo exchanges,

@@ -5,7 +5,9 @@ Written step by step in the paper's order and notation; every heavy operation
 is one of the plain per-op C definitions in oracle/__init__.py.
 Readings: Z3 coarse solve exact (LU) by default, "several steps of
 the smoothing iteration" as option; Z5 right preconditioning, MGS,
-restart m, stop at |g_{j+1}| <= rtol * beta_0; Z6 Euclidean norm over all
+restart m, a cycle ends at |g_{j+1}| <= rtol * beta_0 and the solve stops when
+the true residual ||b - A x|| <= rtol * beta_0 (else it restarts) or on a happy
+breakdown; Z6 Euclidean norm over all
 DOFs; Z21 the coarse solve ignores the incoming x; iteration count = number of
 preconditioner applications.
 """
@@ -244,7 +246,7 @@ def gmres(h: MgHierarchy, b, x0=None, rtol=1e-10, restart=30, max_iter=200, prec
         V[0] = r / beta
         g[0] = beta
         k = 0
-        done = False
+        happy = False                                    # happy breakdown h_{j+1,j} = 0
         for j in range(m):
             Z[j] = vcycle(h, Lf, np.zeros(N), V[j]) if precondition else V[j]
             its += 1
@@ -269,7 +271,7 @@ def gmres(h: MgHierarchy, b, x0=None, rtol=1e-10, restart=30, max_iter=200, prec
             hist.append(abs(g[j + 1]) / beta0)
             k = j + 1
             if abs(g[j + 1]) <= rtol * beta0 or breakdown:
-                done = True
+                happy = breakdown
                 break
             V[j + 1] = w / hn
         y = np.zeros(k)                                  # back substitution H y = g
@@ -279,8 +281,8 @@ def gmres(h: MgHierarchy, b, x0=None, rtol=1e-10, restart=30, max_iter=200, prec
             x = x + y[i] * Z[i]
         r = residual(F.n, F.bs, F.rp, F.col, F.val, x, b)
         beta = nrm2(r)
-        if done or beta <= rtol * beta0:
-            break
+        if happy or beta <= rtol * beta0:               # converged on the TRUE residual; an estimate
+            break                                        # below rtol with a true residual above it restarts
     if mc is not None:
         x = project_zero_mean(x, *mc)                    # the normalised solution int p = 0
     return x, its, hist, beta / beta0

@@ -31,7 +31,7 @@ MG_ERR_SINGULAR, MG_ERR_STATE, MG_ERR_CUDA, MG_ERR_NCCL, MG_ERR_OOM = -5, -6, -7
 MG_MEM_HOST, MG_MEM_DEVICE = 0, 1
 MG_COARSE_DIRECT, MG_COARSE_SMOOTH = 0, 1
 MG_GMRES, MG_RICHARDSON = 0, 1
-MG_TRANSPORT_NCCL, MG_TRANSPORT_LOCAL = 0, 1
+MG_TRANSPORT_NCCL, MG_TRANSPORT_LOCAL, MG_TRANSPORT_IPC = 0, 1, 2
 MG_PREC_FP64, MG_PREC_MIXED = 0, 1
 
 STATUS_NAMES = {0: "MG_OK", 1: "MG_NOT_CONVERGED", -1: "MG_ERR_INVALID_ARG", -2: "MG_ERR_DIMENSION",
@@ -211,6 +211,55 @@ def _same_mem(*arrs):
     return mems.pop() if mems else MG_MEM_HOST
 
 
+# Per-context facts the binding needs to check buffer sizes and devices before
+# handing raw pointers to the C side (which trusts them): device, block size,
+# number of levels; level row counts are queried (mgi_level_info) and cached.
+_CTX: dict = {}
+_NS: dict = {}
+
+
+def _numel(a) -> int:
+    return int(a.size) if isinstance(a, np.ndarray) else int(a.numel())
+
+
+def _need(a, count: int, what: str, device=None):
+    """Raise ValueError unless `a` holds at least `count` elements (and, for a
+    CUDA tensor, lives on `device`)."""
+    if a is None:
+        return
+    if _numel(a) < count:
+        raise ValueError(f"{what}: {_numel(a)} elements, the call reads/writes {count}")
+    if device is not None and getattr(a, "is_cuda", False) and a.device.index != device:
+        raise ValueError(f"{what}: tensor on cuda:{a.device.index}, context on cuda:{device}")
+
+
+def _rows(ctx, level) -> int:
+    info = _CTX.get(ctx)
+    if info is None:
+        return -1
+    n = info["rows"].get(level)
+    if n is None:
+        n = level_info(ctx, level)["n"] if 0 <= level < info["n_levels"] else -1
+        if n > 0:
+            info["rows"][level] = n
+    return n
+
+
+def _vec(ctx, level, a, what):
+    """Device pointer of a level vector [n_rows(level) * bs] (size and device checked)."""
+    p = _dptr(a)
+    info = _CTX.get(ctx)
+    if info is not None:
+        n = _rows(ctx, level)
+        _need(a, max(n, 0) * info["bs"], what, info["device"])
+    return p
+
+
+def _fine(ctx) -> int:
+    info = _CTX.get(ctx)
+    return info["n_levels"] - 1 if info is not None else 0
+
+
 # ----------------------------------------------------------------------------
 # the C ABI, same names
 # ----------------------------------------------------------------------------
@@ -246,6 +295,7 @@ def mg_create(n_levels, block_size, *, nu_pre=2, nu_post=2, omega=0.8, coarse_mo
         cm = mg_comm(nranks, rank, transport, (ctypes.c_ubyte * 128)(*uid))
     _check(_lib.mg_create(ctypes.byref(h), ctypes.byref(cfg), device, s, ctypes.byref(cm) if cm else None),
            "mg_create")
+    _CTX[h.value] = {"device": int(device), "bs": int(block_size), "n_levels": int(n_levels), "rows": {}}
     return h.value
 
 
@@ -262,6 +312,9 @@ def mg_set_matrix(ctx, level, row_ptr, col, vals):
 
 
 def mg_update_matrix(ctx, level, vals):
+    info = _CTX.get(ctx)
+    if info is not None and 0 <= level < info["n_levels"]:
+        _need(vals, level_info(ctx, level)["nnzb"] * info["bs"] ** 2, "mg_update_matrix vals", info["device"])
     p, mem = _ptr(vals, np.float64)
     _check(_lib.mg_update_matrix(ctx, level, p, mem), "mg_update_matrix")
 
@@ -274,6 +327,9 @@ def mg_set_transfer(ctx, fine_level, row_ptr, col, w, weights_per_entry=1):
 
 
 def mg_set_smoother(ctx, level, omega=0.0, nu_pre=-1, nu_post=-1, dinv=None):
+    info = _CTX.get(ctx)
+    if info is not None and dinv is not None:
+        _need(dinv, max(_rows(ctx, level), 0) * info["bs"] ** 2, "mg_set_smoother dinv", info["device"])
     p, mem = _ptr(dinv, np.float64)
     _check(_lib.mg_set_smoother(ctx, level, omega, nu_pre, nu_post, p, mem), "mg_set_smoother")
 
@@ -300,16 +356,21 @@ def mg_set_mean_constraint(ctx, level, w, k):
         _check(_lib.mg_set_mean_constraint(ctx, level, None, None, MG_MEM_HOST), "mg_set_mean_constraint")
         return
     mem = _same_mem(w, k)
+    info = _CTX.get(ctx)
+    if info is not None:
+        n = max(_rows(ctx, level), 0) * info["bs"]
+        _need(w, n, "mg_set_mean_constraint w", info["device"])
+        _need(k, n, "mg_set_mean_constraint k", info["device"])
     _check(_lib.mg_set_mean_constraint(ctx, level, _ptr(w, np.float64)[0], _ptr(k, np.float64)[0], mem),
            "mg_set_mean_constraint")
 
 
 def mg_project_zero_mean(ctx, level, x):
-    _check(_lib.mg_project_zero_mean(ctx, level, _dptr(x)), "mg_project_zero_mean")
+    _check(_lib.mg_project_zero_mean(ctx, level, _vec(ctx, level, x, "x")), "mg_project_zero_mean")
 
 
 def mg_make_consistent(ctx, level, b):
-    _check(_lib.mg_make_consistent(ctx, level, _dptr(b)), "mg_make_consistent")
+    _check(_lib.mg_make_consistent(ctx, level, _vec(ctx, level, b, "b")), "mg_make_consistent")
 
 
 def mg_setup(ctx):
@@ -318,69 +379,79 @@ def mg_setup(ctx):
 
 def mg_destroy(ctx):
     _check(_lib.mg_destroy(ctx), "mg_destroy")
+    _CTX.pop(ctx, None)
 
 
 def mg_vcycle(ctx, x, b):
-    _check(_lib.mg_vcycle(ctx, _dptr(x), _dptr(b)), "mg_vcycle")
+    f = _fine(ctx)
+    _check(_lib.mg_vcycle(ctx, _vec(ctx, f, x, "x"), _vec(ctx, f, b, "b")), "mg_vcycle")
 
 
 def mg_vcycle_zero(ctx, z, v):
-    _check(_lib.mg_vcycle_zero(ctx, _dptr(z), _dptr(v)), "mg_vcycle_zero")
+    f = _fine(ctx)
+    _check(_lib.mg_vcycle_zero(ctx, _vec(ctx, f, z, "z"), _vec(ctx, f, v, "v")), "mg_vcycle_zero")
 
 
 def mg_solve(ctx, x, b, method=MG_GMRES, restart=30, max_iter=200, rtol=1e-10, raise_on_nonconv=False):
     """Returns (status, iterations, rel_residual, converged)."""
     o = mg_solve_opts(method, restart, max_iter, rtol)
     info = mg_solve_info()
-    st = _lib.mg_solve(ctx, _dptr(x), _dptr(b), ctypes.byref(o), ctypes.byref(info))
+    f = _fine(ctx)
+    st = _lib.mg_solve(ctx, _vec(ctx, f, x, "x"), _vec(ctx, f, b, "b"), ctypes.byref(o), ctypes.byref(info))
     _check(st, "mg_solve", ok=(MG_OK,) if raise_on_nonconv else (MG_OK, MG_NOT_CONVERGED))
     return st, info.iterations, info.rel_residual, bool(info.converged)
 
 
 def mg_spmv(ctx, level, alpha, x, beta, y):
-    _check(_lib.mg_spmv(ctx, level, alpha, _dptr(x), beta, _dptr(y)), "mg_spmv")
+    _check(_lib.mg_spmv(ctx, level, alpha, _vec(ctx, level, x, "x"), beta, _vec(ctx, level, y, "y")), "mg_spmv")
 
 
 def mg_sweep(ctx, level, x, b, x_out):
-    _check(_lib.mg_sweep(ctx, level, _dptr(x), _dptr(b), _dptr(x_out)), "mg_sweep")
+    _check(_lib.mg_sweep(ctx, level, _vec(ctx, level, x, "x"), _vec(ctx, level, b, "b"),
+                         _vec(ctx, level, x_out, "x_out")), "mg_sweep")
 
 
 def mg_residual(ctx, level, x, b, r):
-    _check(_lib.mg_residual(ctx, level, _dptr(x), _dptr(b), _dptr(r)), "mg_residual")
+    _check(_lib.mg_residual(ctx, level, _vec(ctx, level, x, "x"), _vec(ctx, level, b, "b"),
+                            _vec(ctx, level, r, "r")), "mg_residual")
 
 
 def mg_smooth(ctx, level, x, b, sweeps=1):
-    _check(_lib.mg_smooth(ctx, level, _dptr(x), _dptr(b), sweeps), "mg_smooth")
+    _check(_lib.mg_smooth(ctx, level, _vec(ctx, level, x, "x"), _vec(ctx, level, b, "b"), sweeps), "mg_smooth")
 
 
 def mg_restrict(ctx, fine_level, r_fine, d_coarse):
-    _check(_lib.mg_restrict(ctx, fine_level, _dptr(r_fine), _dptr(d_coarse)), "mg_restrict")
+    _check(_lib.mg_restrict(ctx, fine_level, _vec(ctx, fine_level, r_fine, "r_fine"),
+                            _vec(ctx, fine_level - 1, d_coarse, "d_coarse")), "mg_restrict")
 
 
 def mg_prolong_add(ctx, fine_level, y_coarse, x_fine):
-    _check(_lib.mg_prolong_add(ctx, fine_level, _dptr(y_coarse), _dptr(x_fine)), "mg_prolong_add")
+    _check(_lib.mg_prolong_add(ctx, fine_level, _vec(ctx, fine_level - 1, y_coarse, "y_coarse"),
+                               _vec(ctx, fine_level, x_fine, "x_fine")), "mg_prolong_add")
 
 
 def mg_coarse_solve(ctx, d, y):
-    _check(_lib.mg_coarse_solve(ctx, _dptr(d), _dptr(y)), "mg_coarse_solve")
+    _check(_lib.mg_coarse_solve(ctx, _vec(ctx, 0, d, "d"), _vec(ctx, 0, y, "y")), "mg_coarse_solve")
 
 
 def mg_apply_constraints(ctx, x):
-    _check(_lib.mg_apply_constraints(ctx, _dptr(x)), "mg_apply_constraints")
+    f = _fine(ctx)
+    _check(_lib.mg_apply_constraints(ctx, _vec(ctx, f, x, "x")), "mg_apply_constraints")
 
 
 def mg_condense_rhs(ctx, b, b_bar):
-    _check(_lib.mg_condense_rhs(ctx, _dptr(b), _dptr(b_bar)), "mg_condense_rhs")
+    f = _fine(ctx)
+    _check(_lib.mg_condense_rhs(ctx, _vec(ctx, f, b, "b"), _vec(ctx, f, b_bar, "b_bar")), "mg_condense_rhs")
 
 
 def mg_dot(ctx, level, a, b) -> float:
     out = _D()
-    _check(_lib.mg_dot(ctx, level, _dptr(a), _dptr(b), ctypes.byref(out)), "mg_dot")
+    _check(_lib.mg_dot(ctx, level, _vec(ctx, level, a, "a"), _vec(ctx, level, b, "b"), ctypes.byref(out)), "mg_dot")
     return out.value
 
 
 def mg_axpy(ctx, level, alpha, x, y):
-    _check(_lib.mg_axpy(ctx, level, alpha, _dptr(x), _dptr(y)), "mg_axpy")
+    _check(_lib.mg_axpy(ctx, level, alpha, _vec(ctx, level, x, "x"), _vec(ctx, level, y, "y")), "mg_axpy")
 
 
 def mg_newton(ctx, x, assemble, n_fine_dof, level_sizes, *, max_newton=3, ntol=1e-8, atol=0.0, reuse_rate=0.0,
@@ -408,7 +479,7 @@ def mg_newton(ctx, x, assemble, n_fine_dof, level_sizes, *, max_newton=3, ntol=1
     fn = MG_NEWTON_ASSEMBLE_FN(cb)
     o = mg_newton_opts(max_newton, ntol, atol, reuse_rate, mg_solve_opts(method, restart, max_iter, rtol))
     info = mg_newton_info()
-    st = _lib.mg_newton(ctx, _dptr(x), fn, None, ctypes.byref(o), ctypes.byref(info))
+    st = _lib.mg_newton(ctx, _vec(ctx, _fine(ctx), x, "x"), fn, None, ctypes.byref(o), ctypes.byref(info))
     if err:
         raise err[0]
     _check(st, "mg_newton", ok=(MG_OK, MG_NOT_CONVERGED))
@@ -449,11 +520,13 @@ from .solver import Multigrid  # noqa: E402,F401
 def ns_create(pressure_ctx, n_u, n_p):
     h = _P()
     _check(_lib.ns_create(ctypes.byref(h), pressure_ctx, int(n_u), int(n_p)), "ns_create")
+    _NS[h.value] = {"n_u": int(n_u), "n_p": int(n_p)}
     return h
 
 
 def ns_destroy(ctx):
     _check(_lib.ns_destroy(ctx), "ns_destroy")
+    _NS.pop(getattr(ctx, "value", ctx), None)
 
 
 def ns_set_momentum(ctx, row_ptr, col, vals):
@@ -472,6 +545,10 @@ def ns_set_coupling(ctx, pi, g):
 
 
 def ns_set_mass(ctx, m_u, m_p):
+    sz = _ns_sizes(ctx)
+    if sz is not None:
+        _need(m_u, sz["n_u"], "ns_set_mass m_u")
+        _need(m_p, sz["n_p"], "ns_set_mass m_p")
     mem = _same_mem(m_u, m_p)
     _check(_lib.ns_set_mass(ctx, _ptr(m_u, np.float64)[0], _ptr(m_p, np.float64)[0], mem), "ns_set_mass")
 
@@ -482,7 +559,14 @@ def ns_set_dirichlet(ctx, rows, vals):
            "ns_set_dirichlet")
 
 
+def _ns_sizes(ctx):
+    return _NS.get(getattr(ctx, "value", ctx))
+
+
 def ns_set_force(ctx, F):
+    sz = _ns_sizes(ctx)
+    if sz is not None and F is not None:
+        _need(F, 3 * sz["n_u"], "ns_set_force F")
     p, mem = _ptr(F, np.float64)
     _check(_lib.ns_set_force(ctx, p, mem), "ns_set_force")
 
@@ -492,7 +576,16 @@ def ns_set_params(ctx, nu, dt, rtol=1e-6, restart=30, max_iter=200, timing=False
            "ns_set_params")
 
 
+def _ns_state_sizes(ctx, u, p, q):
+    sz = _ns_sizes(ctx)
+    if sz is not None:
+        _need(u, 3 * sz["n_u"], "u")
+        _need(p, sz["n_p"], "p")
+        _need(q, sz["n_p"], "q")
+
+
 def ns_set_state(ctx, u, p, q):
+    _ns_state_sizes(ctx, u, p, q)
     mem = _same_mem(u, p, q)
     _check(_lib.ns_set_state(ctx, _ptr(u, np.float64)[0], _ptr(p, np.float64)[0], _ptr(q, np.float64)[0], mem),
            "ns_set_state")
@@ -500,6 +593,7 @@ def ns_set_state(ctx, u, p, q):
 
 def ns_get_state(ctx, u, p, q):
     """Fill u [n_u*3], p, q [n_p] (numpy arrays or CUDA tensors, same memory)."""
+    _ns_state_sizes(ctx, u, p, q)
     mem = _same_mem(u, p, q)
     _check(_lib.ns_get_state(ctx, _ptr(u, np.float64)[0], _ptr(p, np.float64)[0], _ptr(q, np.float64)[0], mem),
            "ns_get_state")
@@ -514,11 +608,17 @@ def ns_step(ctx):
 
 
 def ns_momentum(ctx, u_new):
+    sz = _ns_sizes(ctx)
+    if sz is not None:
+        _need(u_new, 3 * sz["n_u"], "u_new")
     p, mem = _ptr(u_new, np.float64)
     _check(_lib.ns_momentum(ctx, p, mem), "ns_momentum")
 
 
 def ns_get_divergence(ctx, d):
+    sz = _ns_sizes(ctx)
+    if sz is not None:
+        _need(d, sz["n_p"], "d")
     p, mem = _ptr(d, np.float64)
     _check(_lib.ns_get_divergence(ctx, p, mem), "ns_get_divergence")
 

@@ -2138,6 +2138,22 @@ int mgi_stream_info(mgi_ctx c, void **stream, int *device, int *n_levels, int64_
   return MG_OK;
 }
 
+int mgi_agree(mgi_ctx c, int status, int *agreed) {
+  if (!c || !agreed) return MG_ERR_INVALID_ARG;
+  *agreed = status;
+  if (!c->tr) return MG_OK;
+  std::vector<int> all(size_t(c->tr->nranks), 0);
+  const mg_status s = c->tr->allgather_host(&status, sizeof(int), all.data());
+  if (s != MG_OK) return s;
+  *agreed = MG_OK;
+  for (int v : all)
+    if (v != MG_OK) {
+      *agreed = v;
+      break;
+    }
+  return MG_OK;
+}
+
 int mgi_vcycle_profile(mgi_ctx c, double *x, const double *b, int zero, double *out, int n_out) {
   if (!c || !x || !b || !out) return MG_ERR_INVALID_ARG;
   const int nl = c->L() + 1;
@@ -2193,7 +2209,7 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
   const int64_t N = F.n * bs;
   const double rtol = opts->rtol;
   int its = 0;
-  double rel = 0.0;
+  double rel = 1.0;  // ||b - A x0|| / ||b - A x0|| until an iteration ran (max_iter = 0)
   bool conv = false;
   if (!c->gm_host) CU(cudaMallocHost(&c->gm_host, 16 * sizeof(double)));
   double *hst = c->gm_host;
@@ -2219,7 +2235,7 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
     CU(cudaStreamSynchronize(c->stream));
     const double r0 = hst[0];
     if (!std::isfinite(r0)) return fail(MG_ERR_NONFINITE, "non-finite initial residual");
-    if (r0 == 0.0) conv = true;
+    if (r0 == 0.0) conv = true, rel = 0.0;
     const unsigned eg = unsigned(std::min<int64_t>(std::max<int64_t>(1, (N + 255) / 256), 8 * c->n_sm));
     while (!conv && its < opts->max_iter) {
       if (!mixed) {
@@ -2252,7 +2268,7 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
     CU(cudaStreamSynchronize(c->stream));
     const double beta0 = hst[0];
     if (!std::isfinite(beta0)) return fail(MG_ERR_NONFINITE, "non-finite initial residual");
-    if (beta0 == 0.0) conv = true;
+    if (beta0 == 0.0) conv = true, rel = 0.0;
     const unsigned eg = unsigned(std::min<int64_t>(std::max<int64_t>(1, (N + 255) / 256), 8 * c->n_sm));
     while (!conv && its < opts->max_iter) {
       const int mm = std::min(m, opts->max_iter - its);
@@ -2260,7 +2276,7 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
       ++g_tally, mgk::k_scale_div<<<eg, 256, 0, c->stream>>>(N, V, g.beta, V);
       TRY(check_launch("gmres start"));
       int k = 0;
-      bool done = false;
+      bool happy = false;  // happy breakdown h_{j+1,j} = 0
       for (int j = 0; j < mm; ++j) {
         // one Arnoldi step: a single CUDA graph per j (V-cycle, SpMV, MGS,
         // Givens, scaling, flag copy-out), then one host sync
@@ -2295,8 +2311,8 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
         CU(cudaStreamSynchronize(c->stream));
         k = j + 1;
         if (!std::isfinite(hst[0])) return fail(MG_ERR_NONFINITE, "non-finite GMRES residual estimate");
-        if (hst[1] != 0.0) {
-          done = true;
+        if (hst[1] != 0.0) {  // estimate |g_{j+1}| <= rtol beta_0, or breakdown: end of the cycle
+          happy = hst[2] == 0.0;
           break;
         }
       }
@@ -2309,7 +2325,9 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
       CU(cudaStreamSynchronize(c->stream));
       rel = hst[0] / beta0;
       if (!std::isfinite(rel)) return fail(MG_ERR_NONFINITE, "non-finite residual");
-      if (done || hst[0] <= rtol * beta0) {
+      // converged on the TRUE residual (or a happy breakdown); an estimate below
+      // rtol whose true residual is above it restarts (reading Z5)
+      if (happy || hst[0] <= rtol * beta0) {
         conv = true;
         break;
       }

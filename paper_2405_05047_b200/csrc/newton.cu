@@ -51,6 +51,17 @@ double now_ms() {
 
 extern "C" {
 
+// Every rank learns whether any rank's assembly callback failed, so all ranks
+// leave together instead of the healthy ones blocking in the next collective.
+static mg_status agree_assembly(mg_ctx ctx, mg_status as) {
+  int all = as;
+  const int s = mgi_agree(ctx, as, &all);
+  if (s != MG_OK) return mg_status(s);
+  if (all == MG_OK) return MG_OK;
+  if (as != MG_OK) return as == MG_NOT_CONVERGED ? fail(MG_ERR_INVALID_ARG, "assemble returned %d", as) : as;
+  return fail(MG_ERR_STATE, "the assembly callback failed on another rank (status %d)", all);
+}
+
 mg_status mg_newton(mg_ctx ctx, double *x, mg_newton_assemble_fn assemble, void *user, const mg_newton_opts *opts,
                     mg_newton_info *info) {
   if (!ctx || !assemble || !opts) return fail(MG_ERR_INVALID_ARG, "NULL ctx, assemble or opts");
@@ -107,7 +118,7 @@ mg_status mg_newton(mg_ctx ctx, double *x, mg_newton_assemble_fn assemble, void 
     if (N) CU(cudaMemcpyAsync(w.p, x, size_t(N) * sizeof(double), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     mg_status as = assemble(user, w.p, Fh.p, nullptr);
-    if (as != MG_OK) return as == MG_NOT_CONVERGED ? fail(MG_ERR_INVALID_ARG, "assemble returned %d", as) : as;
+    TRY(agree_assembly(ctx, as));
     inf.ms_assemble += now_ms() - t0;
     // f = F, ||F||_2 on the device over all ranks
     if (N) CU(cudaMemcpyAsync(f.p, Fh.p, size_t(N) * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -128,7 +139,7 @@ mg_status mg_newton(mg_ctx ctx, double *x, mg_newton_assemble_fn assemble, void 
     if (!keep) {
       const double t1 = now_ms();
       as = assemble(user, w.p, nullptr, vptr.data());
-      if (as != MG_OK) return as == MG_NOT_CONVERGED ? fail(MG_ERR_INVALID_ARG, "assemble returned %d", as) : as;
+      TRY(agree_assembly(ctx, as));
       inf.ms_assemble += now_ms() - t1;
       CU(cudaEventRecord(ev.e[0], st));
       for (int l = 0; l < nl; ++l) TRY(mg_update_matrix(ctx, l, vptr[l], MG_MEM_HOST));

@@ -253,6 +253,39 @@ def test_gmres_restart_and_maxiter():
     assert st == m.MG_OK and its == 0 and conv
 
 
+@pytest.mark.parametrize("restart,max_iter", [(3, 6), (30, 4), (2, 5)])
+def test_gmres_truncated_iterate_matches_oracle(restart, max_iter):
+    """max_iter truncation and restarts: the GPU iterate after exactly
+    max_iter preconditioner applications equals the oracle's, whose GMRES(m) is
+    pinned by the minimal-residual property (tests/test_oracle_pins_r2.py)."""
+    import paper_2405_05047_b200 as m
+    lv, bs, om, b, H = case("c3_small")
+    mg = gpu_mg("c3_small")
+    h = orc_mg("c3_small")
+    x = dev(np.zeros(lv[-1].n * bs))
+    st, its, rel, conv = m.mg_solve(mg.ctx, x, dev(b), restart=restart, max_iter=max_iter, rtol=1e-15)
+    xe, ite, _, rele = oracle.gmres(h, b, rtol=1e-15, restart=restart, max_iter=max_iter)
+    assert st == m.MG_NOT_CONVERGED and not conv and its == ite == max_iter
+    assert np.linalg.norm(host(x) - xe) <= 1e-9 * np.linalg.norm(xe)
+    assert abs(rel - rele) <= 1e-6 * rele
+
+
+def test_gmres_beyond_one_restart_cycle_matches_oracle():
+    """A weak preconditioner (V(1,0), coarse problem smoothed twice) so the
+    solve needs more than one GMRES(30) cycle; +-1 iterations and x at 1e-8."""
+    import paper_2405_05047_b200 as m
+    lv, bs, om, b, H = case("c3_small")
+    mg = build_gpu(lv, bs, omega=om, nu=(1, 0), coarse_mode=1, coarse_sweeps=2, H=H)
+    h = build_oracle(lv, omega=om, nu=(1, 0), coarse="smooth", coarse_sweeps=2, H=H)
+    x = dev(np.zeros(lv[-1].n * bs))
+    st, its, rel, conv = m.mg_solve(mg.ctx, x, dev(b), restart=30, max_iter=400, rtol=1e-10)
+    xe, ite, _, rele = oracle.gmres(h, b, rtol=1e-10, restart=30, max_iter=400)
+    assert ite > 30 and conv and st == m.MG_OK
+    assert abs(its - ite) <= 1, (its, ite)
+    assert rel <= 1e-10
+    assert np.linalg.norm(host(x) - xe) <= 1e-8 * np.linalg.norm(xe)
+
+
 def test_apply_constraints_and_dot():
     import paper_2405_05047_b200 as m
     lv, bs, om, b, H = case("c3_small")
