@@ -57,8 +57,10 @@ WORKLOADS = {
     "td_l10": "the paper's transport-diffusion case L10 (P:402-405): uniform 1024x1024 Q1 mesh of the unit square, "
               "1,050,625 DOFs, M^l/dt + lambda K + B (lambda 0.01, b = (0,-1), dt 0.02), 9 levels, GMRES(30)+V(2,2) "
               "Jacobi omega 0.8, direct coarse solve",
-    "c5": "C5: 3D NS-shaped generalised Stokes (PSPG, eps M_p), Q1 4x4 blocks (p,u,v,w), (0,1)^2x(0,2) cavity, "
-          "128x128x256 cells, 6 levels, per-component transfers, GMRES(30)+V(2,2) omega=0.6",
+    "c5": "C5 weak scaling: 3D NS-shaped generalised Stokes (PSPG, eps M_p), Q1 4x4 blocks (p,u,v,w), "
+          "(0,1)^2x(0,2) lid cavity of equal cubic cells, root*2^R per GPU count (P=1 128^2x256 = 17.1M DOFs, "
+          "P=2 160^2x320, P=4 192^2x384, P=8 256^2x512 = 135.5M DOFs), lexicographic numbering, each rank "
+          "generates its own z-slab of every level, per-component transfers, GMRES(30)+V(2,2) omega=0.6",
     "pres": "N2: pure-Neumann pressure Poisson of the projection step (Alg. 2 Step 2, P:618-636) on the NS cavity "
             "(0,1)^2x(0,2), Q1, 128x128x256 cells (4,293,249 DOFs), 6 levels, int p = 0 imposed on every level "
             "(P:158), GMRES(30)+V(2,2) Jacobi omega=0.8, regularised direct coarse solve",
@@ -181,6 +183,39 @@ def build_problem(name):
     return P
 
 
+class StructuredProblem:
+    """This rank's part of the per-rank generated C5 workload, with the fields
+    of problems.configs.Problem that bench.py uses."""
+
+    def __init__(self, levels, b, ranges, ws, n_dof):
+        from problems import structured as S
+        self.levels, self.b, self.ranges = levels, b, ranges
+        self.bs, self.omega, self.nu_pre, self.nu_post = 4, S.OMEGA, 2, 2
+        self.n_dof = n_dof
+        self.level_kinds = (["single"] * len(levels) if ws == 1 else
+                            ["replicated" if all(r == (0, L.n_global) for r in ranges[l]) else "distributed"
+                             for l, L in enumerate(levels)])
+
+    @property
+    def fine(self):
+        class _F:
+            H = None
+            mean_w = None
+        return _F()
+
+
+def build_structured(args, ws, rank):
+    from problems import structured as S
+    if ws not in S.C5_WEAK:
+        raise SystemExit(f"c5 weak scaling is defined for 1/2/4/8 ranks (SURVEY §8(d)), not {ws}")
+    t = time.time()
+    levels, b, ranges = S.build_rank(ws, rank, min_rows_per_rank=args.min_rows_per_rank)
+    P = StructuredProblem(levels, b, ranges, ws, S.n_dof(ws))
+    log(f"[bench] rank {rank}: generated its C5 rows ({levels[-1].n * 4} of {P.n_dof} DOFs, levels "
+        f"{[L.n for L in levels]}) in {time.time() - t:.1f}s")
+    return P
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -226,7 +261,7 @@ def run_reference(args):
     ws, rank, local = dist_env()
     if rank != 0:
         return
-    P = build_problem(args.config)
+    P = build_structured(args, 1, 0) if args.config in WEAK_CONFIGS else build_problem(args.config)
     times, cores = oracle_vcycle_rate(P, n_cycles=args.steps, warmup=args.warmup)
     tot = sum(times)
     val = args.steps / tot
@@ -291,7 +326,11 @@ def run_ours(args):
     import paper_2405_05047_b200 as mg
 
     cleanup = None
-    if ws > 1:
+    if args.config in WEAK_CONFIGS:
+        # C5 weak scaling: every rank generates its own rows of every level
+        # (problems/structured.py), ~17M DOFs per rank, no data-path broadcast
+        P = build_structured(args, ws, rank)
+    elif ws > 1:
         # one generation on rank 0, arrays shared through memory-mapped .npy files
         from problems.share import shared_build
 
@@ -308,7 +347,15 @@ def run_ours(args):
     vb = 4 if args.precision == "mixed" else 8
     stream = torch.cuda.current_stream()
     t = time.time()
-    if ws > 1:
+    if args.config in WEAK_CONFIGS:
+        H = None
+        b_np = P.b
+        n_global = P.n_dof
+        comm = (ws, rank, group_key(transport), transport) if ws > 1 else None
+        solver = mg.Multigrid(P.levels, bs, omega=P.omega, nu_pre=P.nu_pre, nu_post=P.nu_post, H=None,
+                              device=dev, stream=stream, use_graphs=not args.no_graphs, precision=prec, comm=comm)
+        level_kinds = P.level_kinds
+    elif ws > 1:
         # row partition: nnz-balanced Morton splitters on every
         # level; levels with < 16k rows per rank are replicated (agglomerated)
         from problems.partition import partition

@@ -654,7 +654,13 @@ __global__ void k_scale_div(int64_t n, const double *in, const double *den, doub
 
 // Apply the previous rotations to column j, form the new one, update g and
 // the convergence flag (|g_{j+1}| <= rtol * beta0, or breakdown h_{j+1,j} = 0).
-__global__ void k_givens(GmresDev st, int j, double rtol) {
+// Device-side loop control (mg_solve's conditional-graph restart cycle): with
+// `cond`, the step also sets the switch handle to j + 1 (the next Arnoldi step)
+// and the while handle to "continue" = no stop yet and j + 1 < mm, so one graph
+// launch runs the whole cycle without a host round trip (P:346-347 did the
+// Givens part on the CPU).  out[3] = k = j + 1, the steps done so far.
+__global__ void k_givens(GmresDev st, int j, double rtol, int mm, cudaGraphConditionalHandle hw,
+                         cudaGraphConditionalHandle hs, int cond) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const int ld = st.m + 1;
   double *h = st.H + int64_t(j) * ld;
@@ -674,13 +680,20 @@ __global__ void k_givens(GmresDev st, int j, double rtol) {
   st.g[j] = st.cs[j] * st.g[j];
   const double b0 = *st.beta0;
   st.out[0] = fabs(st.g[j + 1]) / b0;
-  st.out[1] = (fabs(st.g[j + 1]) <= rtol * b0 || hn == 0.0) ? 1.0 : 0.0;
+  const bool stop = fabs(st.g[j + 1]) <= rtol * b0 || hn == 0.0;
+  st.out[1] = stop ? 1.0 : 0.0;
   st.out[2] = hn;
+  st.out[3] = double(j + 1);
+  if (cond) {
+    cudaGraphSetConditional(hs, unsigned(j + 1));
+    cudaGraphSetConditional(hw, (!stop && j + 1 < mm) ? 1u : 0u);
+  }
 }
 
 // Back substitution H(0:k,0:k) y = g(0:k).
-__global__ void k_backsolve(GmresDev st, int k) {
+__global__ void k_backsolve(GmresDev st, int k, const double *kdev) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (kdev) k = int(*kdev);  // steps done, set on the device (conditional-graph cycle)
   const int ld = st.m + 1;
   for (int i = k - 1; i >= 0; --i) {
     double s = 0.0;
@@ -691,8 +704,9 @@ __global__ void k_backsolve(GmresDev st, int k) {
 
 // x += sum_{t<k} y_t Z_t  (Z: k vectors of length n at stride ldz).
 __global__ void k_update_x(int64_t n, int k, const double *__restrict__ y, const double *__restrict__ Z, int64_t ldz,
-                           double *__restrict__ x) {
+                           double *__restrict__ x, const double *kdev = nullptr) {
   __shared__ double ys[64];
+  if (kdev) k = int(*kdev);
   if (threadIdx.x < k) ys[threadIdx.x] = y[threadIdx.x];
   __syncthreads();
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {

@@ -213,6 +213,13 @@ struct GraphExec {
   int64_t kernels = 0;
 };
 
+// A GMRES restart cycle captured as one graph with a while node around a
+// switch node over the Arnoldi steps (kernels[j]: kernel nodes of step j).
+struct CycleGraph {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<int64_t> kernels;
+};
+
 struct GraphKey {
   const double *x;
   const double *b;
@@ -251,6 +258,7 @@ struct mg_ctx_s {
   unsigned tail_grid = 0;
   std::map<GraphKey, GraphExec> graphs;
   std::map<std::tuple<int, double, int>, GraphExec> iter_graphs;  // GMRES iteration j (j, rtol, m)
+  std::map<std::tuple<int, double, int>, CycleGraph> cycle_graphs;  // GMRES restart cycle (mm, rtol, m)
   int64_t launches = 0;
   // GMRES workspace
   int gm_m = 0;
@@ -271,6 +279,8 @@ struct mg_ctx_s {
   void clear_graphs() {
     for (auto &kv : graphs) cudaGraphExecDestroy(kv.second.exec);
     for (auto &kv : iter_graphs) cudaGraphExecDestroy(kv.second.exec);
+    for (auto &kv : cycle_graphs) cudaGraphExecDestroy(kv.second.exec);
+    cycle_graphs.clear();
     graphs.clear();
     iter_graphs.clear();
   }
@@ -283,6 +293,12 @@ struct mg_ctx_s {
   int nranks() const { return tr ? tr->nranks : 1; }
   int rank() const { return tr ? tr->rank : 0; }
   bool use_graphs() const { return cfg.use_graphs && (!tr || tr->graph_safe()); }
+  // GMRES restart cycles as conditional graphs (MGB200_GMRES_LOOP=host: one
+  // graph + host sync per Arnoldi step, the round-1 path)
+  bool gmres_device_loop() const {
+    const char *e = std::getenv("MGB200_GMRES_LOOP");
+    return !(e && std::string(e) == "host");
+  }
 };
 
 namespace {
@@ -1289,6 +1305,57 @@ mg_status capture(mg_ctx_s *c, F &&body, GraphExec &out) {
   return MG_OK;
 }
 
+// Build the conditional graph of one GMRES restart cycle of mm steps:
+//   while (hw) { switch (hs) { case j: step(j) } }
+// hw (default 1) and hs (default 0) are reset at every launch; step j's
+// k_givens sets hs = j + 1 and hw = "continue", so the loop runs at most mm
+// bodies whatever the data (no unbounded device loop).
+template <class Step>
+mg_status capture_cycle(mg_ctx_s *c, int mm, Step &&step, CycleGraph &out) {
+  cudaGraph_t G = nullptr;
+  CU(cudaGraphCreate(&G, 0));
+  struct Guard {
+    cudaGraph_t &g;
+    ~Guard() {
+      if (g) cudaGraphDestroy(g);
+    }
+  } guard{G};
+  cudaGraphConditionalHandle hw, hs;
+  CU(cudaGraphConditionalHandleCreate(&hw, G, 1, cudaGraphCondAssignDefault));
+  CU(cudaGraphConditionalHandleCreate(&hs, G, 0, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams wp{};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = hw;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wn;
+  CU(cudaGraphAddNode(&wn, G, nullptr, 0, &wp));
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+  cudaGraphNodeParams sp{};
+  sp.type = cudaGraphNodeTypeConditional;
+  sp.conditional.handle = hs;
+  sp.conditional.type = cudaGraphCondTypeSwitch;
+  sp.conditional.size = unsigned(mm);
+  cudaGraphNode_t sn;
+  CU(cudaGraphAddNode(&sn, body, nullptr, 0, &sp));
+  out.kernels.assign(size_t(mm), 0);
+  for (int j = 0; j < mm; ++j) {
+    const int64_t t0 = g_tally;
+    CU(cudaStreamBeginCaptureToGraph(c->stream, sp.conditional.phGraph_out[j], nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeThreadLocal));
+    const mg_status st = step(j, true, hw, hs);
+    out.kernels[size_t(j)] = g_tally - t0;
+    g_tally = t0;
+    cudaGraph_t cap = nullptr;
+    const cudaError_t ee = cudaStreamEndCapture(c->stream, &cap);
+    if (st != MG_OK) return st;
+    if (ee != cudaSuccess) return fail(MG_ERR_CUDA, "GMRES cycle capture (step %d): %s", j, cudaGetErrorString(ee));
+  }
+  const cudaError_t ie = cudaGraphInstantiate(&out.exec, G, 0);
+  if (ie != cudaSuccess) return fail(MG_ERR_CUDA, "GMRES cycle graph instantiate: %s", cudaGetErrorString(ie));
+  return MG_OK;
+}
+
 mg_status launch_graph(mg_ctx_s *c, const GraphExec &g) {
   CU(cudaGraphLaunch(g.exec, c->stream));
   g_tally += g.kernels;
@@ -2277,52 +2344,84 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
       TRY(check_launch("gmres start"));
       int k = 0;
       bool happy = false;  // happy breakdown h_{j+1,j} = 0
-      for (int j = 0; j < mm; ++j) {
-        // one Arnoldi step: a single CUDA graph per j (V-cycle, SpMV, MGS,
-        // Givens, scaling, flag copy-out), then one host sync
-        auto step = [&]() -> mg_status {
-          double *vj = V + size_t(j) * NS, *zj = Z + size_t(j) * NS, *w = V + size_t(j + 1) * NS;
-          TRY(vcycle_rec(c, Lf, zj, vj, true));      // z_j = GMG(L, 0, v_j)
-          TRY(a_pass_spmv(c, Lf, 1.0, zj, 0.0, w, true));  // w = A z_j
-          double *hcol = g.H + size_t(j) * ld;
-          TRY(dev_dot(c, dist, N, w, V, hcol + 0, false));  // h_0j = (w, v_0)
-          for (int i = 0; i < j; ++i)                       // w -= h_ij v_i ; h_{i+1,j} = (w, v_{i+1})
-            TRY(dev_axpy_dot(c, dist, N, w, V + size_t(i) * NS, hcol + i, V + size_t(i + 1) * NS, hcol + i + 1));
-          TRY(dev_axpy_dot(c, dist, N, w, vj, hcol + j, nullptr, hcol + j + 1));  // w -= h_jj v_j ; ||w||
-          ++g_tally, mgk::k_givens<<<1, 32, 0, c->stream>>>(g, j, rtol);
-          ++g_tally, mgk::k_scale_div<<<eg, 256, 0, c->stream>>>(N, w, g.hn + j, w);  // v_{j+1} = w / h_{j+1,j}
-          TRY(check_launch("givens"));
-          CU(cudaMemcpyAsync(hst, g.out, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-          return MG_OK;
-        };
-        if (c->use_graphs()) {
-          const auto key = std::make_tuple(j, rtol, g.m);
-          auto it = c->iter_graphs.find(key);
-          if (it == c->iter_graphs.end()) {
-            GraphExec ge;
-            TRY(capture(c, step, ge));
-            it = c->iter_graphs.emplace(key, ge).first;
-          }
-          TRY(launch_graph(c, it->second));
-        } else {
-          TRY(step());
+      // one Arnoldi step j (V-cycle, SpMV, MGS, Givens, scaling); `cond`: the
+      // step runs inside the conditional-graph cycle and steers it itself
+      auto step = [&](int j, bool cond, cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hs) -> mg_status {
+        double *vj = V + size_t(j) * NS, *zj = Z + size_t(j) * NS, *w = V + size_t(j + 1) * NS;
+        TRY(vcycle_rec(c, Lf, zj, vj, true));      // z_j = GMG(L, 0, v_j)
+        TRY(a_pass_spmv(c, Lf, 1.0, zj, 0.0, w, true));  // w = A z_j
+        double *hcol = g.H + size_t(j) * ld;
+        TRY(dev_dot(c, dist, N, w, V, hcol + 0, false));  // h_0j = (w, v_0)
+        for (int i = 0; i < j; ++i)                       // w -= h_ij v_i ; h_{i+1,j} = (w, v_{i+1})
+          TRY(dev_axpy_dot(c, dist, N, w, V + size_t(i) * NS, hcol + i, V + size_t(i + 1) * NS, hcol + i + 1));
+        TRY(dev_axpy_dot(c, dist, N, w, vj, hcol + j, nullptr, hcol + j + 1));  // w -= h_jj v_j ; ||w||
+        ++g_tally, mgk::k_givens<<<1, 32, 0, c->stream>>>(g, j, rtol, mm, hw, hs, cond ? 1 : 0);
+        ++g_tally, mgk::k_scale_div<<<eg, 256, 0, c->stream>>>(N, w, g.hn + j, w);  // v_{j+1} = w / h_{j+1,j}
+        TRY(check_launch("givens"));
+        if (!cond) CU(cudaMemcpyAsync(hst, g.out, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        return MG_OK;
+      };
+      const double *kdev = nullptr;
+      if (c->use_graphs() && !dist && c->gmres_device_loop()) {
+        // the whole restart cycle as ONE graph launch: while (continue) {
+        // switch (j) { step j } }, steered by k_givens on the device; the host
+        // reads (beta, k, stop flags) once per cycle instead of once per step
+        const auto key = std::make_tuple(mm, rtol, g.m);
+        auto it = c->cycle_graphs.find(key);
+        if (it == c->cycle_graphs.end()) {
+          CycleGraph cg;
+          TRY(capture_cycle(c, mm, step, cg));
+          it = c->cycle_graphs.emplace(key, std::move(cg)).first;
         }
-        ++its;
+        CU(cudaGraphLaunch(it->second.exec, c->stream));
+        CU(cudaMemcpyAsync(hst + 4, g.out, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        kdev = g.out + 3;
+        ++g_tally, mgk::k_backsolve<<<1, 32, 0, c->stream>>>(g, 0, kdev);
+        ++g_tally, mgk::k_update_x<<<eg, 256, 0, c->stream>>>(N, 0, g.y, Z, NS, x, kdev);
+        TRY(check_launch("gmres update"));
+        TRY(a_pass_resid(c, Lf, x, b, V, true));
+        TRY(dev_dot(c, dist, N, V, V, g.beta, true));
+        CU(cudaMemcpyAsync(hst, g.beta, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         CU(cudaStreamSynchronize(c->stream));
-        k = j + 1;
-        if (!std::isfinite(hst[0])) return fail(MG_ERR_NONFINITE, "non-finite GMRES residual estimate");
-        if (hst[1] != 0.0) {  // estimate |g_{j+1}| <= rtol beta_0, or breakdown: end of the cycle
-          happy = hst[2] == 0.0;
-          break;
+        k = int(hst[4 + 3]);
+        if (k < 1 || k > mm) return fail(MG_ERR_STATE, "GMRES cycle graph ran %d steps (expected 1..%d)", k, mm);
+        for (int j = 0; j < k; ++j) g_tally += it->second.kernels[size_t(j)];
+        its += k;
+        happy = hst[4 + 1] != 0.0 && hst[4 + 2] == 0.0;
+      } else {
+        for (int j = 0; j < mm; ++j) {
+          auto step_j = [&]() { return step(j, false, 0, 0); };
+          if (c->use_graphs()) {  // a single CUDA graph per step j, then one host sync
+            const auto key = std::make_tuple(j, rtol, g.m);
+            auto it = c->iter_graphs.find(key);
+            if (it == c->iter_graphs.end()) {
+              GraphExec ge;
+              TRY(capture(c, step_j, ge));
+              it = c->iter_graphs.emplace(key, ge).first;
+            }
+            TRY(launch_graph(c, it->second));
+          } else {
+            TRY(step_j());
+          }
+          ++its;
+          CU(cudaStreamSynchronize(c->stream));
+          k = j + 1;
+          if (!std::isfinite(hst[0])) return fail(MG_ERR_NONFINITE, "non-finite GMRES residual estimate");
+          if (hst[1] != 0.0) {  // estimate |g_{j+1}| <= rtol beta_0, or breakdown: end of the cycle
+            happy = hst[2] == 0.0;
+            break;
+          }
         }
       }
-      ++g_tally, mgk::k_backsolve<<<1, 32, 0, c->stream>>>(g, k);
-      ++g_tally, mgk::k_update_x<<<eg, 256, 0, c->stream>>>(N, k, g.y, Z, NS, x);
-      TRY(check_launch("gmres update"));
-      TRY(a_pass_resid(c, Lf, x, b, V, true));
-      TRY(dev_dot(c, dist, N, V, V, g.beta, true));
-      CU(cudaMemcpyAsync(hst, g.beta, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-      CU(cudaStreamSynchronize(c->stream));
+      if (!kdev) {
+        ++g_tally, mgk::k_backsolve<<<1, 32, 0, c->stream>>>(g, k, nullptr);
+        ++g_tally, mgk::k_update_x<<<eg, 256, 0, c->stream>>>(N, k, g.y, Z, NS, x, nullptr);
+        TRY(check_launch("gmres update"));
+        TRY(a_pass_resid(c, Lf, x, b, V, true));
+        TRY(dev_dot(c, dist, N, V, V, g.beta, true));
+        CU(cudaMemcpyAsync(hst, g.beta, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+      }
       rel = hst[0] / beta0;
       if (!std::isfinite(rel)) return fail(MG_ERR_NONFINITE, "non-finite residual");
       // converged on the TRUE residual (or a happy breakdown); an estimate below

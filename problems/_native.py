@@ -31,6 +31,12 @@ def lib():
         L.asm_condensed.restype = ctypes.c_int
         L.asm_condensed.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, P,
                                     P, P, P, ctypes.c_int, P, P, ctypes.c_int, ctypes.c_int, P, P, P]
+        L.asm_structured.restype = ctypes.c_int
+        L.asm_structured.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, P, P, ctypes.c_int,
+                                     ctypes.c_int64, ctypes.c_int64, ctypes.c_int, P, P, P, P]
+        L.tr_structured.restype = ctypes.c_int
+        L.tr_structured.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, P, ctypes.c_int64,
+                                    ctypes.c_int64, ctypes.c_int, P, P, P]
         _lib = L
     return _lib
 

@@ -183,3 +183,141 @@ int asm_condensed(i64 n_nodes, int bs, int nloc, i64 n_elem, const i64 *conn,
   free(sl_w);
   return err ? -1 : 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Structured (uniform box-cell) Q1 assembly of the C5 workload, any subset  */
+/* of rows -- the per-rank generator of the weak-scaling runs.               */
+/*                                                                          */
+/* Grid of nx*ny*nz equal box cells, nodes numbered lexicographically,      */
+/* id = i + (nx+1)*(j + (ny+1)*k).  Every cell has the same element matrix   */
+/* Ae ((8*bs)^2, node-major, corner c has bit a = offset along axis a, the   */
+/* layout of problems/fem.py).  Row m = (i,j,k) collects Ae[a_m, b] of every */
+/* cell around it (cells in (ez, ey, ex) ascending order), columns in        */
+/* ascending id.  Dirichlet on boundary nodes for the components flagged in  */
+/* bmask (symmetric elimination, reading Z9): with g = 1 on component       */
+/* lid_comp of the nodes of the face k = 0 (the cavity lid) and 0 elsewhere, */
+/*   b_m -= A_mn g_n (all r), then rows/cols of constrained components are   */
+/* zeroed, identity on their diagonal, and b_m = g_m there.  b (rows r0..r1, */
+/* raw right-hand side) is updated in place when non-NULL.                   */
+/* pass 0: row_ptr (r1-r0+1); pass 1: col (global ids), val, b.             */
+/* ------------------------------------------------------------------------ */
+static int on_bnd(i64 i, i64 j, i64 k, i64 nx, i64 ny, i64 nz) {
+  return i == 0 || j == 0 || k == 0 || i == nx || j == ny || k == nz;
+}
+
+int asm_structured(i64 nx, i64 ny, i64 nz, int bs, const double *Ae, const unsigned char *bmask, int lid_comp,
+                   i64 r0, i64 r1, int pass, i64 *row_ptr, i64 *col, double *val, double *b) {
+  const i64 px = nx + 1, plane = (nx + 1) * (ny + 1);
+  const int nl = 8 * bs, bb = bs * bs;
+  if (pass == 0) {
+    row_ptr[0] = 0;
+    for (i64 m = r0; m < r1; ++m) {
+      const i64 k = m / plane, j = (m % plane) / px, i = m % px;
+      const i64 cx = 1 + (i > 0) + (i < nx), cy = 1 + (j > 0) + (j < ny), cz = 1 + (k > 0) + (k < nz);
+      row_ptr[m - r0 + 1] = row_ptr[m - r0] + cx * cy * cz;
+    }
+    return 0;
+  }
+#pragma omp parallel for schedule(static, 4096)
+  for (i64 m = r0; m < r1; ++m) {
+    const i64 k = m / plane, j = (m % plane) / px, i = m % px;
+    const i64 lx = i > 0, ly = j > 0, lz = k > 0;
+    const i64 cx = 1 + lx + (i < nx), cy = 1 + ly + (j < ny);
+    const i64 base = row_ptr[m - r0];
+    const i64 cnt = row_ptr[m - r0 + 1] - base;
+    double *v = val + (size_t)base * bb;
+    memset(v, 0, sizeof(double) * (size_t)cnt * bb);
+    for (i64 dz = -lz; dz <= (k < nz); ++dz)
+      for (i64 dy = -ly; dy <= (j < ny); ++dy)
+        for (i64 dx = -lx; dx <= (i < nx); ++dx)
+          col[base + ((dz + lz) * cy + (dy + ly)) * cx + (dx + lx)] = (i + dx) + px * ((j + dy) + (ny + 1) * (k + dz));
+    for (i64 ez = k - 1; ez <= k; ++ez) {
+      if (ez < 0 || ez >= nz) continue;
+      for (i64 ey = j - 1; ey <= j; ++ey) {
+        if (ey < 0 || ey >= ny) continue;
+        for (i64 ex = i - 1; ex <= i; ++ex) {
+          if (ex < 0 || ex >= nx) continue;
+          const int am = (int)((i - ex) | ((j - ey) << 1) | ((k - ez) << 2));
+          for (int bc = 0; bc < 8; ++bc) {
+            const i64 dx = ex + (bc & 1) - i, dy = ey + ((bc >> 1) & 1) - j, dz = ez + ((bc >> 2) & 1) - k;
+            double *blk = v + (size_t)(((dz + lz) * cy + (dy + ly)) * cx + (dx + lx)) * bb;
+            for (int r = 0; r < bs; ++r)
+              for (int c = 0; c < bs; ++c) blk[r * bs + c] += Ae[(size_t)(am * bs + r) * nl + bc * bs + c];
+          }
+        }
+      }
+    }
+    /* Dirichlet elimination */
+    const int bm = on_bnd(i, j, k, nx, ny, nz);
+    for (i64 t = 0; t < cnt; ++t) {
+      const i64 n = col[base + t];
+      const i64 nk = n / plane, nj = (n % plane) / px, ni = n % px;
+      const int bn = on_bnd(ni, nj, nk, nx, ny, nz);
+      double *blk = v + (size_t)t * bb;
+      if (b && bn) {
+        for (int r = 0; r < bs; ++r) {
+          double corr = 0.0;
+          for (int c = 0; c < bs; ++c) {
+            const double gc = (bmask[c] && c == lid_comp && nk == 0) ? 1.0 : 0.0;
+            corr += blk[r * bs + c] * gc;
+          }
+          b[(m - r0) * bs + r] += -corr;
+        }
+      }
+      if (bm || bn)
+        for (int r = 0; r < bs; ++r)
+          for (int c = 0; c < bs; ++c)
+            if ((bm && bmask[r]) || (bn && bmask[c])) blk[r * bs + c] = 0.0;
+      if (n == m && bm)
+        for (int c = 0; c < bs; ++c)
+          if (bmask[c]) blk[c * bs + c] = 1.0;
+    }
+    if (b && bm)
+      for (int c = 0; c < bs; ++c)
+        if (bmask[c]) b[(m - r0) * bs + c] = (c == lid_comp && k == 0) ? 1.0 : 0.0;
+  }
+  return 0;
+}
+
+/* Trilinear prolongation of the structured grid (fine nx = 2 * coarse nx),
+ * rows r0..r1 of the fine grid, per-component weights (wpe = bs) with the
+ * Dirichlet components of boundary nodes dropped on both sides (Pi_f E Pi_c,
+ * reading G6/Z8); entries whose weights are all zero are omitted.  Columns in
+ * ascending coarse id.  pass 0: row_ptr; pass 1: col, w [nnz*bs]. */
+int tr_structured(i64 nxf, i64 nyf, i64 nzf, int bs, const unsigned char *bmask, i64 r0, i64 r1, int pass,
+                  i64 *row_ptr, i64 *col, double *w) {
+  const i64 px = nxf + 1, plane = (nxf + 1) * (nyf + 1);
+  const i64 nxc = nxf / 2, nyc = nyf / 2, nzc = nzf / 2, pxc = nxc + 1, planec = (nxc + 1) * (nyc + 1);
+  if (pass == 0) row_ptr[0] = 0;
+#pragma omp parallel for schedule(static, 4096) if (pass)
+  for (i64 m = r0; m < r1; ++m) {
+    const i64 k = m / plane, j = (m % plane) / px, i = m % px;
+    const int bf = on_bnd(i, j, k, nxf, nyf, nzf);
+    i64 ci[2], cj[2], ck[2];
+    double wi[2], wj[2], wk[2];
+    int ni = 1, nj = 1, nk = 1;
+    if (i & 1) ci[0] = (i - 1) / 2, ci[1] = (i + 1) / 2, wi[0] = wi[1] = 0.5, ni = 2; else ci[0] = i / 2, wi[0] = 1.0;
+    if (j & 1) cj[0] = (j - 1) / 2, cj[1] = (j + 1) / 2, wj[0] = wj[1] = 0.5, nj = 2; else cj[0] = j / 2, wj[0] = 1.0;
+    if (k & 1) ck[0] = (k - 1) / 2, ck[1] = (k + 1) / 2, wk[0] = wk[1] = 0.5, nk = 2; else ck[0] = k / 2, wk[0] = 1.0;
+    i64 t = pass ? row_ptr[m - r0] : 0;
+    for (int a = 0; a < nk; ++a)
+      for (int bq = 0; bq < nj; ++bq)
+        for (int c = 0; c < ni; ++c) {
+          const double wt = wk[a] * wj[bq] * wi[c];
+          const int bc = on_bnd(ci[c], cj[bq], ck[a], nxc, nyc, nzc);
+          int any = 0;
+          for (int q = 0; q < bs; ++q)
+            if (!((bf || bc) && bmask[q])) any = 1;
+          if (!any) continue;
+          if (pass) {
+            col[t] = ci[c] + pxc * cj[bq] + planec * ck[a];
+            for (int q = 0; q < bs; ++q) w[(size_t)t * bs + q] = ((bf || bc) && bmask[q]) ? 0.0 : wt;
+          }
+          ++t;
+        }
+    if (!pass) row_ptr[m - r0 + 1] = t;  /* count; prefix-summed by the caller */
+  }
+  if (!pass)
+    for (i64 m = r0; m < r1; ++m) row_ptr[m - r0 + 1] += row_ptr[m - r0];
+  return 0;
+}

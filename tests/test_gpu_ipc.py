@@ -72,7 +72,8 @@ def test_ipc_processes_vcycle_bitwise_and_gmres(name, P, tmp_path):
     assert len(its) == 1 and all(bool(r["conv"]) for r in res)
     xsol = np.concatenate([r["xs"] for r in res])
     xe, ite, _, _ = oracle.gmres(h, Pr.b, rtol=1e-10)
-    xe = oracle.apply_H(Pr.fine.H, xe, bs)
+    from oracle.mg import apply_H
+    xe = apply_H(Pr.fine.H, xe, bs)
     assert abs(its.pop() - ite) <= 1
     assert np.linalg.norm(xsol - xe) <= 1e-8 * np.linalg.norm(xe)
     # the per-level split reports halo time on the distributed levels
@@ -92,4 +93,38 @@ def test_ipc_smoothing_coarse_mode(tmp_path):
     m.mg_vcycle(s.ctx, xs, dev(Pr.b))
     got = np.concatenate([r["x"] for r in res])
     assert np.array_equal(got, host(xs))
+    s.close()
+
+
+@pytest.mark.parametrize("P", [1, 2, 3])
+def test_ipc_structured_c5_per_rank_generation(P, tmp_path):
+    """C5 weak-scaling path: each process generates only its own rows
+    (problems/structured.py) -- the distributed V-cycle equals the single-GPU
+    V-cycle of the globally generated system bit for bit, both match the
+    oracle, and GMRES+MG agrees +-1 iteration with the oracle."""
+    import paper_2405_05047_b200 as m
+    from problems import structured as S
+    R = 3
+    res = run_procs(f"c5w{R}", P, tmp_path, min_rows=8) if P > 1 else None
+    glob, b, _ = S.build_rank(1, 0, root=(2, 2, 4), R=R)
+    n_dof = glob[-1].n * 4
+    x0 = np.random.default_rng(5).standard_normal(n_dof)
+    s = build_gpu(glob, 4, omega=S.OMEGA, H=None)
+    xs = dev(x0)
+    m.mg_vcycle(s.ctx, xs, dev(b))
+    h = oracle.MgHierarchy.from_arrays(glob, omega=S.OMEGA)
+    exp = oracle.vcycle(h, R, x0.copy(), b)
+    assert np.linalg.norm(host(xs) - exp) <= TOL_VCYCLE * np.linalg.norm(exp)
+    xe, ite, _, _ = oracle.gmres(h, b, rtol=1e-10)
+    if res is None:
+        x = dev(np.zeros(n_dof))
+        st, its, rel, conv = m.mg_solve(s.ctx, x, dev(b), rtol=1e-10)
+        assert conv and abs(its - ite) <= 1 and np.linalg.norm(host(x) - xe) <= 1e-8 * np.linalg.norm(xe)
+    else:
+        got = np.concatenate([r["x"] for r in res])
+        assert np.array_equal(got, host(xs))
+        its = {int(r["its"]) for r in res}
+        assert len(its) == 1 and abs(its.pop() - ite) <= 1
+        xsol = np.concatenate([r["xs"] for r in res])
+        assert np.linalg.norm(xsol - xe) <= 1e-8 * np.linalg.norm(xe)
     s.close()

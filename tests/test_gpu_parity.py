@@ -434,3 +434,26 @@ def test_coarse_tail_kernel_bitidentical(name, coarse_mode, precision, monkeypat
     for o in outs[1:]:
         assert np.array_equal(outs[0][0], o[0])
         assert outs[0][1] == o[1] and np.array_equal(outs[0][2], o[2])
+
+
+@pytest.mark.parametrize("name", ["c1", "c3_small", "c5_small", "e6_face_l2"])
+def test_gmres_device_loop_equals_host_loop(name, monkeypatch):
+    """The restart cycle as one conditional graph (while + switch steered by
+    k_givens on the device) computes exactly what the per-step host loop
+    computes: same iterates bit for bit, same iteration counts."""
+    import paper_2405_05047_b200 as m
+    lv, bs, om, b, H = case(name)
+    out = []
+    for mode in ("host", "device"):
+        monkeypatch.setenv("MGB200_GMRES_LOOP", mode)
+        mg = build_gpu(lv, bs, omega=om, H=H)
+        res = []
+        for restart, max_iter, rtol in ((30, 200, 1e-10), (3, 200, 1e-10), (4, 7, 1e-14)):
+            x = dev(np.zeros(lv[-1].n * bs))
+            st, its, rel, conv = m.mg_solve(mg.ctx, x, dev(b), restart=restart, max_iter=max_iter, rtol=rtol)
+            res.append((host(x), its, rel, conv, st))
+        out.append(res)
+        mg.close()
+    for (xh, ih, rh, ch, sh), (xd, idv, rd, cd, sd) in zip(*out):
+        assert ih == idv and ch == cd and sh == sd
+        assert np.array_equal(xh, xd) and rh == rd
