@@ -53,6 +53,20 @@ int mgi_sell_fill_f32(int64_t n, const int64_t *row_ptr, const int64_t *col_in, 
                       int vpe, int sigma, int64_t *slice_ptr, int32_t *perm, int32_t *col,
                       float *val);
 
+/* Transfer layout (P_l, R_l): SELL-C-sigma with C = 32 / bs rows per
+ * slice, so a warp's lane (r, q) = (lane / bs, lane % bs) handles component q
+ * of the slice's row r and the bs components of one gathered node come from
+ * ONE load instruction (adjacent lanes, adjacent words).  Rows are stably
+ * sorted by length inside windows of sigma rows (sigma % C == 0); entry k of
+ * slice-row r sits at slice_ptr[s] + k*C + r; padding repeats the row's last
+ * column with weight 0.  Weights are stored as fp32 -- exact for the dyadic
+ * transfer weights (G6): mgi_tsell_fill returns 2 (nothing written) when some
+ * weight is not exactly representable, and the caller keeps the fp64 SELL-32
+ * layout.  w[e*wpe + t]; perm[n_slices*C] (-1 = padding). */
+int mgi_tsell_size(int64_t n, const int64_t *row_ptr, int C, int sigma, int64_t *n_slices, int64_t *n_entries);
+int mgi_tsell_fill(int64_t n, const int64_t *row_ptr, const int64_t *col_in, const double *w_in, int wpe, int C,
+                   int sigma, int64_t *slice_ptr, int32_t *perm, int32_t *col, float *w);
+
 /* Value-update map of a SELL-32-sigma layout (mg_update_matrix): map[k] = the
  * SELL entry e holding original CSR entry k (k < row_ptr[n]); row_pos[r] =
  * slice*32 + lane of row r (row_pos may be NULL). */

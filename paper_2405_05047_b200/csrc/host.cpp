@@ -181,6 +181,66 @@ int mgi_sell_fill_f32(int64_t n, const int64_t *rp, const int64_t *col_in, const
   return sell_fill<float>(n, rp, col_in, val_in, vpe, sigma, slice_ptr, perm, col, val);
 }
 
+int mgi_tsell_size(int64_t n, const int64_t *rp, int C, int sigma, int64_t *n_slices, int64_t *n_entries) {
+  if (n < 0 || C < 1 || C > 32 || sigma < C || sigma % C) return MG_ERR_INVALID_ARG;
+  const int64_t ns = (n + C - 1) / C;
+  const int64_t nw = (n + sigma - 1) / sigma;
+  int64_t total = 0;
+#pragma omp parallel for schedule(static) reduction(+ : total)
+  for (int64_t w = 0; w < nw; ++w) {
+    const int64_t r0 = w * sigma, r1 = std::min<int64_t>(n, r0 + sigma);
+    std::vector<int64_t> len(r1 - r0);
+    for (int64_t i = r0; i < r1; ++i) len[i - r0] = rp[i + 1] - rp[i];
+    std::sort(len.begin(), len.end(), std::greater<int64_t>());
+    for (size_t s = 0; s < len.size(); s += size_t(C)) total += len[s] * C;
+  }
+  *n_slices = ns;
+  *n_entries = total;
+  return 0;
+}
+
+int mgi_tsell_fill(int64_t n, const int64_t *rp, const int64_t *col_in, const double *w_in, int wpe, int C, int sigma,
+                   int64_t *slice_ptr, int32_t *perm, int32_t *col, float *w) {
+  if (n < 0 || C < 1 || C > 32 || sigma < C || sigma % C || wpe < 1) return MG_ERR_INVALID_ARG;
+  if (n >= (int64_t(1) << 31)) return MG_ERR_DIMENSION;
+  const int64_t nnz = rp[n];
+  for (int64_t t = 0; t < nnz * wpe; ++t)
+    if (double(float(w_in[t])) != w_in[t]) return 2;  // not exact in fp32: caller keeps the fp64 layout
+  const int64_t ns = (n + C - 1) / C;
+  const int64_t nw = (n + sigma - 1) / sigma;
+#pragma omp parallel for schedule(static)
+  for (int64_t wi = 0; wi < nw; ++wi) {
+    const int64_t r0 = wi * sigma, r1 = std::min<int64_t>(n, r0 + sigma);
+    std::vector<int32_t> idx(r1 - r0);
+    std::iota(idx.begin(), idx.end(), int32_t(r0));
+    std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) {
+      return (rp[a + 1] - rp[a]) > (rp[b + 1] - rp[b]);
+    });
+    std::copy(idx.begin(), idx.end(), perm + r0);
+  }
+  for (int64_t t = n; t < ns * C; ++t) perm[t] = -1;
+  slice_ptr[0] = 0;
+  for (int64_t s = 0; s < ns; ++s) {
+    const int32_t r = perm[s * C];
+    slice_ptr[s + 1] = slice_ptr[s] + (r >= 0 ? rp[r + 1] - rp[r] : 0) * C;
+  }
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t s = 0; s < ns; ++s) {
+    const int64_t len = (slice_ptr[s + 1] - slice_ptr[s]) / C;
+    for (int q = 0; q < C; ++q) {
+      const int32_t r = perm[s * C + q];
+      const int64_t rl = r >= 0 ? rp[r + 1] - rp[r] : 0;
+      for (int64_t k = 0; k < len; ++k) {
+        const int64_t e = slice_ptr[s] + k * C + q;
+        const bool real = k < rl;
+        col[e] = real ? int32_t(col_in[rp[r] + k]) : (rl > 0 ? int32_t(col_in[rp[r] + rl - 1]) : 0);
+        for (int t = 0; t < wpe; ++t) w[e * wpe + t] = real ? float(w_in[(rp[r] + k) * wpe + t]) : 0.0f;
+      }
+    }
+  }
+  return 0;
+}
+
 int mgi_sell_entry_map(int64_t n, const int64_t *rp, const int64_t *slice_ptr, const int32_t *perm, int64_t *map,
                        int32_t *row_pos) {
   const int64_t ns = (n + kSlice - 1) / kSlice;

@@ -362,6 +362,85 @@ __global__ void __launch_bounds__(kCta) k_transfer(Sell T, const double *__restr
   transfer_task<BS, WPE, ACCUM, STREAM, HALO, KS, false>(T, blockIdx.x, in, ing, n_own, out);
 }
 
+// Transfer on the SELL-C layout of mgi_tsell_fill (C = 32 / BS rows per
+// slice): lane (r, q) = (lane / BS, lane % BS) accumulates component q of the
+// slice's row r, so the BS components of a gathered node are ONE warp load
+// instruction over adjacent lanes (one L1 wavefront per node instead of BS:
+// the SELL-32 transfer was bound by L1 data-pipe wavefronts, ncu r2a).  Column
+// and weight of an entry are one 8-byte load (int2 {col, fp32 weight bits}:
+// the dyadic weights are exact in fp32) when WPE = 1; per-component weights
+// (WPE = BS) are fp32 planes indexed e*BS + q, contiguous over the warp.
+// Accumulation order per row and split-k combine as k_transfer: bit-identical.
+struct TSell {
+  const int64_t *slice_ptr;  // [n_slices+1], multiples of C
+  const int32_t *perm;       // [n_slices*C] row of each slice position, -1 = padding
+  const int2 *cw;            // WPE = 1: {col, __float_as_int(w)} per entry
+  const int32_t *col;        // WPE = BS: columns
+  const float *w;            // WPE = BS: [entries*BS]
+  int64_t n_slices;
+};
+
+template <int BS, int WPE, bool ACCUM, bool HALO, int KS>
+__global__ void __launch_bounds__(kCta) k_tsell(TSell T, const double *__restrict__ in,
+                                                const double *__restrict__ ing, int n_own,
+                                                double *__restrict__ out) {
+  constexpr int C = 32 / BS;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int sub = KS == 1 ? 0 : wid % KS;
+  const int64_t s = int64_t(blockIdx.x) * (kWarpsPerCta / KS) + wid / KS;
+  const bool live = s < T.n_slices;
+  if (KS == 1 && !live) return;
+  const int r = lane / BS, q = lane - r * BS;
+  const bool act = live && r < C;
+  double acc[1] = {0.0};
+  int row = -1;
+  if (act) {
+    const int64_t e0 = T.slice_ptr[s], len = (T.slice_ptr[s + 1] - e0) / C;
+    row = T.perm[s * C + r];
+    const int64_t eb = e0 + r;
+    int64_t k = sub;
+    constexpr int UB = 4;  // loads of 4 entries in flight before their use (summed in order)
+    for (; k + (UB - 1) * KS < len; k += UB * KS) {
+      int c[UB];
+      double w[UB], v[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int64_t e = eb + (k + u * KS) * C;
+        if constexpr (WPE == 1) {
+          const int2 t = __ldg(T.cw + e);
+          c[u] = t.x;
+          w[u] = double(__int_as_float(t.y));
+        } else {
+          c[u] = __ldg(T.col + e);
+          w[u] = double(__ldg(T.w + e * BS + q));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u) v[u] = __ldg(col_ptr<BS, HALO>(in, ing, n_own, c[u]) + q);
+#pragma unroll
+      for (int u = 0; u < UB; ++u) acc[0] = fma(w[u], v[u], acc[0]);
+    }
+    for (; k < len; k += KS) {
+      const int64_t e = eb + k * C;
+      int c;
+      double w;
+      if constexpr (WPE == 1) {
+        const int2 t = __ldg(T.cw + e);
+        c = t.x;
+        w = double(__int_as_float(t.y));
+      } else {
+        c = __ldg(T.col + e);
+        w = double(__ldg(T.w + e * BS + q));
+      }
+      acc[0] = fma(w, __ldg(col_ptr<BS, HALO>(in, ing, n_own, c) + q), acc[0]);
+    }
+  }
+  if (!combine_split<1, KS>(acc, wid, sub, lane)) return;
+  if (!act || row < 0) return;
+  const int64_t o = int64_t(row) * BS + q;
+  out[o] = ACCUM ? out[o] + acc[0] : acc[0];
+}
+
 // Coarse solve y = A_0^{-1} d with the dense inverse (row stride ld, even,
 // zero padded): one warp per row, 16-byte loads, shuffle reduction.
 template <bool CG>

@@ -79,6 +79,18 @@ struct SellOp {
   mgk::Sell view() const { return mgk::Sell{slice_ptr.p, perm.p, col.p, val.p, n_slices, valf.p}; }
 };
 
+// Transfer operator in the SELL-C layout of mgi_tsell_fill (k_tsell).
+struct TSellOp {
+  DevArray<int64_t> slice_ptr;
+  DevArray<int32_t> perm, col;
+  DevArray<int2> cw;
+  DevArray<float> w;
+  int64_t n_slices = 0, n_entries = 0;
+  int C = 32, wpe = 1, ks = 1;
+  bool set = false;
+  mgk::TSell view() const { return mgk::TSell{slice_ptr.p, perm.p, cw.p, col.p, w.p, n_slices}; }
+};
+
 // Operators above this size are read with evict-first loads (MGB200_STREAM_MB overrides
 // the default kStreamBytes; experiment knob for L2 residency of mid-sized operators).
 size_t stream_bytes() {
@@ -126,6 +138,45 @@ mg_status build_sell(SellOp &op, int64_t n, const int64_t *rp, const int64_t *co
   op.f32 = f32;
   op.stream = size_t(ne) * ((f32 ? 4 : 8) * vpe + 4) > stream_bytes();
   op.set = true;
+  return MG_OK;
+}
+
+// Transfer layout SELL-C (C = 32 / bs); leaves T unset (fp64 SELL-32 path)
+// when a weight is not exact in fp32 or MGB200_TSELL=0.
+mg_status build_tsell(TSellOp &T, int64_t n, const int64_t *rp, const int64_t *col, const double *w, int wpe, int bs) {
+  T = TSellOp();
+  const char *e = std::getenv("MGB200_TSELL");
+  if (e && e[0] == '0') return MG_OK;
+  const int C = 32 / bs;
+  const int sigma = C * ((kSigma + C - 1) / C);
+  int64_t ns = 0, ne = 0;
+  int st = mgi_tsell_size(n, rp, C, sigma, &ns, &ne);
+  if (st) return fail(mg_status(st), "transfer layout: invalid input");
+  std::vector<int64_t> sp(ns + 1);
+  std::vector<int32_t> perm(ns * C), cl(ne);
+  std::vector<float> wf(ne * wpe);
+  st = mgi_tsell_fill(n, rp, col, w, wpe, C, sigma, sp.data(), perm.data(), cl.data(), wf.data());
+  if (st == 2) return MG_OK;  // weights not exact in fp32: keep the fp64 layout
+  if (st) return fail(mg_status(st), "transfer layout: fill failed (%d)", st);
+  TRY(T.slice_ptr.upload(sp.data(), sp.size()));
+  TRY(T.perm.upload(perm.data(), perm.size()));
+  if (wpe == 1) {
+    std::vector<int2> cw(ne);
+    for (int64_t t = 0; t < ne; ++t) {
+      int wb;
+      std::memcpy(&wb, &wf[t], sizeof wb);
+      cw[t] = make_int2(cl[t], wb);
+    }
+    TRY(T.cw.upload(cw.data(), cw.size()));
+  } else {
+    TRY(T.col.upload(cl.data(), cl.size()));
+    TRY(T.w.upload(wf.data(), wf.size()));
+  }
+  T.n_slices = ns;
+  T.n_entries = ne;
+  T.C = C;
+  T.wpe = wpe;
+  T.set = true;
   return MG_OK;
 }
 
@@ -180,6 +231,7 @@ struct Level {
   std::vector<double> val0;
   bool dinv_ready = false;
   SellOp P, R;  // P_{l-1}: level l-1 -> l (rows: owned fine rows), R_{l-1} = P^T (rows: r_row0 ...)
+  TSellOp Pt, Rt;  // the same operators in the SELL-C layout (fp32-exact weights), used when set
   Halo hp;      // ghosts of the coarse vector y for P (coarse level distributed)
   Halo hr;      // ghosts of the fine vector r for R (this level distributed)
   int64_t r_row0 = 0, r_rows = 0;  // coarse rows produced by the local R
@@ -463,6 +515,39 @@ mg_status launch_transfer(int bs, bool acc, const SellOp &T, In in, double *out,
     default: return fail(MG_ERR_INVALID_ARG, "block size %d not supported", bs);
   }
   return check_launch(acc ? "prolong-add" : "transfer");
+}
+
+template <int BS, int WPE, bool ACC, bool HALO>
+void launch_tsell_h(const TSellOp &T, In in, double *out, cudaStream_t st) {
+  const unsigned g = grid_for_slices(T.n_slices, T.ks);
+  if (T.ks > 1)
+    ++g_tally, mgk::k_tsell<BS, WPE, ACC, HALO, 4><<<g, mgk::kCta, 0, st>>>(T.view(), in.x, in.xg, in.n_own, out);
+  else
+    ++g_tally, mgk::k_tsell<BS, WPE, ACC, HALO, 1><<<g, mgk::kCta, 0, st>>>(T.view(), in.x, in.xg, in.n_own, out);
+}
+
+template <int BS, bool ACC>
+void launch_tsell_bs(const TSellOp &T, In in, double *out, cudaStream_t st) {
+  if (T.n_slices == 0) return;
+  if (T.wpe == 1 || BS == 1) {
+    if (in.xg) launch_tsell_h<BS, 1, ACC, true>(T, in, out, st);
+    else launch_tsell_h<BS, 1, ACC, false>(T, in, out, st);
+  } else {
+    if (in.xg) launch_tsell_h<BS, BS, ACC, true>(T, in, out, st);
+    else launch_tsell_h<BS, BS, ACC, false>(T, in, out, st);
+  }
+}
+
+mg_status launch_tsell(int bs, bool acc, const TSellOp &T, In in, double *out, cudaStream_t st) {
+  switch (bs) {
+    case 1: acc ? launch_tsell_bs<1, true>(T, in, out, st) : launch_tsell_bs<1, false>(T, in, out, st); break;
+    case 2: acc ? launch_tsell_bs<2, true>(T, in, out, st) : launch_tsell_bs<2, false>(T, in, out, st); break;
+    case 3: acc ? launch_tsell_bs<3, true>(T, in, out, st) : launch_tsell_bs<3, false>(T, in, out, st); break;
+    case 4: acc ? launch_tsell_bs<4, true>(T, in, out, st) : launch_tsell_bs<4, false>(T, in, out, st); break;
+    case 6: acc ? launch_tsell_bs<6, true>(T, in, out, st) : launch_tsell_bs<6, false>(T, in, out, st); break;
+    default: return fail(MG_ERR_INVALID_ARG, "block size %d not supported", bs);
+  }
+  return check_launch(acc ? "prolong-add (tsell)" : "restrict (tsell)");
 }
 
 // profiling marks: tag = level (compute), 100 + level (halo), 200 + level (agglomeration)
@@ -1142,7 +1227,8 @@ mg_status do_restrict(mg_ctx_s *c, int l, const double *r, double *d) {
   Level &L = c->lv[l];
   const int bs = c->bs();
   TRY(halo_exchange(c, L.hr, r));
-  TRY(launch_transfer(bs, false, L.R, in_of(L, L.hr, r), d + L.r_row0 * bs, c->stream));
+  if (L.Rt.set) TRY(launch_tsell(bs, false, L.Rt, in_of(L, L.hr, r), d + L.r_row0 * bs, c->stream));
+  else TRY(launch_transfer(bs, false, L.R, in_of(L, L.hr, r), d + L.r_row0 * bs, c->stream));
   if (L.agglomerate) {
     mark(c, 200 + l);
     TRY(c->tr->allgatherv(d + L.r_row0 * bs, d, L.ag_counts, L.ag_displs, c->stream));
@@ -1156,7 +1242,9 @@ mg_status do_prolong(mg_ctx_s *c, int l, const double *y, double *x) {
   Level &L = c->lv[l];
   Level &C = c->lv[l - 1];
   TRY(halo_exchange(c, L.hp, y));
-  return launch_transfer(c->bs(), true, L.P, In{y, L.hp.active ? L.hp.ghost.p : nullptr, int(C.n)}, x, c->stream);
+  const In in{y, L.hp.active ? L.hp.ghost.p : nullptr, int(C.n)};
+  if (L.Pt.set) return launch_tsell(c->bs(), true, L.Pt, in, x, c->stream);
+  return launch_transfer(c->bs(), true, L.P, in, x, c->stream);
 }
 
 mg_status vanka_sweep(mg_ctx_s *c, int l, double *x, const double *b, bool zero) {
@@ -1801,6 +1889,8 @@ mg_status mg_set_transfer(mg_ctx c, int fine_level, const int64_t *row_ptr, cons
   }
   TRY(build_sell(L.R, L.r_rows, rrp.data(), rcl.data(), rv.data(), wpe));
   L.R.ks = 4;  // R rows gather 9-27+ fine entries: split them over 4 warps
+  TRY(build_tsell(L.Rt, L.r_rows, rrp.data(), rcl.data(), rv.data(), wpe, c->bs()));
+  L.Rt.ks = 4;
   // ---- P: columns are coarse rows ------------------------------------------
   if (C.dist) {
     std::vector<int64_t> ghosts;
@@ -1810,6 +1900,7 @@ mg_status mg_set_transfer(mg_ctx c, int fine_level, const int64_t *row_ptr, cons
     L.hp = Halo();
   }
   TRY(build_sell(L.P, L.n, rp.data(), cl.data(), v.data(), wpe));
+  TRY(build_tsell(L.Pt, L.n, rp.data(), cl.data(), v.data(), wpe, c->bs()));
   L.wpe = wpe;
   L.nnz_p = nnz;
   c->invalidate();

@@ -135,6 +135,68 @@ def test_sell_transfer_layout_wpe():
     assert c.min() >= 0 and c.max() < nc          # rectangular: every stored column < n_coarse
 
 
+def _tsell(rp, col, w, wpe, C, sigma):
+    L = _lib()
+    n = len(rp) - 1
+    ns, ne = ctypes.c_int64(), ctypes.c_int64()
+    assert L.mgi_tsell_size(ctypes.c_int64(n), _p(rp), C, sigma, ctypes.byref(ns), ctypes.byref(ne)) == 0
+    sp = np.zeros(ns.value + 1, np.int64)
+    perm = np.zeros(ns.value * C, np.int32)
+    c = np.zeros(ne.value, np.int32)
+    wf = np.zeros(ne.value * wpe, np.float32)
+    st = L.mgi_tsell_fill(ctypes.c_int64(n), _p(rp), _p(col), _p(w), wpe, C, sigma, _p(sp), _p(perm), _p(c), _p(wf))
+    return st, sp, perm, c, wf
+
+
+@pytest.mark.parametrize("name,C,sigma", [("c3_small", 10, 40), ("c3_small", 10, 4100), ("c5_small", 8, 64),
+                                           ("c2_small", 32, 4096)])
+def test_transfer_sellc_layout_bitexact(name, C, sigma):
+    """SELL-C transfer layout (mgi_tsell_fill, include/mg_internal.h): every
+    P and R = P^T row reappears entry by entry in CSR order at
+    slice_ptr[s] + k*C + r, weights bit-exact in fp32 (dyadic, G6), padding
+    with weight 0 at an in-range column; rows are a permutation within the
+    sigma windows."""
+    P = problem(name)
+    L = _lib()
+    lv = P.levels[-1]
+    nc = P.levels[-2].n
+    rp, col, w = lv.P
+    wpe = lv.wpe
+    rrp = np.zeros(nc + 1, np.int64)
+    rcol = np.zeros(len(col), np.int64)
+    rw = np.zeros(len(w))
+    assert L.mgi_csr_transpose(ctypes.c_int64(lv.n), ctypes.c_int64(nc), _p(rp), _p(col), _p(w), wpe,
+                               _p(rrp), _p(rcol), _p(rw)) == 0
+    for (trp, tcol, tw, n, ncols) in ((rp, col, w, lv.n, nc), (rrp, rcol, rw, nc, lv.n)):
+        st, sp, perm, c, wf = _tsell(trp, tcol, np.ascontiguousarray(tw), wpe, C, sigma)
+        assert st == 0
+        seen = np.zeros(n, bool)
+        for s in range(len(sp) - 1):
+            ln = (sp[s + 1] - sp[s]) // C
+            assert (sp[s + 1] - sp[s]) % C == 0
+            for r in range(C):
+                i = perm[s * C + r]
+                if i < 0:
+                    continue
+                assert s * C // sigma == i // sigma          # permutation inside the window
+                seen[i] = True
+                a, b = trp[i], trp[i + 1]
+                assert b - a <= ln
+                for k in range(ln):
+                    e = sp[s] + k * C + r
+                    if k < b - a:
+                        assert c[e] == tcol[a + k]
+                        assert np.array_equal(wf[e * wpe:(e + 1) * wpe].astype(np.float64),
+                                              tw[(a + k) * wpe:(a + k + 1) * wpe])
+                    else:
+                        assert np.all(wf[e * wpe:(e + 1) * wpe] == 0.0) and 0 <= c[e] < ncols
+        assert seen.all()
+    # a weight that is not exact in fp32 keeps the fp64 layout (status 2)
+    w2 = np.ascontiguousarray(w.copy())
+    w2[0] = 0.1
+    assert _tsell(rp, col, w2, wpe, C, sigma)[0] == 2
+
+
 @pytest.mark.parametrize("name", ["c2_small", "c3_small"])
 def test_transpose_bitexact_vs_oracle(name):
     L = _lib()
