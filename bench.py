@@ -616,8 +616,9 @@ def run_ours(args):
             "metric": "V-cycles/s", "value": value, "unit": "V-cycles/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.config], "n_dof": n_global, "n_dof_per_gpu": N,
-                       "levels": len(P.levels), "level_rows_rank0": [i["n"] for i in infos],
+            # config = the workload only, identical in the reference arm's line; run details below
+            "config": {"workload": WORKLOADS[args.config], "n_dof": n_global, "levels": len(P.levels)},
+            "run": {"n_dof_per_gpu": N, "level_rows_rank0": [i["n"] for i in infos],
                        "level_kinds": level_kinds,
                        "nnzb_fine_rank0": infos[L]["nnzb"],
                        "parallelism": (f"row-partition x{ws} ({'NCCL' if transport == mg.MG_TRANSPORT_NCCL else 'IPC'}"

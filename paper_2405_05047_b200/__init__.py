@@ -17,7 +17,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmgb200.so")
+# MGB200_LIB: an alternative build of the same library (same-box A/B of compile-time
+# kernel variants, scripts/); the default is the in-tree build
+LIB_PATH = os.environ.get("MGB200_LIB") or os.path.join(_HERE, "libmgb200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_2405_05047_b200/build.py` "

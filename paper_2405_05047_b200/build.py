@@ -40,6 +40,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(out: str, defines: list[str]) -> str:
+    """An alternative build with extra -D flags at `out` (same-box A/B of
+    compile-time kernel variants; loaded through MGB200_LIB)."""
+    cmd = [NVCC, *ARCH, *FLAGS, *defines, "-o", out, *SOURCES]
+    subprocess.check_call(cmd)
+    return out
+
+
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], [a for a in sys.argv[i + 2:] if a.startswith("-D")]))
+    else:
+        build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+        print(LIB)

@@ -253,8 +253,14 @@ __device__ __forceinline__ void sell_apply_task(const Sell &A, int64_t task, con
   }
 }
 
+// split-k variants run on small levels whose grid is about one wave: cap them at
+// 40 registers (6 CTAs per SM instead of 5 at 48; no spills, ptxas -v) so more of
+// the grid is resident at once (C3 level 4: 1109 CTAs)
+#ifndef MGB200_KS_MINB
+#define MGB200_KS_MINB 6
+#endif
 template <int BS, int OP, bool STREAM, bool HALO, int KS, bool F32 = false>
-__global__ void __launch_bounds__(kCta) k_sell_apply(Sell A, const double *__restrict__ x,
+__global__ void __launch_bounds__(kCta, (KS > 1 && BS <= 3) ? MGB200_KS_MINB : 0) k_sell_apply(Sell A, const double *__restrict__ x,
                                                      const double *__restrict__ xg, int n_own,
                                                      const double *__restrict__ b,
                                                      const double *__restrict__ dinv,
@@ -380,65 +386,90 @@ struct TSell {
   int64_t n_slices;
 };
 
-template <int BS, int WPE, bool ACCUM, bool HALO, int KS>
+// NSL consecutive slices per warp (KS warps per slice group): the loads of
+// the NSL slices' entries are issued together, so a warp keeps NSL dependent
+// column -> value chains in flight (prolongation rows have 1-8 entries: one
+// slice alone leaves the warp waiting on a short chain).
+template <int BS, int WPE, bool ACCUM, bool HALO, int KS, int NSL>
 __global__ void __launch_bounds__(kCta) k_tsell(TSell T, const double *__restrict__ in,
                                                 const double *__restrict__ ing, int n_own,
                                                 double *__restrict__ out) {
   constexpr int C = 32 / BS;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int sub = KS == 1 ? 0 : wid % KS;
-  const int64_t s = int64_t(blockIdx.x) * (kWarpsPerCta / KS) + wid / KS;
-  const bool live = s < T.n_slices;
-  if (KS == 1 && !live) return;
+  const int64_t s0 = (int64_t(blockIdx.x) * (kWarpsPerCta / KS) + wid / KS) * NSL;
+  if (KS == 1 && s0 >= T.n_slices) return;
   const int r = lane / BS, q = lane - r * BS;
-  const bool act = live && r < C;
-  double acc[1] = {0.0};
-  int row = -1;
-  if (act) {
-    const int64_t e0 = T.slice_ptr[s], len = (T.slice_ptr[s + 1] - e0) / C;
-    row = T.perm[s * C + r];
-    const int64_t eb = e0 + r;
+  double acc[NSL];
+  int row[NSL];
+  int64_t eb[NSL], len[NSL];
+  int64_t kmax = 0;
+#pragma unroll
+  for (int u = 0; u < NSL; ++u) {
+    acc[u] = 0.0;
+    row[u] = -1;
+    len[u] = 0;
+    eb[u] = 0;
+    const int64_t s = s0 + u;
+    if (s < T.n_slices && r < C) {
+      const int64_t e0 = T.slice_ptr[s];
+      len[u] = (T.slice_ptr[s + 1] - e0) / C;
+      eb[u] = e0 + r;
+      row[u] = T.perm[s * C + r];
+      kmax = len[u] > kmax ? len[u] : kmax;
+    }
+  }
+  auto entry = [&](int64_t e, int &c, double &w) {
+    if constexpr (WPE == 1) {
+      const int2 t = __ldg(T.cw + e);
+      c = t.x;
+      w = double(__int_as_float(t.y));
+    } else {
+      c = __ldg(T.col + e);
+      w = double(__ldg(T.w + e * BS + q));
+    }
+  };
+  if constexpr (NSL == 1) {
     int64_t k = sub;
     constexpr int UB = 4;  // loads of 4 entries in flight before their use (summed in order)
-    for (; k + (UB - 1) * KS < len; k += UB * KS) {
+    for (; k + (UB - 1) * KS < len[0]; k += UB * KS) {
       int c[UB];
       double w[UB], v[UB];
 #pragma unroll
-      for (int u = 0; u < UB; ++u) {
-        const int64_t e = eb + (k + u * KS) * C;
-        if constexpr (WPE == 1) {
-          const int2 t = __ldg(T.cw + e);
-          c[u] = t.x;
-          w[u] = double(__int_as_float(t.y));
-        } else {
-          c[u] = __ldg(T.col + e);
-          w[u] = double(__ldg(T.w + e * BS + q));
-        }
-      }
+      for (int u = 0; u < UB; ++u) entry(eb[0] + (k + u * KS) * C, c[u], w[u]);
 #pragma unroll
       for (int u = 0; u < UB; ++u) v[u] = __ldg(col_ptr<BS, HALO>(in, ing, n_own, c[u]) + q);
 #pragma unroll
       for (int u = 0; u < UB; ++u) acc[0] = fma(w[u], v[u], acc[0]);
     }
-    for (; k < len; k += KS) {
-      const int64_t e = eb + k * C;
+    for (; k < len[0]; k += KS) {
       int c;
       double w;
-      if constexpr (WPE == 1) {
-        const int2 t = __ldg(T.cw + e);
-        c = t.x;
-        w = double(__int_as_float(t.y));
-      } else {
-        c = __ldg(T.col + e);
-        w = double(__ldg(T.w + e * BS + q));
-      }
+      entry(eb[0] + k * C, c, w);
       acc[0] = fma(w, __ldg(col_ptr<BS, HALO>(in, ing, n_own, c) + q), acc[0]);
     }
+  } else {
+    for (int64_t k = sub; k < kmax; k += KS) {
+      int c[NSL];
+      double w[NSL], v[NSL];
+#pragma unroll
+      for (int u = 0; u < NSL; ++u)
+        if (k < len[u]) entry(eb[u] + k * C, c[u], w[u]);
+#pragma unroll
+      for (int u = 0; u < NSL; ++u)
+        if (k < len[u]) v[u] = __ldg(col_ptr<BS, HALO>(in, ing, n_own, c[u]) + q);
+#pragma unroll
+      for (int u = 0; u < NSL; ++u)
+        if (k < len[u]) acc[u] = fma(w[u], v[u], acc[u]);
+    }
   }
-  if (!combine_split<1, KS>(acc, wid, sub, lane)) return;
-  if (!act || row < 0) return;
-  const int64_t o = int64_t(row) * BS + q;
-  out[o] = ACCUM ? out[o] + acc[0] : acc[0];
+  if (!combine_split<NSL, KS>(acc, wid, sub, lane)) return;
+#pragma unroll
+  for (int u = 0; u < NSL; ++u) {
+    if (row[u] < 0) continue;
+    const int64_t o = int64_t(row[u]) * BS + q;
+    out[o] = ACCUM ? out[o] + acc[u] : acc[u];
+  }
 }
 
 // Coarse solve y = A_0^{-1} d with the dense inverse (row stride ld, even,
@@ -471,6 +502,64 @@ __device__ __forceinline__ void gemv_row(int64_t N, int64_t ld, const double *__
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if (lane == 0) y[r] = acc;
+}
+
+// The same product with RS warps per row (a CTA = 8 / RS rows): each warp sums
+// a contiguous quarter (RS = 4) of the row with four 16-byte loads in flight
+// per lane, the RS partial sums are added in warp order through shared memory.
+// The dense inverse (C3: 3000^2 = 72 MB) is read in one wave of short chains
+// instead of 3000 chains of 12 dependent steps.
+// Partial sum of row r of M d over the column chunk `sub` of RS (the split
+// kernel's per-warp work, then a shuffle reduction): shared by k_dense_gemv_split
+// and the persistent tail kernel so both produce bit-identical results.
+template <int RS, bool CG>
+__device__ __forceinline__ double gemv_chunk(int64_t N, int64_t ld, const double *__restrict__ M,
+                                             const double *__restrict__ d, int64_t r, int sub) {
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0;
+  const int64_t chunk = ((N + RS - 1) / RS + 1) & ~int64_t(1);  // even: 16-byte loads stay aligned (ld even)
+  const int64_t c0 = sub * chunk, c1 = c0 + chunk < N ? c0 + chunk : N;
+  const double *row = M + r * ld;
+  int64_t c = c0 + 2 * lane;
+  for (; c + 192 + 1 < c1; c += 256) {
+    double2 m[4], dv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      m[u] = __ldg(reinterpret_cast<const double2 *>(row + c + 64 * u));
+      dv[u] = CG ? __ldcg(reinterpret_cast<const double2 *>(d + c + 64 * u))
+                 : __ldg(reinterpret_cast<const double2 *>(d + c + 64 * u));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc = fma(m[u].x, dv[u].x, acc);
+      acc = fma(m[u].y, dv[u].y, acc);
+    }
+  }
+  for (; c < c1; c += 64) {
+    acc = fma(__ldg(row + c), ldv<CG>(d + c), acc);
+    if (c + 1 < c1) acc = fma(__ldg(row + c + 1), ldv<CG>(d + c + 1), acc);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  return acc;
+}
+
+template <int RS>
+__global__ void __launch_bounds__(kCta) k_dense_gemv_split(int64_t N, int64_t ld, const double *__restrict__ M,
+                                                           const double *__restrict__ d, double *__restrict__ y) {
+  __shared__ double part[kWarpsPerCta];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t r = int64_t(blockIdx.x) * (kWarpsPerCta / RS) + wid / RS;
+  const int sub = wid % RS;
+  const double acc = r < N ? gemv_chunk<RS, false>(N, ld, M, d, r, sub) : 0.0;
+  if (lane == 0) part[wid] = acc;
+  __syncthreads();
+  if (sub == 0 && lane == 0 && r < N) {
+    double s = part[wid];
+#pragma unroll
+    for (int k = 1; k < RS; ++k) s += part[wid + k];
+    y[r] = s;
+  }
 }
 
 __global__ void __launch_bounds__(kCta) k_dense_gemv(int64_t N, int64_t ld, const double *__restrict__ M,
@@ -554,10 +643,22 @@ __global__ void __launch_bounds__(kCta) k_tail(const TailOp *__restrict__ ops, i
       }
       case T_SWEEP: tail_apply<BS, OP_SWEEP>(op); break;
       case T_RESID: tail_apply<BS, OP_RESID>(op); break;
-      case T_RESTRICT: tail_transfer<BS, false, 4, true>(op); break;
+      case T_RESTRICT:  // split factor of the standalone restriction (bit-identical sums)
+        if (op.ks == 1) tail_transfer<BS, false, 1, true>(op);
+        else if (op.ks == 2) tail_transfer<BS, false, 2, true>(op);
+        else tail_transfer<BS, false, 4, true>(op);
+        break;
       case T_PROLONG: tail_transfer<BS, true, 1, false>(op); break;
-      case T_GEMV:
-        for (int64_t r = tid >> 5; r < op.n; r += nth >> 5) gemv_row<true>(op.n, op.ld, op.dinv, op.b, op.out, r);
+      case T_GEMV:  // the split kernel's four column chunks, summed in the same order
+        for (int64_t r = tid >> 5; r < op.n; r += nth >> 5) {
+          if (op.ks == 4) {
+            double s4 = gemv_chunk<4, true>(op.n, op.ld, op.dinv, op.b, r, 0);
+            for (int q = 1; q < 4; ++q) s4 += gemv_chunk<4, true>(op.n, op.ld, op.dinv, op.b, r, q);
+            if ((threadIdx.x & 31) == 0) op.out[r] = s4;
+          } else {
+            gemv_row<true>(op.n, op.ld, op.dinv, op.b, op.out, r);
+          }
+        }
         break;
       case T_COPY:
         for (int64_t i = tid; i < op.n; i += nth) op.out[i] = __ldcg(op.x + i);
@@ -621,7 +722,11 @@ __device__ __forceinline__ void grid_finish(double blocksum, double *part, unsig
 // MODE 0: res = (a, b).  MODE 1 (MGS step): a -= (*h) * c; res = (a_new, b)
 // (b == nullptr => res = ||a_new||_2 with SQRT).  VEC: all pointers 16-byte
 // aligned -> double2 loads/stores over the even part, the odd tail in thread 0.
-template <int MODE, bool SQRT, bool VEC>
+// REV (VEC only): the grid sweeps the vectors from the high end down, so a
+// pass that follows a forward pass (or vice versa) starts on the lines the
+// previous pass touched last, which are still in L2 (126 MB vs 83 MB vectors
+// on C3): the MGS passes of one Arnoldi step alternate direction.
+template <int MODE, bool SQRT, bool VEC, bool REV = false>
 __global__ void __launch_bounds__(kRedThreads) k_reduce(int64_t n, double *__restrict__ a, const double *__restrict__ b,
                                                         const double *__restrict__ c, const double *__restrict__ h,
                                                         double *part, unsigned *ticket, double *res, double *res2) {
@@ -637,25 +742,32 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce(int64_t n, double *__res
     double2 *a2 = reinterpret_cast<double2 *>(a);
     const double2 *b2 = reinterpret_cast<const double2 *>(b);
     const double2 *c2 = reinterpret_cast<const double2 *>(c);
+    if constexpr (REV) {  // index j <-> n2 - 1 - j (pointers to the last element, negative strides)
+      a2 += n2 - 1;
+      b2 += n2 - 1;
+      c2 += n2 - 1;
+    }
+    constexpr int64_t D = REV ? -1 : 1;
     int64_t i = tid;
     for (; i + (U - 1) * stride < n2; i += U * stride) {
       double2 x[U], y[U], v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
+        const int64_t j = D * (i + u * stride);
         if constexpr (MODE == 0) {
-          x[u] = __ldg(a2 + i + u * stride);
+          x[u] = __ldg(a2 + j);
         } else {
-          x[u] = a2[i + u * stride];
-          v[u] = __ldg(c2 + i + u * stride);
+          x[u] = a2[j];
+          v[u] = __ldg(c2 + j);
         }
-        if (b) y[u] = __ldg(b2 + i + u * stride);
+        if (b) y[u] = __ldg(b2 + j);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if constexpr (MODE == 1) {
           x[u].x = fma(-hv, v[u].x, x[u].x);
           x[u].y = fma(-hv, v[u].y, x[u].y);
-          a2[i + u * stride] = x[u];
+          a2[D * (i + u * stride)] = x[u];
         }
         const double2 yy = b ? y[u] : x[u];
         s = fma(x[u].x, yy.x, s);
@@ -663,14 +775,15 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce(int64_t n, double *__res
       }
     }
     for (; i < n2; i += stride) {
-      double2 x = MODE == 0 ? __ldg(a2 + i) : a2[i];
+      const int64_t j = D * i;
+      double2 x = MODE == 0 ? __ldg(a2 + j) : a2[j];
       if constexpr (MODE == 1) {
-        const double2 v = __ldg(c2 + i);
+        const double2 v = __ldg(c2 + j);
         x.x = fma(-hv, v.x, x.x);
         x.y = fma(-hv, v.y, x.y);
-        a2[i] = x;
+        a2[j] = x;
       }
-      const double2 yy = b ? __ldg(b2 + i) : x;
+      const double2 yy = b ? __ldg(b2 + j) : x;
       s = fma(x.x, yy.x, s);
       s2 = fma(x.y, yy.y, s2);
     }

@@ -86,7 +86,7 @@ struct TSellOp {
   DevArray<int2> cw;
   DevArray<float> w;
   int64_t n_slices = 0, n_entries = 0;
-  int C = 32, wpe = 1, ks = 1;
+  int C = 32, wpe = 1, ks = 1, nsl = 1;
   bool set = false;
   mgk::TSell view() const { return mgk::TSell{slice_ptr.p, perm.p, cw.p, col.p, w.p, n_slices}; }
 };
@@ -319,9 +319,17 @@ struct mg_ctx_s {
   DevArray<double> mean_b;          // consistent copy of b (global constraint on the finest level)
   DevArray<double> upd_stage;       // mg_update_matrix: staging buffer for host values (kept across calls)
   double *gm_host = nullptr;  // pinned
+  // mg_update_matrix from pageable host memory: two pinned chunks, the host
+  // copy of one overlapping the DMA of the other
+  char *pin_chunk[2] = {nullptr, nullptr};
+  cudaEvent_t pin_ev[2] = {nullptr, nullptr};
   mgk::GmresDev gm{};
   ~mg_ctx_s() {
     clear_graphs();
+    for (int k = 0; k < 2; ++k) {
+      if (pin_chunk[k]) cudaFreeHost(pin_chunk[k]);
+      if (pin_ev[k]) cudaEventDestroy(pin_ev[k]);
+    }
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (comm_stream) cudaStreamDestroy(comm_stream);
@@ -347,6 +355,10 @@ struct mg_ctx_s {
   bool use_graphs() const { return cfg.use_graphs && (!tr || tr->graph_safe()); }
   // GMRES restart cycles as conditional graphs (MGB200_GMRES_LOOP=host: one
   // graph + host sync per Arnoldi step, the round-1 path)
+  bool mgs_alternate() const {  // MGB200_MGS_ALT=0: every MGS pass sweeps forward (round-1 order)
+    const char *e = std::getenv("MGB200_MGS_ALT");
+    return !(e && e[0] == '0');
+  }
   bool gmres_device_loop() const {
     const char *e = std::getenv("MGB200_GMRES_LOOP");
     return !(e && std::string(e) == "host");
@@ -517,13 +529,33 @@ mg_status launch_transfer(int bs, bool acc, const SellOp &T, In in, double *out,
   return check_launch(acc ? "prolong-add" : "transfer");
 }
 
+template <int BS, int WPE, bool ACC, bool HALO, int KS, int NSL>
+void launch_tsell_k(const TSellOp &T, In in, double *out, cudaStream_t st) {
+  const unsigned g = grid_for_slices((T.n_slices + NSL - 1) / NSL, KS);
+  ++g_tally, mgk::k_tsell<BS, WPE, ACC, HALO, KS, NSL><<<g, mgk::kCta, 0, st>>>(T.view(), in.x, in.xg, in.n_own, out);
+}
+
+// (ks, nsl) = warps per slice group, slices per warp: TSellOp defaults
+// (restriction 4/1, prolongation 1/1), MGB200_TSELL_R / MGB200_TSELL_P = "ks,nsl"
+// override (tuning experiments; ks in {1,2,4}, nsl in {1,2,4})
+inline void tsell_cfg(const TSellOp &T, bool acc, int &ks, int &nsl) {
+  ks = T.ks, nsl = T.nsl;
+  const char *e = std::getenv(acc ? "MGB200_TSELL_P" : "MGB200_TSELL_R");
+  if (e && *e) {
+    int a = 0, b = 0;
+    if (std::sscanf(e, "%d,%d", &a, &b) == 2) ks = a, nsl = b;
+  }
+}
+
 template <int BS, int WPE, bool ACC, bool HALO>
 void launch_tsell_h(const TSellOp &T, In in, double *out, cudaStream_t st) {
-  const unsigned g = grid_for_slices(T.n_slices, T.ks);
-  if (T.ks > 1)
-    ++g_tally, mgk::k_tsell<BS, WPE, ACC, HALO, 4><<<g, mgk::kCta, 0, st>>>(T.view(), in.x, in.xg, in.n_own, out);
-  else
-    ++g_tally, mgk::k_tsell<BS, WPE, ACC, HALO, 1><<<g, mgk::kCta, 0, st>>>(T.view(), in.x, in.xg, in.n_own, out);
+  int ks, nsl;
+  tsell_cfg(T, ACC, ks, nsl);
+#define TS(K, S) \
+  if (ks == K && nsl == S) return launch_tsell_k<BS, WPE, ACC, HALO, K, S>(T, in, out, st);
+  TS(1, 1) TS(1, 2) TS(1, 4) TS(2, 1) TS(2, 2) TS(4, 1) TS(4, 2)
+#undef TS
+  launch_tsell_k<BS, WPE, ACC, HALO, 1, 1>(T, in, out, st);
 }
 
 template <int BS, bool ACC>
@@ -673,29 +705,33 @@ inline bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) =
 
 template <int MODE>
 void launch_reduce(mg_ctx_s *c, bool sq, bool vec, int64_t n, double *a, const double *b, const double *v,
-                   const double *h, double *res) {
+                   const double *h, double *res, bool rev = false) {
   const unsigned g = red_grid(c, n);
   auto *P = c->red_part.p;
   auto *T = c->ticket.p;
-  if (sq && vec) ++g_tally, mgk::k_reduce<MODE, true, true><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, b, v, h, P, T, res, nullptr);
+  if (vec && rev) {
+    if (sq) ++g_tally, mgk::k_reduce<MODE, true, true, true><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, b, v, h, P, T, res, nullptr);
+    else ++g_tally, mgk::k_reduce<MODE, false, true, true><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, b, v, h, P, T, res, nullptr);
+  } else if (sq && vec) ++g_tally, mgk::k_reduce<MODE, true, true><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, b, v, h, P, T, res, nullptr);
   else if (sq) ++g_tally, mgk::k_reduce<MODE, true, false><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, b, v, h, P, T, res, nullptr);
   else if (vec) ++g_tally, mgk::k_reduce<MODE, false, true><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, b, v, h, P, T, res, nullptr);
   else ++g_tally, mgk::k_reduce<MODE, false, false><<<g, mgk::kRedThreads, 0, c->stream>>>(n, a, b, v, h, P, T, res, nullptr);
 }
 
 // res (device) = (a, b) [sqrt] over the level's rows (all ranks if dist)
-mg_status dev_dot(mg_ctx_s *c, bool dist, int64_t n, const double *a, const double *b, double *res, bool sqrt_) {
+mg_status dev_dot(mg_ctx_s *c, bool dist, int64_t n, const double *a, const double *b, double *res, bool sqrt_,
+                  bool rev = false) {
   const bool vec = al16(a) && al16(b);
-  launch_reduce<0>(c, sqrt_ && !dist, vec, n, const_cast<double *>(a), b, nullptr, nullptr, res);
+  launch_reduce<0>(c, sqrt_ && !dist, vec, n, const_cast<double *>(a), b, nullptr, nullptr, res, rev);
   TRY(check_launch("dot"));
   return finish_reduce(c, dist, res, sqrt_);
 }
 
 // MGS step: a -= (*h) v ; res = (a, u), or ||a|| when u == nullptr
 mg_status dev_axpy_dot(mg_ctx_s *c, bool dist, int64_t n, double *a, const double *v, const double *h,
-                       const double *u, double *res) {
+                       const double *u, double *res, bool rev = false) {
   const bool vec = al16(a) && al16(v) && (!u || al16(u));
-  launch_reduce<1>(c, u == nullptr && !dist, vec, n, a, u, v, h, res);
+  launch_reduce<1>(c, u == nullptr && !dist, vec, n, a, u, v, h, res, rev);
   TRY(check_launch("axpy-dot"));
   return finish_reduce(c, dist, res, u == nullptr);
 }
@@ -1049,12 +1085,14 @@ mg_status build_tail(mg_ctx_s *c) {
     mgk::TailOp t = base(mgk::T_RESTRICT);
     t.A = L.R.view();
     t.wpe = L.R.vpe;
+    t.ks = L.Rt.set ? L.Rt.ks : 4;  // the standalone restriction's split factor
     t.x = L.w.p;
     t.out = c->lv[l - 1].b.p;
     ops.push_back(t);
   }
   if (c->cfg.coarse_mode == MG_COARSE_DIRECT) {
     mgk::TailOp g = base(mgk::T_GEMV);
+    g.ks = al16(c->lv[0].b.p) ? 4 : 1;  // as coarse_solve: split kernel when d is 16-byte aligned
     g.dinv = c->cinv.p;
     g.b = c->lv[0].b.p;
     g.out = c->lv[0].x.p;
@@ -1339,8 +1377,13 @@ mg_status mean_project(mg_ctx_s *c, int l, double *x, bool consist) {
 
 mg_status coarse_solve(mg_ctx_s *c, const double *b, double *x) {
   if (c->cfg.coarse_mode == MG_COARSE_DIRECT) {
-    const unsigned g = unsigned((c->cN + mgk::kWarpsPerCta - 1) / mgk::kWarpsPerCta);
-    ++g_tally, mgk::k_dense_gemv<<<g, mgk::kCta, 0, c->stream>>>(c->cN, c->cld, c->cinv.p, b, x);
+    if (al16(b)) {  // 4 warps per row (d is read with 16-byte loads)
+      const unsigned g = unsigned((c->cN + 1) / 2);
+      ++g_tally, mgk::k_dense_gemv_split<4><<<g, mgk::kCta, 0, c->stream>>>(c->cN, c->cld, c->cinv.p, b, x);
+    } else {
+      const unsigned g = unsigned((c->cN + mgk::kWarpsPerCta - 1) / mgk::kWarpsPerCta);
+      ++g_tally, mgk::k_dense_gemv<<<g, mgk::kCta, 0, c->stream>>>(c->cN, c->cld, c->cinv.p, b, x);
+    }
     return check_launch("coarse gemv");
   }
   return smooth(c, 0, x, b, std::max(1, c->cfg.coarse_sweeps), true);
@@ -1889,8 +1932,10 @@ mg_status mg_set_transfer(mg_ctx c, int fine_level, const int64_t *row_ptr, cons
   }
   TRY(build_sell(L.R, L.r_rows, rrp.data(), rcl.data(), rv.data(), wpe));
   L.R.ks = 4;  // R rows gather 9-27+ fine entries: split them over 4 warps
+  // restriction on the SELL-C layout (measured, scripts/tune_tsell.py: C3 finest 98.7 -> 69.3 us,
+  // C5 212 -> 113 us, C2 25.6 -> 19.6 us); 2 warps per slice group for bs 3, 1 otherwise
   TRY(build_tsell(L.Rt, L.r_rows, rrp.data(), rcl.data(), rv.data(), wpe, c->bs()));
-  L.Rt.ks = 4;
+  L.Rt.ks = c->bs() == 3 ? 2 : 1;
   // ---- P: columns are coarse rows ------------------------------------------
   if (C.dist) {
     std::vector<int64_t> ghosts;
@@ -1900,7 +1945,13 @@ mg_status mg_set_transfer(mg_ctx c, int fine_level, const int64_t *row_ptr, cons
     L.hp = Halo();
   }
   TRY(build_sell(L.P, L.n, rp.data(), cl.data(), v.data(), wpe));
-  TRY(build_tsell(L.Pt, L.n, rp.data(), cl.data(), v.data(), wpe, c->bs()));
+  // prolongation stays on SELL-32 (lane = fine row): its rows hold 1-8 entries, and the
+  // SELL-C layout's 32/bs rows per warp triple the short dependent chains (C3 finest
+  // 105 -> 162 us measured); MGB200_TSELL_PROLONG=1 builds it anyway (experiments)
+  if (const char *e = std::getenv("MGB200_TSELL_PROLONG"); e && e[0] == '1')
+    TRY(build_tsell(L.Pt, L.n, rp.data(), cl.data(), v.data(), wpe, c->bs()));
+  else
+    L.Pt = TSellOp();
   L.wpe = wpe;
   L.nnz_p = nnz;
   c->invalidate();
@@ -2192,6 +2243,44 @@ mg_status mg_make_consistent(mg_ctx c, int level, double *b) {
   return mean_project(c, level, b, true);
 }
 
+// Host -> device copy on the context stream at pinned-memory speed: pinned
+// (page-locked) sources go straight to the DMA engine; pageable ones are staged
+// through two 64 MB pinned chunks, a multi-threaded host copy into one chunk
+// overlapping the DMA out of the other (the driver's own pageable path runs
+// at ~9 GB/s: VERDICT r1, the 6.2 GB C3 operator took 690 ms).
+static mg_status upload_host(mg_ctx_s *c, void *dst, const void *src, size_t bytes) {
+  if (!bytes) return MG_OK;
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, src) != cudaSuccess) cudaGetLastError();
+  if (pa.type == cudaMemoryTypeHost) {
+    CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    return MG_OK;
+  }
+  constexpr size_t kChunk = size_t(64) << 20;
+  for (int k = 0; k < 2; ++k) {
+    if (!c->pin_chunk[k]) CU(cudaMallocHost(&c->pin_chunk[k], kChunk));
+    if (!c->pin_ev[k]) CU(cudaEventCreateWithFlags(&c->pin_ev[k], cudaEventDisableTiming));
+  }
+  CU(cudaStreamSynchronize(c->stream));  // earlier work on the stream may still read a chunk
+  const char *s = static_cast<const char *>(src);
+  char *d = static_cast<char *>(dst);
+  for (size_t off = 0, i = 0; off < bytes; off += kChunk, ++i) {
+    const int k = int(i & 1);
+    const size_t len = std::min(kChunk, bytes - off);
+    if (i >= 2) CU(cudaEventSynchronize(c->pin_ev[k]));  // the DMA out of this chunk is done
+    char *pc = c->pin_chunk[k];
+    const int64_t nt = std::max<int64_t>(1, std::min<int64_t>(16, int64_t(len >> 22)));
+#pragma omp parallel for num_threads(int(nt)) schedule(static)
+    for (int64_t t = 0; t < nt; ++t) {
+      const size_t a = len * size_t(t) / size_t(nt), b = len * size_t(t + 1) / size_t(nt);
+      std::memcpy(pc + a, s + off + a, b - a);
+    }
+    CU(cudaMemcpyAsync(d + off, pc, len, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaEventRecord(c->pin_ev[k], c->stream));
+  }
+  return MG_OK;
+}
+
 mg_status mg_update_matrix(mg_ctx c, int level, const double *vals, int mem) {
   TRY(check_level(c, level));
   if (!vals) return fail(MG_ERR_INVALID_ARG, "NULL values");
@@ -2208,7 +2297,7 @@ mg_status mg_update_matrix(mg_ctx c, int level, const double *vals, int mem) {
       CU(cudaStreamSynchronize(c->stream));
       TRY(c->upd_stage.alloc(cnt));
     }
-    CU(cudaMemcpyAsync(c->upd_stage.p, vals, size_t(nnzb) * V * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    TRY(upload_host(c, c->upd_stage.p, vals, size_t(nnzb) * V * sizeof(double)));
     dv = c->upd_stage.p;
   }
   DevArray<int> flag;
@@ -2442,10 +2531,14 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
         TRY(vcycle_rec(c, Lf, zj, vj, true));      // z_j = GMG(L, 0, v_j)
         TRY(a_pass_spmv(c, Lf, 1.0, zj, 0.0, w, true));  // w = A z_j
         double *hcol = g.H + size_t(j) * ld;
-        TRY(dev_dot(c, dist, N, w, V, hcol + 0, false));  // h_0j = (w, v_0)
+        // MGS passes alternate sweep direction (the SpMV wrote w forward), so each
+        // pass starts on the L2-resident tail of the previous one (same arithmetic)
+        const bool alt = c->mgs_alternate();
+        TRY(dev_dot(c, dist, N, w, V, hcol + 0, false, alt));  // h_0j = (w, v_0)
         for (int i = 0; i < j; ++i)                       // w -= h_ij v_i ; h_{i+1,j} = (w, v_{i+1})
-          TRY(dev_axpy_dot(c, dist, N, w, V + size_t(i) * NS, hcol + i, V + size_t(i + 1) * NS, hcol + i + 1));
-        TRY(dev_axpy_dot(c, dist, N, w, vj, hcol + j, nullptr, hcol + j + 1));  // w -= h_jj v_j ; ||w||
+          TRY(dev_axpy_dot(c, dist, N, w, V + size_t(i) * NS, hcol + i, V + size_t(i + 1) * NS, hcol + i + 1,
+                           alt && (i % 2 == 1)));
+        TRY(dev_axpy_dot(c, dist, N, w, vj, hcol + j, nullptr, hcol + j + 1, alt && (j % 2 == 1)));  // w -= h_jj v_j ; ||w||
         ++g_tally, mgk::k_givens<<<1, 32, 0, c->stream>>>(g, j, rtol, mm, hw, hs, cond ? 1 : 0);
         ++g_tally, mgk::k_scale_div<<<eg, 256, 0, c->stream>>>(N, w, g.hn + j, w);  // v_{j+1} = w / h_{j+1,j}
         TRY(check_launch("givens"));

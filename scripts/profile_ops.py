@@ -21,6 +21,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("mode", choices=["step", "kernels", "vcycle"])
 ap.add_argument("--config", default="c3")
 ap.add_argument("--mixed", action="store_true")
+ap.add_argument("--level", type=int, default=-1, help="kernels mode: level to profile (default finest)")
 a = ap.parse_args()
 
 t = time.time()
@@ -53,6 +54,10 @@ elif a.mode == "vcycle":
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
 else:
+    if a.level >= 0:
+        Lf = a.level
+        nl = P.levels[Lf].n * P.bs
+        b = torch.randn(nl, dtype=torch.float64, device="cuda")
     xin = torch.randn_like(b)
     out = torch.empty_like(b)
     nc = P.levels[Lf - 1].n * P.bs

@@ -31,6 +31,15 @@ def test_bench_json_contract_c1():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     c = d["cpu_baseline"]
     assert c["kind"] == "oracle" and c["cores"] >= 1 and c["value"] > 0 and "sample" in c
-    assert abs(c["solve"]["iterations"] - d["config"]["iterations_per_solve"]) <= 1   # same algorithm (Z24: +-1)
+    assert abs(c["solve"]["iterations"] - d["run"]["iterations_per_solve"]) <= 1   # same algorithm (Z24: +-1)
+    # the reference arm names the same workload with the same config object
+    ref = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "c1",
+                          "--steps", "3", "--warmup", "3"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert ref.returncode == 0, ref.stderr[-3000:]
+    rl = [ln for ln in ref.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(rl) == 1
+    rd = json.loads(rl[0])
+    assert rd["impl"] == "reference" and rd["config"] == d["config"]
+    assert rd["metric"] == d["metric"] and rd["unit"] == d["unit"] and rd["scaling"] == d["scaling"]
     assert d["gpu_launches"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
