@@ -412,6 +412,9 @@ def run_ours(args):
     l0 = mg.launch_count(ctx)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    ncu_range = os.environ.get("MGB200_PROFILE_TIMED") == "1"   # ncu --profile-from-start off: timed steps only
+    if ncu_range:
+        torch.cuda.profiler.start()
     e0.record(stream)
     total_its = 0
     for _ in range(args.steps):
@@ -419,6 +422,8 @@ def run_ours(args):
         total_its += its
     e1.record(stream)
     torch.cuda.synchronize()
+    if ncu_range:
+        torch.cuda.profiler.stop()
     barrier()
     t_ms = e0.elapsed_time(e1)
     launches = mg.launch_count(ctx) - l0

@@ -118,6 +118,17 @@ __device__ __forceinline__ void load_entry_raw(const float *__restrict__ gval, i
 // ---------------------------------------------------------------------------
 enum { OP_SPMV = 0, OP_RESID = 1, OP_SWEEP = 2 };
 
+// Programmatic dependent launch (PDL).  The standalone V-cycle kernels let the
+// next kernel launch as soon as all their CTAs are running (trigger at entry),
+// and each one loads what does not depend on its predecessor -- slice
+// pointers, row permutation, first column indices, D^-1 -- BEFORE waiting for
+// the predecessor's results (x, b, r).  On the small levels, whose kernels are
+// a few dependent load round trips each, the launch and the structure loads
+// overlap the predecessor's tail.  Both instructions are no-ops for a kernel
+// launched without the PDL attribute (mg.cu `kl`) and in the tail kernel.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // HALO: columns >= n_own are ghosts (multi-GPU), read from xg[c - n_own].
 template <int BS, bool HALO>
 __device__ __forceinline__ const double *col_ptr(const double *x, const double *xg, int n_own, int c) {
@@ -151,7 +162,7 @@ __device__ __forceinline__ bool combine_split(double (&acc)[BS], int wid, int su
 
 // One CTA-task of an A-pass: slice s = task * (8 / KS) + warp / KS.  All warps
 // of the CTA must call it (the split-k combine synchronises the CTA).
-template <int BS, int OP, bool STREAM, bool HALO, int KS, bool F32, bool CG>
+template <int BS, int OP, bool STREAM, bool HALO, int KS, bool F32, bool CG, bool WAIT = false>
 __device__ __forceinline__ void sell_apply_task(const Sell &A, int64_t task, const double *__restrict__ x,
                                                 const double *__restrict__ xg, int n_own,
                                                 const double *__restrict__ b, const double *__restrict__ dinv,
@@ -171,6 +182,7 @@ __device__ __forceinline__ void sell_apply_task(const Sell &A, int64_t task, con
     row = A.perm[s * 32 + lane];
     int64_t g = e0 + 32 * sub;
     int cn = g < e1 ? ld_col<STREAM>(A.col + g + lane) : 0;  // column of the next entry (prefetched)
+    if constexpr (WAIT) pdl_wait();  // x, b are the predecessor's results
     // Few bytes per entry (fp32 values, or bs <= 2): issue the loads of UB
     // entries before the first use so enough bytes are in flight per warp.
     // Entries are still accumulated in order (bit-identical to UB = 1).
@@ -228,6 +240,7 @@ __device__ __forceinline__ void sell_apply_task(const Sell &A, int64_t task, con
         for (int q = 0; q < BS; ++q) acc[r] = fma(v[r * BS + q], xv[q], acc[r]);
     }
   }
+  if constexpr (WAIT) pdl_wait();  // warps without entries (they skipped the loop)
   if (!combine_split<BS, KS>(acc, wid, sub, lane)) return;
   if (!live || row < 0) return;
   const int64_t o = int64_t(row) * BS;
@@ -253,11 +266,12 @@ __device__ __forceinline__ void sell_apply_task(const Sell &A, int64_t task, con
   }
 }
 
-// split-k variants run on small levels whose grid is about one wave: cap them at
-// 40 registers (6 CTAs per SM instead of 5 at 48; no spills, ptxas -v) so more of
-// the grid is resident at once (C3 level 4: 1109 CTAs)
+// MGB200_KS_MINB (compile-time experiment): minimum CTAs per SM for the split-k
+// variants.  6 caps them at 40 registers (no spills) so more of a one-wave grid is
+// resident; measured on the same box it LOSES (C3 148.8 -> 146.5 V-cycles/s, C2
+// 2194 -> 1964: the lost registers were the batched loads in flight), so 0 = none.
 #ifndef MGB200_KS_MINB
-#define MGB200_KS_MINB 6
+#define MGB200_KS_MINB 0
 #endif
 template <int BS, int OP, bool STREAM, bool HALO, int KS, bool F32 = false>
 __global__ void __launch_bounds__(kCta, (KS > 1 && BS <= 3) ? MGB200_KS_MINB : 0) k_sell_apply(Sell A, const double *__restrict__ x,
@@ -265,11 +279,13 @@ __global__ void __launch_bounds__(kCta, (KS > 1 && BS <= 3) ? MGB200_KS_MINB : 0
                                                      const double *__restrict__ b,
                                                      const double *__restrict__ dinv,
                                                      double *__restrict__ out, double alpha, double beta) {
-  sell_apply_task<BS, OP, STREAM, HALO, KS, F32, false>(A, blockIdx.x, x, xg, n_own, b, dinv, out, alpha, beta);
+  pdl_trigger();
+  sell_apply_task<BS, OP, STREAM, HALO, KS, F32, false, true>(A, blockIdx.x, x, xg, n_own, b, dinv, out, alpha,
+                                                               beta);
 }
 
 // First smoothing step from the zero guess: x = omega D^-1 b, A-free.
-template <int BS, bool CG>
+template <int BS, bool CG, bool WAIT = false>
 __device__ __forceinline__ void sweep0_task(int64_t n_slices, int64_t task, const int32_t *__restrict__ perm,
                                             const double *__restrict__ dinv, const double *__restrict__ b,
                                             double *__restrict__ x, double omega) {
@@ -280,6 +296,7 @@ __device__ __forceinline__ void sweep0_task(int64_t n_slices, int64_t task, cons
   const int row = perm[s * 32 + lane];
   double d[V];
   load_entry<V, true>(dinv + s * 32 * V, lane, d);
+  if constexpr (WAIT) pdl_wait();
   if (row < 0) return;
   const int64_t o = int64_t(row) * BS;
   double t[BS];
@@ -298,13 +315,14 @@ template <int BS>
 __global__ void __launch_bounds__(kCta) k_sweep0(int64_t n_slices, const int32_t *__restrict__ perm,
                                                  const double *__restrict__ dinv, const double *__restrict__ b,
                                                  double *__restrict__ x, double omega) {
-  sweep0_task<BS, false>(n_slices, blockIdx.x, perm, dinv, b, x, omega);
+  pdl_trigger();
+  sweep0_task<BS, false, true>(n_slices, blockIdx.x, perm, dinv, b, x, omega);
 }
 
 // Transfer y = T x (ACCUM = 0) or y += T x (ACCUM = 1) with scalar weights
 // (WPE = 1) or per-component weights (WPE = BS): restriction R r (P:131,
 // P:337), prolongation x + P y, hanging interpolation H x.
-template <int BS, int WPE, bool ACCUM, bool STREAM, bool HALO, int KS, bool CG>
+template <int BS, int WPE, bool ACCUM, bool STREAM, bool HALO, int KS, bool CG, bool WAIT = false>
 __device__ __forceinline__ void transfer_task(const Sell &T, int64_t task, const double *__restrict__ in,
                                               const double *__restrict__ ing, int n_own, double *__restrict__ out) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -321,6 +339,7 @@ __device__ __forceinline__ void transfer_task(const Sell &T, int64_t task, const
     row = T.perm[s * 32 + lane];
     int64_t g = e0 + 32 * sub;
     int cn = g < e1 ? ld_col<STREAM>(T.col + g + lane) : 0;
+    if constexpr (WAIT) pdl_wait();
     constexpr int UB = 4;  // scalar weights: batch the loads of 4 entries (summed in order)
     constexpr int step = 32 * KS;
     for (; g + (UB - 1) * step < e1; g += UB * step) {
@@ -354,6 +373,7 @@ __device__ __forceinline__ void transfer_task(const Sell &T, int64_t task, const
       for (int q = 0; q < BS; ++q) acc[q] = fma(w[WPE == 1 ? 0 : q], ldv<CG>(xc + q), acc[q]);
     }
   }
+  if constexpr (WAIT) pdl_wait();
   if (!combine_split<BS, KS>(acc, wid, sub, lane)) return;
   if (!live || row < 0) return;
   const int64_t o = int64_t(row) * BS;
@@ -365,7 +385,8 @@ template <int BS, int WPE, bool ACCUM, bool STREAM, bool HALO, int KS>
 __global__ void __launch_bounds__(kCta) k_transfer(Sell T, const double *__restrict__ in,
                                                    const double *__restrict__ ing, int n_own,
                                                    double *__restrict__ out) {
-  transfer_task<BS, WPE, ACCUM, STREAM, HALO, KS, false>(T, blockIdx.x, in, ing, n_own, out);
+  pdl_trigger();
+  transfer_task<BS, WPE, ACCUM, STREAM, HALO, KS, false, true>(T, blockIdx.x, in, ing, n_own, out);
 }
 
 // Transfer on the SELL-C layout of mgi_tsell_fill (C = 32 / BS rows per
@@ -395,6 +416,7 @@ __global__ void __launch_bounds__(kCta) k_tsell(TSell T, const double *__restric
                                                 const double *__restrict__ ing, int n_own,
                                                 double *__restrict__ out) {
   constexpr int C = 32 / BS;
+  pdl_trigger();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int sub = KS == 1 ? 0 : wid % KS;
   const int64_t s0 = (int64_t(blockIdx.x) * (kWarpsPerCta / KS) + wid / KS) * NSL;
@@ -419,6 +441,7 @@ __global__ void __launch_bounds__(kCta) k_tsell(TSell T, const double *__restric
       kmax = len[u] > kmax ? len[u] : kmax;
     }
   }
+  pdl_wait();  // `in` is the predecessor's result
   auto entry = [&](int64_t e, int &c, double &w) {
     if constexpr (WPE == 1) {
       const int2 t = __ldg(T.cw + e);
@@ -551,6 +574,8 @@ __global__ void __launch_bounds__(kCta) k_dense_gemv_split(int64_t N, int64_t ld
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t r = int64_t(blockIdx.x) * (kWarpsPerCta / RS) + wid / RS;
   const int sub = wid % RS;
+  pdl_trigger();
+  pdl_wait();
   const double acc = r < N ? gemv_chunk<RS, false>(N, ld, M, d, r, sub) : 0.0;
   if (lane == 0) part[wid] = acc;
   __syncthreads();

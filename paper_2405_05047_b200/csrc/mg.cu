@@ -355,6 +355,10 @@ struct mg_ctx_s {
   bool use_graphs() const { return cfg.use_graphs && (!tr || tr->graph_safe()); }
   // GMRES restart cycles as conditional graphs (MGB200_GMRES_LOOP=host: one
   // graph + host sync per Arnoldi step, the round-1 path)
+  bool pdl() const {  // programmatic dependent launch of the V-cycle kernels (MGB200_PDL=0: plain launches)
+    const char *e = std::getenv("MGB200_PDL");
+    return !(e && e[0] == '0');
+  }
   bool mgs_alternate() const {  // MGB200_MGS_ALT=0: every MGS pass sweeps forward (round-1 order)
     const char *e = std::getenv("MGB200_MGS_ALT");
     return !(e && e[0] == '0');
@@ -399,6 +403,31 @@ int ks_for_level(int64_t n_global) {
   return slices < t8 ? 8 : slices < t4 ? 4 : slices < t2 ? 2 : 1;
 }
 
+// Kernel launch of the V-cycle kernels: with programmatic dependent launch
+// (PDL, see kernels.cuh pdl_trigger / pdl_wait) while g_pdl is set by the
+// calling API entry (Tally), a plain launch otherwise.  Captured into CUDA
+// graphs as programmatic edges.
+thread_local bool g_pdl = false;
+template <typename... P, typename... A>
+void kl(void (*k)(P...), unsigned grid, cudaStream_t st, A &&...args) {
+  ++g_tally;
+  if (g_pdl) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(mgk::kCta);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+  } else {
+    k<<<grid, mgk::kCta, 0, st>>>(std::forward<A>(args)...);
+  }
+}
+
 mg_status check_launch(const char *what = "kernel") {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(MG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
@@ -419,33 +448,24 @@ void launch_apply_h(const SellOp &A, In in, const double *b, const double *dinv,
   const unsigned g = grid_for_slices(A.n_slices, A.ks);
   if (A.ks == 8) {
     if (A.f32)
-      ++g_tally, mgk::k_sell_apply<BS, OP, false, HALO, 8, true>
-                     <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+      kl(mgk::k_sell_apply<BS, OP, false, HALO, 8, true>, g, st, A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
     else
-      ++g_tally, mgk::k_sell_apply<BS, OP, false, HALO, 8, false>
-                     <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+      kl(mgk::k_sell_apply<BS, OP, false, HALO, 8, false>, g, st, A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
   } else if (A.f32) {
     if (A.ks == 4)
-      ++g_tally, mgk::k_sell_apply<BS, OP, false, HALO, 4, true>
-                     <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+      kl(mgk::k_sell_apply<BS, OP, false, HALO, 4, true>, g, st, A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
     else if (A.ks == 2)
-      ++g_tally, mgk::k_sell_apply<BS, OP, true, HALO, 2, true>
-                     <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+      kl(mgk::k_sell_apply<BS, OP, true, HALO, 2, true>, g, st, A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
     else
-      ++g_tally, mgk::k_sell_apply<BS, OP, true, HALO, 1, true>
-                     <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+      kl(mgk::k_sell_apply<BS, OP, true, HALO, 1, true>, g, st, A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
   } else if (A.ks == 4)
-    ++g_tally, mgk::k_sell_apply<BS, OP, false, HALO, 4>
-                   <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+    kl(mgk::k_sell_apply<BS, OP, false, HALO, 4>, g, st, A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
   else if (A.ks == 2)
-    ++g_tally, mgk::k_sell_apply<BS, OP, true, HALO, 2>
-                   <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+    kl(mgk::k_sell_apply<BS, OP, true, HALO, 2>, g, st, A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
   else if (A.stream)
-    ++g_tally, mgk::k_sell_apply<BS, OP, true, HALO, 1>
-                   <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+    kl(mgk::k_sell_apply<BS, OP, true, HALO, 1>, g, st, A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
   else
-    ++g_tally, mgk::k_sell_apply<BS, OP, false, HALO, 1>
-                   <<<g, mgk::kCta, 0, st>>>(A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
+    kl(mgk::k_sell_apply<BS, OP, false, HALO, 1>, g, st, A.view(), in.x, in.xg, in.n_own, b, dinv, out, alpha, beta);
 }
 
 template <int BS, int OP>
@@ -473,8 +493,7 @@ mg_status launch_apply(int bs, const SellOp &A, In in, const double *b, const do
 template <int BS>
 void launch_sweep0_t(const SellOp &A, const double *dinv, const double *b, double *x, double omega, cudaStream_t st) {
   if (A.n_slices == 0) return;
-  ++g_tally,
-      mgk::k_sweep0<BS><<<grid_for_slices(A.n_slices), mgk::kCta, 0, st>>>(A.n_slices, A.perm.p, dinv, b, x, omega);
+  kl(mgk::k_sweep0<BS>, grid_for_slices(A.n_slices), st, A.n_slices, A.perm.p, dinv, b, x, omega);
 }
 
 mg_status launch_sweep0(int bs, const SellOp &A, const double *dinv, const double *b, double *x, double omega,
@@ -494,14 +513,11 @@ template <int BS, int WPE, bool ACC, bool HALO>
 void launch_transfer_h(const SellOp &T, In in, double *out, cudaStream_t st) {
   const unsigned g = grid_for_slices(T.n_slices, T.ks);
   if (T.ks > 1)
-    ++g_tally,
-        mgk::k_transfer<BS, WPE, ACC, true, HALO, 4><<<g, mgk::kCta, 0, st>>>(T.view(), in.x, in.xg, in.n_own, out);
+    kl(mgk::k_transfer<BS, WPE, ACC, true, HALO, 4>, g, st, T.view(), in.x, in.xg, in.n_own, out);
   else if (T.stream)
-    ++g_tally,
-        mgk::k_transfer<BS, WPE, ACC, true, HALO, 1><<<g, mgk::kCta, 0, st>>>(T.view(), in.x, in.xg, in.n_own, out);
+    kl(mgk::k_transfer<BS, WPE, ACC, true, HALO, 1>, g, st, T.view(), in.x, in.xg, in.n_own, out);
   else
-    ++g_tally,
-        mgk::k_transfer<BS, WPE, ACC, false, HALO, 1><<<g, mgk::kCta, 0, st>>>(T.view(), in.x, in.xg, in.n_own, out);
+    kl(mgk::k_transfer<BS, WPE, ACC, false, HALO, 1>, g, st, T.view(), in.x, in.xg, in.n_own, out);
 }
 
 template <int BS, int WPE, bool ACC>
@@ -532,7 +548,7 @@ mg_status launch_transfer(int bs, bool acc, const SellOp &T, In in, double *out,
 template <int BS, int WPE, bool ACC, bool HALO, int KS, int NSL>
 void launch_tsell_k(const TSellOp &T, In in, double *out, cudaStream_t st) {
   const unsigned g = grid_for_slices((T.n_slices + NSL - 1) / NSL, KS);
-  ++g_tally, mgk::k_tsell<BS, WPE, ACC, HALO, KS, NSL><<<g, mgk::kCta, 0, st>>>(T.view(), in.x, in.xg, in.n_own, out);
+  kl(mgk::k_tsell<BS, WPE, ACC, HALO, KS, NSL>, g, st, T.view(), in.x, in.xg, in.n_own, out);
 }
 
 // (ks, nsl) = warps per slice group, slices per warp: TSellOp defaults
@@ -1379,7 +1395,7 @@ mg_status coarse_solve(mg_ctx_s *c, const double *b, double *x) {
   if (c->cfg.coarse_mode == MG_COARSE_DIRECT) {
     if (al16(b)) {  // 4 warps per row (d is read with 16-byte loads)
       const unsigned g = unsigned((c->cN + 1) / 2);
-      ++g_tally, mgk::k_dense_gemv_split<4><<<g, mgk::kCta, 0, c->stream>>>(c->cN, c->cld, c->cinv.p, b, x);
+      kl(mgk::k_dense_gemv_split<4>, g, c->stream, c->cN, c->cld, static_cast<const double *>(c->cinv.p), b, x);
     } else {
       const unsigned g = unsigned((c->cN + mgk::kWarpsPerCta - 1) / mgk::kWarpsPerCta);
       ++g_tally, mgk::k_dense_gemv<<<g, mgk::kCta, 0, c->stream>>>(c->cN, c->cld, c->cinv.p, b, x);
@@ -1512,9 +1528,11 @@ mg_status run_vcycle(mg_ctx_s *c, double *x, const double *b, bool zero) {
 struct Tally {
   mg_ctx_s *c;
   int64_t t0;
-  explicit Tally(mg_ctx_s *ctx) : c(ctx), t0(g_tally) {}
+  bool pdl0;
+  explicit Tally(mg_ctx_s *ctx) : c(ctx), t0(g_tally), pdl0(g_pdl) { g_pdl = ctx && ctx->pdl(); }
   ~Tally() {
     if (c) c->launches += g_tally - t0;
+    g_pdl = pdl0;
   }
 };
 
