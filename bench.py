@@ -518,12 +518,28 @@ def run_ours(args):
         torch.cuda.synchronize()
         upd_ms = 1e3 * (time.perf_counter() - t)
         hv = np.ascontiguousarray(P.levels[L].val.reshape(-1))
-        t = time.perf_counter()
-        mg.mg_update_matrix(ctx, L, hv)
-        torch.cuda.synchronize()
-        upd = {"all_levels_device_ms": upd_ms, "finest_from_host_ms": 1e3 * (time.perf_counter() - t),
-               "note": "mg_update_matrix: device scatter through the entry map + device D^-1 (+ coarse "
-                       "Gauss-Jordan on level 0); graphs stay valid"}
+        hp = torch.from_numpy(hv).pin_memory()
+
+        def _host_upd(src):  # best of 3 (the first call also sizes the staging buffers)
+            best = float("inf")
+            for _ in range(3):
+                torch.cuda.synchronize()
+                t = time.perf_counter()
+                mg.mg_update_matrix(ctx, L, src)
+                torch.cuda.synchronize()
+                best = min(best, 1e3 * (time.perf_counter() - t))
+            return best
+        fin_pageable, fin_pinned = _host_upd(hv), _host_upd(hp)
+        gb = hv.nbytes / 1e9
+        upd = {"all_levels_device_ms": upd_ms, "finest_from_host_ms": fin_pageable,
+               "finest_from_pinned_host_ms": fin_pinned, "finest_gb": gb,
+               "finest_from_host_gbs": gb / (fin_pageable / 1e3),
+               "finest_from_pinned_host_gbs": gb / (fin_pinned / 1e3),
+               "note": "mg_update_matrix of the finest level from host memory (pageable numpy / pinned torch), "
+                       "wall time of the whole call incl. device scatter through the entry map, device D^-1 "
+                       "and the host sync, best of 3; all_levels_device_ms = every level from device memory; "
+                       "graphs stay valid"}
+        del hp
         del dvals
 
     # ---------------- per-level split of one (eager) V-cycle --------------------
