@@ -185,4 +185,5 @@ def bsr_to_dense(n, bs, rp, col, val):
     return A
 
 
-from .mg import (MgHierarchy, MgLevel, consistent, gmres, project_zero_mean, richardson, vcycle)  # noqa: E402,F401
+from .mg import (MgHierarchy, MgLevel, consistent, gmres, gmres_dcgs2, project_zero_mean, richardson,  # noqa: E402,F401
+                 vcycle)

@@ -288,6 +288,139 @@ def gmres(h: MgHierarchy, b, x0=None, rtol=1e-10, restart=30, max_iter=200, prec
     return x, its, hist, beta / beta0
 
 
+def gmres_dcgs2(h: MgHierarchy, b, x0=None, rtol=1e-10, restart=30, max_iter=200, op=None):
+    """Right-preconditioned GMRES(m) whose Arnoldi basis is orthogonalised by
+    classical Gram-Schmidt with ONE delayed reorthogonalisation (DCGS2; reading
+    Z29 in DESIGN.md -- an opt-in alternative to the paper's MGS, with
+    the same Krylov space and the same minimal-residual iterate in exact
+    arithmetic).  Step j, with Q_{j-1} = [q_0 .. q_{j-1}] final and u_j the
+    once-projected (not normalised) new direction:
+      1. z_j = B u_j (V-cycle), w^ = A z_j;
+      2. one reduction: a = Q_{j-1}^T u_j, nu = u_j^T u_j, bb = Q_{j-1}^T w^,
+         mu = u_j^T w^;
+      3. beta = sqrt(nu - a^T a); q_j = (u_j - Q_{j-1} a) / beta; column j-1 of
+         the Hessenberg matrix becomes final: [s_{j-1} + a ; beta];
+      4. w_j = A B q_j = (w^ - Q_j t) / beta with t = Hbar_{j-1} a (Arnoldi
+         relation A B Q_{j-1} = Q_j Hbar_{j-1}); its first projection
+         s_j = Q_j^T w_j = [(bb - t_{0:j}) / beta ; ((mu - a^T bb)/beta - t_j)/beta];
+      5. u_{j+1} = w_j - Q_j s_j = w^/beta - Q_j (t/beta + s_j);
+      6. the tentative column j = [s_j ; ||u_{j+1}||] gives the Givens estimate
+         |g_{j+1}| that ends the cycle (its reorthogonalisation correction is
+         O(eps) and is folded in at step j+1 by redoing rotation j).
+    Since z_j = B u_j and U = Q R (R upper triangular: R[:j, j] = a, R[j, j] =
+    beta), the update is x += Z (R^{-1} y) with y from H y = g.
+    Returns x, iterations, history of estimates, true relative residual (as gmres)."""
+    Lf = len(h.levels) - 1
+    F = h.levels[-1] if op is None else op
+    N = F.n * F.bs
+    mc = h.mean[-1] if h.mean is not None else None
+    if mc is not None:
+        b = consistent(b, mc[1])
+    x = np.zeros(N) if x0 is None else np.array(x0, np.float64)
+    r = residual(F.n, F.bs, F.rp, F.col, F.val, x, b)
+    beta0 = nrm2(r)
+    hist = [1.0]
+    if beta0 == 0.0:
+        return x, 0, hist, 0.0
+    its = 0
+    beta_true = beta0
+    while its < max_iter:
+        m = min(restart, max_iter - its)
+        Q = np.zeros((m + 1, N))       # slot j: u_j until step j turns it into q_j
+        Z = np.zeros((m, N))           # z_j = B u_j
+        Hraw = np.zeros((m + 1, m))    # unrotated Hessenberg columns (final or tentative)
+        R = np.zeros((m, m))
+        cs, sn = np.zeros(m), np.zeros(m)
+        g = np.zeros(m + 1)
+        gpre = np.zeros(m + 1)         # g_j before rotation j (rotation j is redone at step j+1)
+        Q[0] = r
+        k = 0
+        happy = False
+
+        def rotate(j):                  # rotations 0..j-1 applied to raw column j, then rotation j
+            col = Hraw[:j + 2, j].copy()
+            for i in range(j):
+                t = cs[i] * col[i] + sn[i] * col[i + 1]
+                col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1]
+                col[i] = t
+            rho = np.hypot(col[j], col[j + 1])
+            cs[j] = col[j] / rho
+            sn[j] = col[j + 1] / rho
+            g[j + 1] = -sn[j] * gpre[j]
+            g[j] = cs[j] * gpre[j]
+
+        for j in range(m):
+            u = Q[j]
+            Z[j] = vcycle(h, Lf, np.zeros(N), u)
+            its += 1
+            wh = spmv(F.n, F.bs, F.rp, F.col, F.val, Z[j])
+            a = np.array([dot(Q[i], u) for i in range(j)])
+            bb = np.array([dot(Q[i], wh) for i in range(j)])
+            nu = dot(u, u)
+            mu = dot(u, wh)
+            beta = np.sqrt(max(nu - float(a @ a) if j else nu, 0.0))
+            R[:j, j] = a
+            R[j, j] = beta
+            if j == 0:
+                g[0] = beta                            # = ||r0|| of this cycle
+            else:
+                Hraw[:j, j - 1] += a                   # column j-1 final: [s_{j-1} + a ; beta]
+                Hraw[j, j - 1] = beta
+                rotate(j - 1)
+            if beta == 0.0:                            # u_j in span(Q_{j-1}): breakdown at j-1
+                happy = True
+                break
+            t = Hraw[:j + 1, :j] @ a if j else np.zeros(1)
+            s = np.empty(j + 1)
+            s[:j] = (bb - t[:j]) / beta
+            s[j] = ((mu - float(a @ bb) if j else mu) / beta - t[j]) / beta
+            c = t / beta + s
+            q = u.copy()
+            for i in range(j):
+                q = q - a[i] * Q[i]
+            q = q / beta
+            un = wh / beta
+            for i in range(j):
+                un = un - c[i] * Q[i]
+            un = un - c[j] * q
+            Q[j] = q
+            Q[j + 1] = un
+            hn = nrm2(un)
+            Hraw[:j + 1, j] = s                         # tentative column j
+            Hraw[j + 1, j] = hn
+            gpre[j] = g[j]
+            rotate(j)
+            hist.append(abs(g[j + 1]) / beta0)
+            k = j + 1
+            if abs(g[j + 1]) <= rtol * beta0 or hn == 0.0:
+                happy = hn == 0.0
+                break
+        if k:
+            Hr = np.zeros((k, k))                      # rotated H (upper triangular)
+            for jj in range(k):
+                col = Hraw[:jj + 2, jj].copy()
+                for i in range(jj + 1):
+                    t = cs[i] * col[i] + sn[i] * col[i + 1]
+                    col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1]
+                    col[i] = t
+                Hr[:jj + 1, jj] = col[:jj + 1]
+            y = np.zeros(k)                            # back substitution H y = g
+            for i in range(k - 1, -1, -1):
+                y[i] = (g[i] - Hr[i, i + 1:k] @ y[i + 1:k]) / Hr[i, i]
+            yp = np.zeros(k)                           # R y' = y
+            for i in range(k - 1, -1, -1):
+                yp[i] = (y[i] - R[i, i + 1:k] @ yp[i + 1:k]) / R[i, i]
+            for i in range(k):
+                x = x + yp[i] * Z[i]
+        r = residual(F.n, F.bs, F.rp, F.col, F.val, x, b)
+        beta_true = nrm2(r)
+        if happy or beta_true <= rtol * beta0:
+            break
+    if mc is not None:
+        x = project_zero_mean(x, *mc)
+    return x, its, hist, beta_true / beta0
+
+
 def apply_H(H, x, bs):
     """x <- H x after the solve (reading Z7)."""
     rp, col, w = H
