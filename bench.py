@@ -386,7 +386,8 @@ def run_ours(args):
     b_host = torch.from_numpy(np.ascontiguousarray(b_np)).pin_memory()
     b = b_host.cuda()
     x = torch.zeros(N, dtype=torch.float64, device="cuda")
-    opts = dict(restart=30, max_iter=200, rtol=args.rtol)
+    orth_method = {"mgs": mg.MG_GMRES, "dcgs2": mg.MG_GMRES_DCGS2}
+    opts = dict(restart=30, max_iter=200, rtol=args.rtol, method=orth_method[args.orth])
 
     def step(xv, bv):
         xv.zero_()
@@ -581,6 +582,47 @@ def run_ours(args):
         with open(tp) as f:
             traffic = json.load(f).get(args.config, {}).get("sweep_fine_dram_bytes")
 
+    # ---------------- the other GMRES orthogonalisation on the same workload ----
+    # MGS (the paper's) vs delayed CGS2 (reading Z29): same solver, same
+    # graphs for the V-cycles, only the Arnoldi orthogonalisation differs
+    orth_side = None
+    if not args.no_orth_side:
+        other = "dcgs2" if args.orth == "mgs" else "mgs"
+        o_opts = dict(opts, method=orth_method[other])
+
+        def ostep(xv, bv):
+            xv.zero_()
+            st, its, rel, conv = solver.solve(xv, bv, **o_opts)
+            if not conv:
+                raise RuntimeError(f"{other} solve did not converge: {its} its, rel {rel:.3e}")
+            if H is not None:
+                solver.apply_constraints(xv)
+            return its, rel
+        for _ in range(args.warmup):
+            ostep(x, b)
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        o_its = 0
+        for _ in range(args.steps):
+            its, rel = ostep(x, b)
+            o_its += its
+        e1.record(stream)
+        torch.cuda.synchronize()
+        o_ms = e0.elapsed_time(e1)
+        if ws > 1:
+            tt = torch.tensor([o_ms], dtype=torch.float64, device=red)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            o_ms = float(tt[0])
+        orth_side = {"orth": other, "value": o_its / (o_ms / 1e3), "unit": "V-cycles/s",
+                     "solve_ms": o_ms / args.steps, "iterations_per_solve": o_its / args.steps,
+                     "true_rel_residual": rel,
+                     "allreduces_per_arnoldi_step": "2" if other == "dcgs2" else "j + 2 (step j)",
+                     "vector_passes_per_arnoldi_step": "2j + 6" if other == "dcgs2" else "4j + 7",
+                     "note": "same solve with the other Arnoldi orthogonalisation: mgs = the paper's modified "
+                             "Gram-Schmidt (P:346), dcgs2 = classical Gram-Schmidt with one delayed "
+                             "reorthogonalisation (DESIGN.md Z29)"}
+
     # ---------------- mixed precision on the same workload ---------
     mixed = None
     if ws == 1 and args.precision == "fp64" and not args.no_mixed:
@@ -664,6 +706,8 @@ def run_ours(args):
                               "halo_ms": prof["halo_ms"], "agglomeration_ms": prof["agglomeration_ms"],
                               "note": "one eager V(2,2) from zero, CUDA events between phases"},
             "paper_context": PAPER_CONTEXT.get(args.config),
+            "orth": args.orth,
+            "orth_other": orth_side,
             "mixed_precision": mixed,
             "update_matrix": upd,
             "vcycle_only": {"ms": vc_ms, "per_s": 1e3 / vc_ms, "batch_ms": batches,
@@ -937,6 +981,9 @@ def main():
     ap.add_argument("--no-cpu-solve", action="store_true", help="skip the oracle's full GMRES solve in cpu_baseline")
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--no-mixed", action="store_true", help="skip the mixed-precision side measurement")
+    ap.add_argument("--orth", choices=["mgs", "dcgs2"], default="mgs",
+                    help="GMRES orthogonalisation of the timed solve: mgs (the paper's, P:346) or dcgs2 (Z29)")
+    ap.add_argument("--no-orth-side", action="store_true", help="skip timing the other orthogonalisation")
     ap.add_argument("--precision", choices=["fp64", "mixed"], default="fp64",
                     help="mixed: fp32-stored V-cycle operators inside fp64 GMRES (SURVEY N1)")
     ap.add_argument("--vanka", action="store_true", help="c4ns / ns: Vanka-type cell-patch smoother (P:822)")

@@ -80,7 +80,7 @@ typedef enum {
 enum { MG_MEM_HOST = 0, MG_MEM_DEVICE = 1 };
 enum { MG_TRANSPORT_NCCL = 0, MG_TRANSPORT_LOCAL = 1, MG_TRANSPORT_IPC = 2 };
 enum { MG_COARSE_DIRECT = 0, MG_COARSE_SMOOTH = 1 };
-enum { MG_GMRES = 0, MG_RICHARDSON = 1 };
+enum { MG_GMRES = 0, MG_RICHARDSON = 1, MG_GMRES_DCGS2 = 2 };
 enum { MG_PREC_FP64 = 0, MG_PREC_MIXED = 1 };
 
 /* Global multigrid configuration (SPEC MgConfig; readings Z1-Z3).
@@ -139,7 +139,12 @@ typedef struct {
 } mg_comm;
 
 /* Solve options (SPEC GmresConfig S:410-413; reading Z5).
- * method: MG_GMRES (right-preconditioned GMRES(restart), MGS + Givens) or
+ * method: MG_GMRES (right-preconditioned GMRES(restart), MGS + Givens),
+ *   MG_GMRES_DCGS2 (the same GMRES with the basis orthogonalised by classical
+ *   Gram-Schmidt with one delayed reorthogonalisation: one multi-dot pass and
+ *   one update pass per Arnoldi step, 2 all-reduces instead of j + 2; same
+ *   Krylov space and minimal-residual iterate, an opt-in departure from the
+ *   paper's MGS, reading Z29; restart <= 64) or
  *   MG_RICHARDSON (x <- GMG(L, x, b));
  * max_iter: maximum number of preconditioner applications (= V-cycles);
  * rtol: stop when ||b - A x||_2 <= rtol * ||b - A x0||_2 (GMRES: the Givens

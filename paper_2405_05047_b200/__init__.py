@@ -32,7 +32,7 @@ MG_ERR_INVALID_ARG, MG_ERR_DIMENSION, MG_ERR_STRUCTURE, MG_ERR_NONFINITE = -1, -
 MG_ERR_SINGULAR, MG_ERR_STATE, MG_ERR_CUDA, MG_ERR_NCCL, MG_ERR_OOM = -5, -6, -7, -8, -9
 MG_MEM_HOST, MG_MEM_DEVICE = 0, 1
 MG_COARSE_DIRECT, MG_COARSE_SMOOTH = 0, 1
-MG_GMRES, MG_RICHARDSON = 0, 1
+MG_GMRES, MG_RICHARDSON, MG_GMRES_DCGS2 = 0, 1, 2
 MG_TRANSPORT_NCCL, MG_TRANSPORT_LOCAL, MG_TRANSPORT_IPC = 0, 1, 2
 MG_PREC_FP64, MG_PREC_MIXED = 0, 1
 

@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace mgk {
 
 constexpr int kWarpsPerCta = 8;
@@ -186,41 +188,60 @@ __device__ __forceinline__ void sell_apply_task(const Sell &A, int64_t task, con
     // Few bytes per entry (fp32 values, or bs <= 2): issue the loads of UB
     // entries before the first use so enough bytes are in flight per warp.
     // Entries are still accumulated in order (bit-identical to UB = 1).
+    // Rows are processed in batches of UB entries whose loads are all issued
+    // before their (in-order) FMAs; the last, partial batch of a slice is a
+    // batch of exactly the remaining count (a warp-uniform switch over
+    // compile-time sizes), so short rows -- 9 entries of a 2D Q1 row, 4-5 per
+    // warp under split-k 2 -- are one batch of independent loads instead of a
+    // dependent column -> x chain per entry.  Summation order unchanged.
     constexpr int UB = F32 ? 4 : (V == 1 ? 8 : (V == 4 ? 4 : 1));
     if constexpr (UB > 1) {
       constexpr int step = 32 * KS;
-      for (; g + (UB - 1) * step < e1; g += UB * step) {
-        int cc[UB];
+      auto batch = [&](auto NC) {
+        constexpr int N = decltype(NC)::value;
+        int cc[N];
         cc[0] = cn;
 #pragma unroll
-        for (int u = 1; u < UB; ++u) cc[u] = ld_col<STREAM>(A.col + g + u * step + lane);
-        if (g + UB * step < e1) cn = ld_col<STREAM>(A.col + g + UB * step + lane);
-        double vd[UB][V];
+        for (int u = 1; u < N; ++u) cc[u] = ld_col<STREAM>(A.col + g + u * step + lane);
+        if (g + N * step < e1) cn = ld_col<STREAM>(A.col + g + N * step + lane);
+        double vd[N][V];
         if constexpr (F32) {
-          float vf[UB][V];
+          float vf[N][V];
 #pragma unroll
-          for (int u = 0; u < UB; ++u) load_entry_raw<V, STREAM>(A.valf + (g + u * step) * V, lane, vf[u]);
+          for (int u = 0; u < N; ++u) load_entry_raw<V, STREAM>(A.valf + (g + u * step) * V, lane, vf[u]);
 #pragma unroll
-          for (int u = 0; u < UB; ++u)
+          for (int u = 0; u < N; ++u)
 #pragma unroll
             for (int j = 0; j < V; ++j) vd[u][j] = double(vf[u][j]);
         } else {
 #pragma unroll
-          for (int u = 0; u < UB; ++u) load_entry<V, STREAM>(A.val + (g + u * step) * V, lane, vd[u]);
+          for (int u = 0; u < N; ++u) load_entry<V, STREAM>(A.val + (g + u * step) * V, lane, vd[u]);
         }
-        double xv[UB][BS];
+        double xv[N][BS];
 #pragma unroll
-        for (int u = 0; u < UB; ++u) {
+        for (int u = 0; u < N; ++u) {
           const double *xc = col_ptr<BS, HALO>(x, xg, n_own, cc[u]);
 #pragma unroll
           for (int q = 0; q < BS; ++q) xv[u][q] = ldv<CG>(xc + q);
         }
 #pragma unroll
-        for (int u = 0; u < UB; ++u)
+        for (int u = 0; u < N; ++u)
 #pragma unroll
           for (int r = 0; r < BS; ++r)
 #pragma unroll
             for (int q = 0; q < BS; ++q) acc[r] = fma(vd[u][r * BS + q], xv[u][q], acc[r]);
+        g += N * step;
+      };
+      while (g + (UB - 1) * step < e1) batch(std::integral_constant<int, UB>{});
+      switch (int((e1 - g + step - 1) / step)) {  // 0 .. UB-1 entries left
+        case 1: batch(std::integral_constant<int, 1>{}); break;
+        case 2: batch(std::integral_constant<int, 2>{}); break;
+        case 3: batch(std::integral_constant<int, 3>{}); break;
+        case 4: if constexpr (UB > 4) batch(std::integral_constant<int, (UB > 4 ? 4 : 1)>{}); break;
+        case 5: if constexpr (UB > 5) batch(std::integral_constant<int, (UB > 5 ? 5 : 1)>{}); break;
+        case 6: if constexpr (UB > 6) batch(std::integral_constant<int, (UB > 6 ? 6 : 1)>{}); break;
+        case 7: if constexpr (UB > 7) batch(std::integral_constant<int, (UB > 7 ? 7 : 1)>{}); break;
+        default: break;
       }
     }
 #pragma unroll 4
@@ -340,37 +361,39 @@ __device__ __forceinline__ void transfer_task(const Sell &T, int64_t task, const
     int64_t g = e0 + 32 * sub;
     int cn = g < e1 ? ld_col<STREAM>(T.col + g + lane) : 0;
     if constexpr (WAIT) pdl_wait();
-    constexpr int UB = 4;  // scalar weights: batch the loads of 4 entries (summed in order)
+    // batches of UB entries' loads in flight (summed in order); the last batch
+    // of exactly the remaining count, as in sell_apply_task, so a 1-8-entry
+    // prolongation row is one batch
+    constexpr int UB = 4;
     constexpr int step = 32 * KS;
-    for (; g + (UB - 1) * step < e1; g += UB * step) {
-      int cc[UB];
+    auto batch = [&](auto NC) {
+      constexpr int N = decltype(NC)::value;
+      int cc[N];
       cc[0] = cn;
 #pragma unroll
-      for (int u = 1; u < UB; ++u) cc[u] = ld_col<STREAM>(T.col + g + u * step + lane);
-      if (g + UB * step < e1) cn = ld_col<STREAM>(T.col + g + UB * step + lane);
-      double w[UB][WPE], xv[UB][BS];
+      for (int u = 1; u < N; ++u) cc[u] = ld_col<STREAM>(T.col + g + u * step + lane);
+      if (g + N * step < e1) cn = ld_col<STREAM>(T.col + g + N * step + lane);
+      double w[N][WPE], xv[N][BS];
 #pragma unroll
-      for (int u = 0; u < UB; ++u) load_entry<WPE, STREAM>(T.val + (g + u * step) * WPE, lane, w[u]);
+      for (int u = 0; u < N; ++u) load_entry<WPE, STREAM>(T.val + (g + u * step) * WPE, lane, w[u]);
 #pragma unroll
-      for (int u = 0; u < UB; ++u) {
+      for (int u = 0; u < N; ++u) {
         const double *xc = col_ptr<BS, HALO>(in, ing, n_own, cc[u]);
 #pragma unroll
         for (int q = 0; q < BS; ++q) xv[u][q] = ldv<CG>(xc + q);
       }
 #pragma unroll
-      for (int u = 0; u < UB; ++u)
+      for (int u = 0; u < N; ++u)
 #pragma unroll
         for (int q = 0; q < BS; ++q) acc[q] = fma(w[u][WPE == 1 ? 0 : q], xv[u][q], acc[q]);
-    }
-#pragma unroll 4
-    for (; g < e1; g += 32 * KS) {
-      const int c = cn;
-      if (g + 32 * KS < e1) cn = ld_col<STREAM>(T.col + g + 32 * KS + lane);
-      double w[WPE];
-      load_entry<WPE, STREAM>(T.val + g * WPE, lane, w);
-      const double *xc = col_ptr<BS, HALO>(in, ing, n_own, c);
-#pragma unroll
-      for (int q = 0; q < BS; ++q) acc[q] = fma(w[WPE == 1 ? 0 : q], ldv<CG>(xc + q), acc[q]);
+      g += N * step;
+    };
+    while (g + (UB - 1) * step < e1) batch(std::integral_constant<int, UB>{});
+    switch (int((e1 - g + step - 1) / step)) {
+      case 1: batch(std::integral_constant<int, 1>{}); break;
+      case 2: batch(std::integral_constant<int, 2>{}); break;
+      case 3: batch(std::integral_constant<int, 3>{}); break;
+      default: break;
     }
   }
   if constexpr (WAIT) pdl_wait();
@@ -453,23 +476,28 @@ __global__ void __launch_bounds__(kCta) k_tsell(TSell T, const double *__restric
     }
   };
   if constexpr (NSL == 1) {
+    // loads of UB entries in flight before their use (summed in order); the last
+    // batch of exactly the remaining count (len is uniform over the slice)
+    constexpr int UB = 4;
     int64_t k = sub;
-    constexpr int UB = 4;  // loads of 4 entries in flight before their use (summed in order)
-    for (; k + (UB - 1) * KS < len[0]; k += UB * KS) {
-      int c[UB];
-      double w[UB], v[UB];
+    auto batch = [&](auto NC) {
+      constexpr int N = decltype(NC)::value;
+      int c[N];
+      double w[N], v[N];
 #pragma unroll
-      for (int u = 0; u < UB; ++u) entry(eb[0] + (k + u * KS) * C, c[u], w[u]);
+      for (int u = 0; u < N; ++u) entry(eb[0] + (k + u * KS) * C, c[u], w[u]);
 #pragma unroll
-      for (int u = 0; u < UB; ++u) v[u] = __ldg(col_ptr<BS, HALO>(in, ing, n_own, c[u]) + q);
+      for (int u = 0; u < N; ++u) v[u] = __ldg(col_ptr<BS, HALO>(in, ing, n_own, c[u]) + q);
 #pragma unroll
-      for (int u = 0; u < UB; ++u) acc[0] = fma(w[u], v[u], acc[0]);
-    }
-    for (; k < len[0]; k += KS) {
-      int c;
-      double w;
-      entry(eb[0] + k * C, c, w);
-      acc[0] = fma(w, __ldg(col_ptr<BS, HALO>(in, ing, n_own, c) + q), acc[0]);
+      for (int u = 0; u < N; ++u) acc[0] = fma(w[u], v[u], acc[0]);
+      k += N * KS;
+    };
+    while (k + (UB - 1) * KS < len[0]) batch(std::integral_constant<int, UB>{});
+    switch (int(k < len[0] ? (len[0] - k + KS - 1) / KS : 0)) {
+      case 1: batch(std::integral_constant<int, 1>{}); break;
+      case 2: batch(std::integral_constant<int, 2>{}); break;
+      case 3: batch(std::integral_constant<int, 3>{}); break;
+      default: break;
     }
   } else {
     for (int64_t k = sub; k < kmax; k += KS) {
@@ -841,6 +869,15 @@ struct GmresDev {
   double *beta0;  // initial residual norm
   double *out;    // [4]: est = |g_{j+1}|/beta0, flag, ...
   int m;
+  // delayed-CGS2 orthogonalisation (MG_GMRES_DCGS2, reading Z29)
+  double *Hraw;   // (m+1) x m unrotated Hessenberg columns (final, last one tentative)
+  double *R;      // m x m upper triangular, U = Q R
+  double *gpre;   // [m+1] g_j before rotation j
+  double *dots;   // [2m+2] a, bb, nu, mu of the step's reduction
+  double *coef;   // [2m+2] a, c, 1/beta
+  double *nu1;    // ||u_{j+1}||^2
+  double *dead;   // 1: breakdown found at the start of a step (u_j in span Q)
+  double *y2;     // [m] R^{-1} y
 };
 
 // v0 = r / beta; g = (beta, 0, ...)
@@ -930,6 +967,273 @@ __global__ void k_update_x(int64_t n, int k, const double *__restrict__ y, const
     double v = x[i];
     for (int t = 0; t < k; ++t) v = fma(ys[t], __ldg(Z + int64_t(t) * ldz + i), v);
     x[i] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// GMRES with delayed classical Gram-Schmidt reorthogonalisation (DCGS2,
+// MG_GMRES_DCGS2; reading Z29, oracle.gmres_dcgs2): per Arnoldi step ONE
+// multi-dot pass (k_dcgs_dots: Q_{j-1}^T u_j, Q_{j-1}^T w^, u_j^T u_j,
+// u_j^T w^) and ONE update pass (k_dcgs_update: q_j and u_{j+1}, fused
+// ||u_{j+1}||^2) -- 2j + 6 vector passes and 2 all-reduces per step, against
+// 4j + 7 passes and j + 2 all-reduces of the paper's MGS.  Q slots at
+// stride ldq; slot j holds u_j until the update turns it into q_j; w^ = A z_j
+// is written into slot j + 1, where the update leaves u_{j+1}.
+// ---------------------------------------------------------------------------
+// Block + grid reduction of NO values per thread (deterministic: warp shuffles,
+// warps in order, CTAs in order by the last CTA).
+// Block + grid reduction of NO per-thread values to nout outputs, value o going
+// to output map(o) (< 0: dropped).  Deterministic: warp shuffles, warps in
+// order, CTAs in order by the last CTA to arrive.
+template <int NO, class Map>
+__device__ __forceinline__ void grid_reduce_many(const double (&v)[NO], int nout, Map map, double *part,
+                                                 unsigned *ticket, double *out) {
+  __shared__ double sh[kRedThreads / 32][NO];
+  __shared__ bool last;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 0; o < NO; ++o) {
+    const int d = map(o);
+    if (d < 0) continue;
+    double t = v[o];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if (lane == 0) sh[w][d] = t;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < nout; o += blockDim.x) {
+    double t = 0.0;
+    for (int ww = 0; ww < int(blockDim.x >> 5); ++ww) t += sh[ww][o];
+    part[int64_t(blockIdx.x) * nout + o] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int o = threadIdx.x; o < nout; o += blockDim.x) {
+    double t = 0.0;
+    for (int b = 0; b < int(gridDim.x); ++b) t += __ldcg(part + int64_t(b) * nout + o);
+    out[o] = t;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+// out = [a (j) | bb (j) | nu | mu]; JB >= j (template bucket: accumulators in registers)
+template <int JB>
+__global__ void __launch_bounds__(kRedThreads) k_dcgs_dots(int64_t n, int j, const double *__restrict__ Q,
+                                                           int64_t ldq, double *part, unsigned *ticket,
+                                                           double *out) {
+  double acc[2 * JB + 2];
+#pragma unroll
+  for (int o = 0; o < 2 * JB + 2; ++o) acc[o] = 0.0;
+  const double *u = Q + int64_t(j) * ldq, *wh = Q + int64_t(j + 1) * ldq;
+  const int64_t n2 = n / 2;
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  auto body = [&](double2 uu, double2 ww, auto ldq_i) {
+    double2 q[JB];
+#pragma unroll
+    for (int i = 0; i < JB; ++i)
+      if (i < j) q[i] = ldq_i(i);
+#pragma unroll
+    for (int i = 0; i < JB; ++i)
+      if (i < j) {
+        acc[i] = fma(q[i].y, uu.y, fma(q[i].x, uu.x, acc[i]));
+        acc[JB + i] = fma(q[i].y, ww.y, fma(q[i].x, ww.x, acc[JB + i]));
+      }
+    acc[2 * JB] = fma(uu.y, uu.y, fma(uu.x, uu.x, acc[2 * JB]));
+    acc[2 * JB + 1] = fma(uu.y, ww.y, fma(uu.x, ww.x, acc[2 * JB + 1]));
+  };
+  for (int64_t e = tid; e < n2; e += stride)
+    body(__ldcs(reinterpret_cast<const double2 *>(u) + e), __ldcs(reinterpret_cast<const double2 *>(wh) + e),
+         [&](int i) { return __ldg(reinterpret_cast<const double2 *>(Q + int64_t(i) * ldq) + e); });
+  if ((n & 1) && tid == 0)  // the odd last element (zero second half)
+    body(make_double2(u[n - 1], 0.0), make_double2(wh[n - 1], 0.0),
+         [&](int i) { return make_double2(Q[int64_t(i) * ldq + n - 1], 0.0); });
+  auto map = [j](int o) {
+    if (o < JB) return o < j ? o : -1;
+    if (o < 2 * JB) return o - JB < j ? j + o - JB : -1;
+    return 2 * j + (o - 2 * JB);
+  };
+  grid_reduce_many<2 * JB + 2>(acc, 2 * j + 2, map, part, ticket, out);
+}
+
+// rotations 0..jj-1 applied to raw column jj, rotation jj formed, rotated column
+// stored in H, g updated from gpre[jj]
+__device__ __forceinline__ void dcgs_rotate(GmresDev &st, int jj) {
+  const int ld = st.m + 1;
+  const double *raw = st.Hraw + int64_t(jj) * ld;
+  double *h = st.H + int64_t(jj) * ld;
+  for (int i = 0; i <= jj + 1; ++i) h[i] = raw[i];
+  for (int i = 0; i < jj; ++i) {
+    const double t = st.cs[i] * h[i] + st.sn[i] * h[i + 1];
+    h[i + 1] = -st.sn[i] * h[i] + st.cs[i] * h[i + 1];
+    h[i] = t;
+  }
+  const double rho = hypot(h[jj], h[jj + 1]);
+  st.cs[jj] = h[jj] / rho;
+  st.sn[jj] = h[jj + 1] / rho;
+  h[jj] = rho;
+  h[jj + 1] = 0.0;
+  st.g[jj + 1] = -st.sn[jj] * st.gpre[jj];
+  st.g[jj] = st.cs[jj] * st.gpre[jj];
+}
+
+__global__ void k_dcgs_start(GmresDev st) {
+  for (int i = threadIdx.x; i < (st.m + 1) * st.m; i += blockDim.x) st.Hraw[i] = 0.0;
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    for (int i = 0; i <= st.m; ++i) st.g[i] = st.gpre[i] = 0.0;
+    *st.dead = 0.0;
+  }
+}
+
+// After the step's reduction: beta, column j of R, column j-1 made final (its
+// rotation redone), the coefficients of the update pass.  A breakdown (u_j in
+// span Q_{j-1}) ends the cycle with k = j steps.
+__global__ void k_dcgs_coef(GmresDev st, int j, int mm, cudaGraphConditionalHandle hw, int cond) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int ld = st.m + 1;
+  const double *a = st.dots, *bb = st.dots + j;
+  const double nu = st.dots[2 * j], mu = st.dots[2 * j + 1];
+  double aa = 0.0, ab = 0.0;
+  for (int i = 0; i < j; ++i) aa += a[i] * a[i], ab += a[i] * bb[i];
+  const double beta = sqrt(fmax(j ? nu - aa : nu, 0.0));
+  double *Rc = st.R + int64_t(j) * st.m;
+  for (int i = 0; i < j; ++i) Rc[i] = a[i];
+  Rc[j] = beta;
+  if (j == 0) {
+    st.g[0] = beta;
+  } else {
+    double *raw = st.Hraw + int64_t(j - 1) * ld;
+    for (int i = 0; i < j; ++i) raw[i] += a[i];
+    raw[j] = beta;
+    dcgs_rotate(st, j - 1);
+  }
+  double *cf = st.coef;
+  if (!(beta > 0.0) || !isfinite(beta)) {  // breakdown: the cycle ends after j steps
+    *st.dead = 1.0;
+    st.out[0] = j ? fabs(st.g[j]) / *st.beta0 : 0.0;
+    st.out[1] = 1.0;
+    st.out[2] = 0.0;
+    st.out[3] = double(j);
+    st.out[4] = double(j + 1);
+    for (int i = 0; i < 2 * j + 2; ++i) cf[i] = 0.0;
+    if (cond) cudaGraphSetConditional(hw, 0u);
+    return;
+  }
+  const double ib = 1.0 / beta;
+  double *sraw = st.Hraw + int64_t(j) * ld;
+  for (int i = 0; i <= j; ++i) {
+    double t = 0.0;  // t = Hbar_{j-1} a
+    for (int l = 0; l < j; ++l) t += st.Hraw[int64_t(l) * ld + i] * a[l];
+    const double s = i < j ? (bb[i] - t) / beta : ((mu - ab) / beta - t) / beta;
+    sraw[i] = s;
+    cf[j + i] = t / beta + s;
+  }
+  for (int i = 0; i < j; ++i) cf[i] = a[i];
+  cf[2 * j + 1] = ib;
+}
+
+// q_j = (u_j - Q_{j-1} a) / beta ; u_{j+1} = w^/beta - Q_{j-1} c_{0:j} - c_j q_j ;
+// nu1 = ||u_{j+1}||^2.  coef = [a (j) | c (j+1) | 1/beta].
+template <int JB>
+__global__ void __launch_bounds__(kRedThreads) k_dcgs_update(int64_t n, int j, double *__restrict__ Q, int64_t ldq,
+                                                             const double *__restrict__ coef, const double *dead,
+                                                             double *part, unsigned *ticket, double *nu1) {
+  __shared__ double cf[2 * JB + 2];
+  for (int i = threadIdx.x; i < 2 * j + 2; i += blockDim.x) cf[i] = coef[i];
+  __syncthreads();
+  double s = 0.0;
+  if (*dead == 0.0) {
+    double *u = Q + int64_t(j) * ldq, *wh = Q + int64_t(j + 1) * ldq;
+    const double ib = cf[2 * j + 1], cj = cf[2 * j];
+    const int64_t n2 = n / 2;
+    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    auto body = [&](double2 uu, double2 ww, auto ldq_i) {
+      double2 q[JB];
+#pragma unroll
+      for (int i = 0; i < JB; ++i)
+        if (i < j) q[i] = ldq_i(i);
+      double2 qj = uu, un = make_double2(ww.x * ib, ww.y * ib);
+#pragma unroll
+      for (int i = 0; i < JB; ++i)
+        if (i < j) {
+          qj.x = fma(-cf[i], q[i].x, qj.x);
+          qj.y = fma(-cf[i], q[i].y, qj.y);
+        }
+      qj.x *= ib;
+      qj.y *= ib;
+#pragma unroll
+      for (int i = 0; i < JB; ++i)
+        if (i < j) {
+          un.x = fma(-cf[j + i], q[i].x, un.x);
+          un.y = fma(-cf[j + i], q[i].y, un.y);
+        }
+      un.x = fma(-cj, qj.x, un.x);
+      un.y = fma(-cj, qj.y, un.y);
+      return make_double4(qj.x, qj.y, un.x, un.y);
+    };
+    for (int64_t e = tid; e < n2; e += stride) {
+      const double4 r = body(reinterpret_cast<const double2 *>(u)[e], reinterpret_cast<const double2 *>(wh)[e],
+                             [&](int i) { return __ldg(reinterpret_cast<const double2 *>(Q + int64_t(i) * ldq) + e); });
+      reinterpret_cast<double2 *>(u)[e] = make_double2(r.x, r.y);
+      reinterpret_cast<double2 *>(wh)[e] = make_double2(r.z, r.w);
+      s = fma(r.w, r.w, fma(r.z, r.z, s));
+    }
+    if ((n & 1) && tid == 0) {  // the odd last element
+      const double4 r = body(make_double2(u[n - 1], 0.0), make_double2(wh[n - 1], 0.0),
+                             [&](int i) { return make_double2(Q[int64_t(i) * ldq + n - 1], 0.0); });
+      u[n - 1] = r.x;
+      wh[n - 1] = r.z;
+      s = fma(r.z, r.z, s);
+    }
+  }
+  const double v[1] = {s};
+  grid_reduce_many<1>(v, 1, [](int o) { return o; }, part, ticket, nu1);
+}
+
+// Tentative column j = [s_j ; ||u_{j+1}||] -> rotation j, estimate |g_{j+1}|,
+// loop control as k_givens (stop on the estimate or on ||u_{j+1}|| = 0).
+__global__ void k_dcgs_givens(GmresDev st, int j, double rtol, int mm, cudaGraphConditionalHandle hw,
+                              cudaGraphConditionalHandle hs, int cond) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (*st.dead != 0.0) return;  // k_dcgs_coef ended the cycle
+  const int ld = st.m + 1;
+  const double hn = sqrt(*st.nu1);
+  st.Hraw[int64_t(j) * ld + j + 1] = hn;
+  st.hn[j] = hn;
+  st.gpre[j] = st.g[j];
+  dcgs_rotate(st, j);
+  const double b0 = *st.beta0;
+  st.out[0] = fabs(st.g[j + 1]) / b0;
+  const bool stop = fabs(st.g[j + 1]) <= rtol * b0 || hn == 0.0;
+  st.out[1] = stop ? 1.0 : 0.0;
+  st.out[2] = hn;
+  st.out[3] = double(j + 1);
+  st.out[4] = double(j + 1);
+  if (cond) {
+    cudaGraphSetConditional(hs, unsigned(j + 1));
+    cudaGraphSetConditional(hw, (!stop && j + 1 < mm) ? 1u : 0u);
+  }
+}
+
+// H(0:k,0:k) y = g(0:k), then R y2 = y (z_j = B u_j and U = Q R)
+__global__ void k_dcgs_backsolve(GmresDev st, int k, const double *kdev) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (kdev) k = int(*kdev);
+  const int ld = st.m + 1;
+  for (int i = k - 1; i >= 0; --i) {
+    double s = 0.0;
+    for (int l = i + 1; l < k; ++l) s += st.H[int64_t(l) * ld + i] * st.y[l];
+    st.y[i] = (st.g[i] - s) / st.H[int64_t(i) * ld + i];
+  }
+  for (int i = k - 1; i >= 0; --i) {
+    double s = 0.0;
+    for (int l = i + 1; l < k; ++l) s += st.R[int64_t(l) * st.m + i] * st.y2[l];
+    st.y2[i] = (st.y[i] - s) / st.R[int64_t(i) * st.m + i];
   }
 }
 

@@ -315,6 +315,8 @@ struct mg_ctx_s {
   // GMRES workspace
   int gm_m = 0;
   DevArray<double> gm_V, gm_Z, gm_state;
+  DevArray<double> dcgs_part;  // per-CTA partials of the DCGS2 multi-dot ([grid][2m+2])
+  DevArray<unsigned> dcgs_ticket;
   DevArray<double> rich_z, rich_r;  // mixed-precision MG iteration (defect correction)
   DevArray<double> mean_b;          // consistent copy of b (global constraint on the finest level)
   DevArray<double> upd_stage;       // mg_update_matrix: staging buffer for host values (kept across calls)
@@ -397,7 +399,7 @@ int64_t env_i64(const char *name, int64_t dflt) {
 }
 
 int ks_for_level(int64_t n_global) {
-  static const int64_t t4 = env_i64("MGB200_KS4_SLICES", 4096), t2 = env_i64("MGB200_KS2_SLICES", 32768),
+  static const int64_t t4 = env_i64("MGB200_KS4_SLICES", 4096), t2 = env_i64("MGB200_KS2_SLICES", 16384),
                        t8 = env_i64("MGB200_KS8_SLICES", 256);
   const int64_t slices = (n_global + 31) / 32;
   return slices < t8 ? 8 : slices < t4 ? 4 : slices < t2 ? 2 : 1;
@@ -750,6 +752,43 @@ mg_status dev_axpy_dot(mg_ctx_s *c, bool dist, int64_t n, double *a, const doubl
   launch_reduce<1>(c, u == nullptr && !dist, vec, n, a, u, v, h, res, rev);
   TRY(check_launch("axpy-dot"));
   return finish_reduce(c, dist, res, u == nullptr);
+}
+
+// --- DCGS2 passes (MG_GMRES_DCGS2): grid = resident CTAs of the bucket's kernel
+template <int JB>
+unsigned dcgs_grid(const mg_ctx_s *c, const void *k, int64_t n) {
+  int bl = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bl, k, mgk::kRedThreads, 0);
+  const int64_t want = (n / 2 + mgk::kRedThreads - 1) / mgk::kRedThreads;
+  return unsigned(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(std::max(1, std::min(bl, 4))) * c->n_sm)));
+}
+
+template <int JB>
+void dcgs_launch(mg_ctx_s *c, bool update, int64_t n, int j, double *Q, int64_t ldq) {
+  const mgk::GmresDev &g = c->gm;
+  if (!update) {
+    const unsigned gr = dcgs_grid<JB>(c, reinterpret_cast<const void *>(mgk::k_dcgs_dots<JB>), n);
+    ++g_tally, mgk::k_dcgs_dots<JB><<<gr, mgk::kRedThreads, 0, c->stream>>>(n, j, Q, ldq, c->dcgs_part.p,
+                                                                             c->dcgs_ticket.p, g.dots);
+  } else {
+    const unsigned gr = dcgs_grid<JB>(c, reinterpret_cast<const void *>(mgk::k_dcgs_update<JB>), n);
+    ++g_tally, mgk::k_dcgs_update<JB><<<gr, mgk::kRedThreads, 0, c->stream>>>(n, j, Q, ldq, g.coef, g.dead,
+                                                                               c->dcgs_part.p, c->dcgs_ticket.p, g.nu1);
+  }
+}
+
+// one DCGS2 pass of Arnoldi step j (bucketed on j so the j accumulators live in registers)
+mg_status dcgs_pass(mg_ctx_s *c, bool dist, bool update, int64_t n, int j, double *Q, int64_t ldq) {
+  if (j < 2) dcgs_launch<2>(c, update, n, j, Q, ldq);
+  else if (j < 4) dcgs_launch<4>(c, update, n, j, Q, ldq);
+  else if (j < 8) dcgs_launch<8>(c, update, n, j, Q, ldq);
+  else if (j < 16) dcgs_launch<16>(c, update, n, j, Q, ldq);
+  else if (j < 32) dcgs_launch<32>(c, update, n, j, Q, ldq);
+  else if (j < 64) dcgs_launch<64>(c, update, n, j, Q, ldq);
+  else return fail(MG_ERR_INVALID_ARG, "DCGS2: restart %d > 64", j);
+  TRY(check_launch(update ? "dcgs update" : "dcgs dots"));
+  if (dist) TRY(c->tr->allreduce_sum(update ? c->gm.nu1 : c->gm.dots, update ? 1 : 2 * j + 2, c->stream));
+  return MG_OK;
 }
 
 // --- dense coarse inverse on the device (in-place Gauss-Jordan, partial pivoting)
@@ -1559,10 +1598,16 @@ mg_status ensure_gmres(mg_ctx_s *c, int m) {
   c->clear_graphs();  // iteration graphs hold basis pointers
   TRY(c->gm_V.alloc(size_t(m + 1) * gm_stride(N)));
   TRY(c->gm_Z.alloc(size_t(m) * gm_stride(N)));
-  const size_t ns = size_t(m + 1) * m + 6 * size_t(m + 1) + 16;
+  const size_t ns = size_t(m + 1) * m + 6 * size_t(m + 1) + 16  // MGS state
+                    + size_t(m + 1) * m + size_t(m) * m + 6 * size_t(m + 1) + 8;  // DCGS2 state
   TRY(c->gm_state.alloc(ns));
   CU(cudaMemset(c->gm_state.p, 0, ns * sizeof(double)));
   if (!c->gm_host) CU(cudaMallocHost(&c->gm_host, 16 * sizeof(double)));
+  TRY(c->dcgs_part.alloc(size_t(4 * c->n_sm) * size_t(2 * m + 2)));
+  if (!c->dcgs_ticket.p) {
+    TRY(c->dcgs_ticket.alloc(1));
+    CU(cudaMemset(c->dcgs_ticket.p, 0, sizeof(unsigned)));
+  }
   double *p = c->gm_state.p;
   mgk::GmresDev &g = c->gm;
   g.m = m;
@@ -1582,7 +1627,23 @@ mg_status ensure_gmres(mg_ctx_s *c, int m) {
   p += 1;
   g.beta0 = p;
   p += 1;
-  g.out = p;
+  g.out = p;  // [6]
+  p += 14;
+  g.Hraw = p;
+  p += size_t(m + 1) * m;
+  g.R = p;
+  p += size_t(m) * m;
+  g.gpre = p;
+  p += m + 1;
+  g.dots = p;
+  p += 2 * (m + 1);
+  g.coef = p;
+  p += 2 * (m + 1);
+  g.y2 = p;
+  p += m + 1;
+  g.nu1 = p;
+  p += 1;
+  g.dead = p;
   c->gm_m = m;
   return MG_OK;
 }
@@ -2519,7 +2580,8 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
       rel = hst[0] / r0;
       if (hst[0] <= rtol * r0) conv = true;
     }
-  } else if (opts->method == MG_GMRES) {
+  } else if (opts->method == MG_GMRES || opts->method == MG_GMRES_DCGS2) {
+    const bool dcgs = opts->method == MG_GMRES_DCGS2;
     const int m = std::max(1, std::min(opts->restart > 0 ? opts->restart : 30, 64));
     TRY(ensure_gmres(c, m));
     mgk::GmresDev g = c->gm;
@@ -2537,8 +2599,12 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
     const unsigned eg = unsigned(std::min<int64_t>(std::max<int64_t>(1, (N + 255) / 256), 8 * c->n_sm));
     while (!conv && its < opts->max_iter) {
       const int mm = std::min(m, opts->max_iter - its);
-      ++g_tally, mgk::k_gmres_start<<<1, 32, 0, c->stream>>>(g);
-      ++g_tally, mgk::k_scale_div<<<eg, 256, 0, c->stream>>>(N, V, g.beta, V);
+      if (dcgs) {  // u_0 = r stays in slot 0; step 0 normalises it
+        ++g_tally, mgk::k_dcgs_start<<<1, 256, 0, c->stream>>>(g);
+      } else {
+        ++g_tally, mgk::k_gmres_start<<<1, 32, 0, c->stream>>>(g);
+        ++g_tally, mgk::k_scale_div<<<eg, 256, 0, c->stream>>>(N, V, g.beta, V);
+      }
       TRY(check_launch("gmres start"));
       int k = 0;
       bool happy = false;  // happy breakdown h_{j+1,j} = 0
@@ -2546,6 +2612,18 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
       // step runs inside the conditional-graph cycle and steers it itself
       auto step = [&](int j, bool cond, cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hs) -> mg_status {
         double *vj = V + size_t(j) * NS, *zj = Z + size_t(j) * NS, *w = V + size_t(j + 1) * NS;
+        if (dcgs) {  // delayed CGS2: one multi-dot pass, one update pass (reading Z29)
+          TRY(vcycle_rec(c, Lf, zj, vj, true));            // z_j = GMG(L, 0, u_j)
+          TRY(a_pass_spmv(c, Lf, 1.0, zj, 0.0, w, true));  // w^ = A z_j (slot j + 1)
+          TRY(dcgs_pass(c, dist, false, N, j, V, NS));     // a, bb, nu, mu
+          ++g_tally, mgk::k_dcgs_coef<<<1, 32, 0, c->stream>>>(g, j, mm, hw, cond ? 1 : 0);
+          TRY(check_launch("dcgs coef"));
+          TRY(dcgs_pass(c, dist, true, N, j, V, NS));      // q_j, u_{j+1}, ||u_{j+1}||^2
+          ++g_tally, mgk::k_dcgs_givens<<<1, 32, 0, c->stream>>>(g, j, rtol, mm, hw, hs, cond ? 1 : 0);
+          TRY(check_launch("dcgs givens"));
+          if (!cond) CU(cudaMemcpyAsync(hst, g.out, 6 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+          return MG_OK;
+        }
         TRY(vcycle_rec(c, Lf, zj, vj, true));      // z_j = GMG(L, 0, v_j)
         TRY(a_pass_spmv(c, Lf, 1.0, zj, 0.0, w, true));  // w = A z_j
         double *hcol = g.H + size_t(j) * ld;
@@ -2568,7 +2646,7 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
         // the whole restart cycle as ONE graph launch: while (continue) {
         // switch (j) { step j } }, steered by k_givens on the device; the host
         // reads (beta, k, stop flags) once per cycle instead of once per step
-        const auto key = std::make_tuple(mm, rtol, g.m);
+        const auto key = std::make_tuple(dcgs ? -mm : mm, rtol, g.m);
         auto it = c->cycle_graphs.find(key);
         if (it == c->cycle_graphs.end()) {
           CycleGraph cg;
@@ -2576,20 +2654,23 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
           it = c->cycle_graphs.emplace(key, std::move(cg)).first;
         }
         CU(cudaGraphLaunch(it->second.exec, c->stream));
-        CU(cudaMemcpyAsync(hst + 4, g.out, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaMemcpyAsync(hst + 8, g.out, 6 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         kdev = g.out + 3;
-        ++g_tally, mgk::k_backsolve<<<1, 32, 0, c->stream>>>(g, 0, kdev);
-        ++g_tally, mgk::k_update_x<<<eg, 256, 0, c->stream>>>(N, 0, g.y, Z, NS, x, kdev);
+        if (dcgs) ++g_tally, mgk::k_dcgs_backsolve<<<1, 32, 0, c->stream>>>(g, 0, kdev);
+        else ++g_tally, mgk::k_backsolve<<<1, 32, 0, c->stream>>>(g, 0, kdev);
+        ++g_tally, mgk::k_update_x<<<eg, 256, 0, c->stream>>>(N, 0, dcgs ? g.y2 : g.y, Z, NS, x, kdev);
         TRY(check_launch("gmres update"));
         TRY(a_pass_resid(c, Lf, x, b, V, true));
         TRY(dev_dot(c, dist, N, V, V, g.beta, true));
         CU(cudaMemcpyAsync(hst, g.beta, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         CU(cudaStreamSynchronize(c->stream));
-        k = int(hst[4 + 3]);
-        if (k < 1 || k > mm) return fail(MG_ERR_STATE, "GMRES cycle graph ran %d steps (expected 1..%d)", k, mm);
-        for (int j = 0; j < k; ++j) g_tally += it->second.kernels[size_t(j)];
-        its += k;
-        happy = hst[4 + 1] != 0.0 && hst[4 + 2] == 0.0;
+        k = int(hst[8 + 3]);
+        const int ran = dcgs ? int(hst[8 + 4]) : k;  // steps run (a DCGS2 breakdown step has no column)
+        if (ran < 1 || ran > mm || k < 0 || k > ran)
+          return fail(MG_ERR_STATE, "GMRES cycle graph ran %d steps (expected 1..%d)", ran, mm);
+        for (int j = 0; j < ran; ++j) g_tally += it->second.kernels[size_t(j)];
+        its += ran;
+        happy = hst[8 + 1] != 0.0 && hst[8 + 2] == 0.0;
       } else {
         for (int j = 0; j < mm; ++j) {
           auto step_j = [&]() { return step(j, false, 0, 0); };
@@ -2607,7 +2688,7 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
           }
           ++its;
           CU(cudaStreamSynchronize(c->stream));
-          k = j + 1;
+          k = dcgs ? int(hst[3]) : j + 1;
           if (!std::isfinite(hst[0])) return fail(MG_ERR_NONFINITE, "non-finite GMRES residual estimate");
           if (hst[1] != 0.0) {  // estimate |g_{j+1}| <= rtol beta_0, or breakdown: end of the cycle
             happy = hst[2] == 0.0;
@@ -2616,8 +2697,9 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
         }
       }
       if (!kdev) {
-        ++g_tally, mgk::k_backsolve<<<1, 32, 0, c->stream>>>(g, k, nullptr);
-        ++g_tally, mgk::k_update_x<<<eg, 256, 0, c->stream>>>(N, k, g.y, Z, NS, x, nullptr);
+        if (dcgs) ++g_tally, mgk::k_dcgs_backsolve<<<1, 32, 0, c->stream>>>(g, k, nullptr);
+        else ++g_tally, mgk::k_backsolve<<<1, 32, 0, c->stream>>>(g, k, nullptr);
+        ++g_tally, mgk::k_update_x<<<eg, 256, 0, c->stream>>>(N, k, dcgs ? g.y2 : g.y, Z, NS, x, nullptr);
         TRY(check_launch("gmres update"));
         TRY(a_pass_resid(c, Lf, x, b, V, true));
         TRY(dev_dot(c, dist, N, V, V, g.beta, true));
