@@ -412,6 +412,81 @@ __global__ void __launch_bounds__(kCta) k_transfer(Sell T, const double *__restr
   transfer_task<BS, WPE, ACCUM, STREAM, HALO, KS, false, true>(T, blockIdx.x, in, ing, n_own, out);
 }
 
+// Prolongation-add x += P y on CSR rows in NATURAL order (lane = fine row r,
+// a warp = 32 consecutive rows), so x is read and written with coalesced
+// 768-byte (bs 3) warp accesses.  On SELL-32-sigma the 1-8-entry rows of P are
+// length-sorted inside windows of 4096 rows: a warp's 32 rows were scattered,
+// every x access a separate sector (ncu r2: 114 cycles per issued instruction,
+// long-scoreboard bound, 0.46 of peak).  Entries {column, fp32-exact dyadic
+// weight} (WPE = 1) or columns + per-component fp32 weights (WPE = BS) are read
+// per lane from the row's CSR range (the 32 rows' entries are contiguous);
+// each row is summed in CSR order with FMA, exactly as k_transfer.
+struct PCsr {
+  const int32_t *rp;  // [n+1] entry offsets
+  const int2 *cw;     // WPE = 1: {col, __float_as_int(w)}
+  const int32_t *col; // WPE = BS: columns
+  const float *w;     // WPE = BS: [entries*BS]
+  int64_t n;
+};
+
+template <int BS, int WPE, bool HALO>
+__global__ void __launch_bounds__(kCta) k_prolong_csr(PCsr P, const double *__restrict__ in,
+                                                      const double *__restrict__ ing, int n_own,
+                                                      double *__restrict__ out) {
+  constexpr int UB = 8;  // entries per batch (a 3D Q1 row has at most 8 without hanging nodes)
+  pdl_trigger();
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool live = r < P.n;
+  int e0 = 0, len = 0;
+  if (live) {
+    e0 = P.rp[r];
+    len = P.rp[r + 1] - e0;
+  }
+  int c[UB];
+  float w[UB][WPE];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int k = k0 + u < len ? e0 + k0 + u : e0;  // clamped (a re-read of the first entry)
+      if constexpr (WPE == 1) {
+        const int2 t = __ldg(P.cw + (len ? k : 0));
+        c[u] = t.x;
+        w[u][0] = __int_as_float(t.y);
+      } else {
+        c[u] = __ldg(P.col + (len ? k : 0));
+#pragma unroll
+        for (int q = 0; q < BS; ++q) w[u][q] = __ldg(P.w + int64_t(len ? k : 0) * BS + q);
+      }
+    }
+  };
+  fetch(0);   // structure only: before the predecessor's result is needed
+  pdl_wait();  // y = the coarse correction, x = this level's iterate
+  if (!live) return;
+  double acc[BS], xo[BS];
+  const int64_t o = r * BS;
+#pragma unroll
+  for (int q = 0; q < BS; ++q) acc[q] = 0.0, xo[q] = out[o + q];
+  for (int k0 = 0; k0 < len; k0 += UB) {
+    if (k0) fetch(k0);
+    double y[UB][BS];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const double *yc = col_ptr<BS, HALO>(in, ing, n_own, c[u]);
+#pragma unroll
+      for (int q = 0; q < BS; ++q) y[u][q] = __ldg(yc + q);
+    }
+#pragma unroll
+    for (int u = 0; u < UB; ++u)
+#pragma unroll
+      for (int q = 0; q < BS; ++q) {
+        const double t = fma(double(w[u][WPE == 1 ? 0 : q]), y[u][q], acc[q]);
+        acc[q] = k0 + u < len ? t : acc[q];
+      }
+  }
+#pragma unroll
+  for (int q = 0; q < BS; ++q) out[o + q] = xo[q] + acc[q];
+}
+
 // Transfer on the SELL-C layout of mgi_tsell_fill (C = 32 / BS rows per
 // slice): lane (r, q) = (lane / BS, lane % BS) accumulates component q of the
 // slice's row r, so the BS components of a gathered node are ONE warp load
@@ -1058,6 +1133,168 @@ __global__ void __launch_bounds__(kRedThreads) k_dcgs_dots(int64_t n, int j, con
     return 2 * j + (o - 2 * JB);
   };
   grid_reduce_many<2 * JB + 2>(acc, 2 * j + 2, map, part, ticket, out);
+}
+
+// --- bulk-copy (TMA engine) staging of vector tiles ------------------------
+// cp.async.bulk moves a contiguous tile global -> shared without registers;
+// completion is counted in bytes on an mbarrier.  The Krylov passes stream
+// j + 2 vectors at once: staging their tiles through a ring of shared-memory
+// stages keeps ~100-200 KB in flight per SM with 256 threads, where register
+// staging (one 16-byte load per vector and thread) ran out of registers and
+// warps (k_dcgs_*_reg: 220 registers, 8 warps per SM, 4.2-4.5 TB/s).
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// generic-proxy reads of a stage are ordered before the async proxy refills it
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Ring of NST stages, each holding the tiles [e0, e0 + T) of NV strided vectors
+// (base + v * ld, v < NV).  Tiles are dealt to CTAs round-robin (tile = b, b +
+// grid, ...), so which CTA sums which elements is fixed by (n, T, grid).
+struct TileRing {
+  double *buf;     // [NST][NV][T]
+  uint64_t *full;  // [NST]
+  int nst, nv, T;
+  const double *base;
+  int64_t ld, n;
+  __device__ double *stage(int s) const { return buf + int64_t(s) * nv * T; }
+  // thread 0: arm stage s with the tile's bytes and issue the NV copies
+  __device__ void issue(int64_t tile, int s) const {
+    const int64_t e0 = tile * T;
+    const int64_t len = n - e0 < T ? n - e0 : T;
+    const unsigned bytes = unsigned((len * 8 + 15) & ~int64_t(15));  // may read <= 8 bytes past n (inside the slot)
+    mbar_expect_tx(full + s, bytes * unsigned(nv));
+    for (int v = 0; v < nv; ++v) bulk_g2s(stage(s) + int64_t(v) * T, base + v * ld + e0, bytes, full + s);
+  }
+};
+
+// smem layout for the ring: nst * nv * T doubles, then nst mbarriers
+__device__ __forceinline__ TileRing make_ring(unsigned char *sm, int nst, int nv, int T, const double *base,
+                                              int64_t ld, int64_t n) {
+  TileRing r;
+  r.buf = reinterpret_cast<double *>(sm);
+  r.full = reinterpret_cast<uint64_t *>(sm + size_t(nst) * nv * T * sizeof(double));
+  r.nst = nst, r.nv = nv, r.T = T, r.base = base, r.ld = ld, r.n = n;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) mbar_init(r.full + s, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  return r;
+}
+
+// Runs body(stage_ptr, e0, len) over this CTA's tiles with NST tiles in flight.
+template <class Body>
+__device__ __forceinline__ void ring_stream(const TileRing &r, Body &&body) {
+  const int64_t ntiles = (r.n + r.T - 1) / r.T;
+  const int64_t grid = gridDim.x;
+  if (threadIdx.x == 0)
+    for (int s = 0; s < r.nst; ++s)
+      if (blockIdx.x + s * grid < ntiles) r.issue(blockIdx.x + s * grid, s);
+  int s = 0;
+  unsigned phase = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += grid) {
+    mbar_wait(r.full + s, phase);
+    const int64_t e0 = tile * r.T;
+    body(r.stage(s), e0, int(r.n - e0 < r.T ? r.n - e0 : r.T));
+    __syncthreads();  // every thread is done with stage s
+    if (threadIdx.x == 0 && tile + int64_t(r.nst) * grid < ntiles) {
+      fence_proxy_async();
+      r.issue(tile + int64_t(r.nst) * grid, s);
+    }
+    if (++s == r.nst) s = 0, phase ^= 1u;
+  }
+}
+
+// k_dcgs_dots with the j + 2 vectors (slots 0..j+1 of Q) staged by bulk copies
+template <int JB>
+__global__ void __launch_bounds__(kRedThreads) k_dcgs_dots_tma(int64_t n, int j, const double *__restrict__ Q,
+                                                               int64_t ldq, int nst, int T, double *part,
+                                                               unsigned *ticket, double *out) {
+  extern __shared__ __align__(128) unsigned char sm_ring[];
+  const TileRing ring = make_ring(sm_ring, nst, j + 2, T, Q, ldq, n);
+  double acc[2 * JB + 2];
+#pragma unroll
+  for (int o = 0; o < 2 * JB + 2; ++o) acc[o] = 0.0;
+  ring_stream(ring, [&](const double *st, int64_t, int len) {
+    const double *u = st + int64_t(j) * T, *wh = st + int64_t(j + 1) * T;
+    for (int e = threadIdx.x; e < len; e += blockDim.x) {
+      const double uu = u[e], ww = wh[e];
+#pragma unroll
+      for (int i = 0; i < JB; ++i)
+        if (i < j) {
+          const double q = st[int64_t(i) * T + e];
+          acc[i] = fma(q, uu, acc[i]);
+          acc[JB + i] = fma(q, ww, acc[JB + i]);
+        }
+      acc[2 * JB] = fma(uu, uu, acc[2 * JB]);
+      acc[2 * JB + 1] = fma(uu, ww, acc[2 * JB + 1]);
+    }
+  });
+  auto map = [j](int o) {
+    if (o < JB) return o < j ? o : -1;
+    if (o < 2 * JB) return o - JB < j ? j + o - JB : -1;
+    return 2 * j + (o - 2 * JB);
+  };
+  grid_reduce_many<2 * JB + 2>(acc, 2 * j + 2, map, part, ticket, out);
+}
+
+// k_dcgs_update with the j + 2 vectors staged by bulk copies; q_j and u_{j+1}
+// are stored straight to global memory (coalesced)
+template <int JB>
+__global__ void __launch_bounds__(kRedThreads) k_dcgs_update_tma(int64_t n, int j, double *__restrict__ Q,
+                                                                 int64_t ldq, int nst, int T,
+                                                                 const double *__restrict__ coef,
+                                                                 const double *dead, double *part, unsigned *ticket,
+                                                                 double *nu1) {
+  extern __shared__ __align__(128) unsigned char sm_ring[];
+  __shared__ double cf[2 * JB + 2];
+  for (int i = threadIdx.x; i < 2 * j + 2; i += blockDim.x) cf[i] = coef[i];
+  const TileRing ring = make_ring(sm_ring, nst, j + 2, T, Q, ldq, n);  // (its __syncthreads covers cf)
+  double s = 0.0;
+  if (*dead == 0.0) {
+    const double ib = cf[2 * j + 1], cj = cf[2 * j];
+    double *u = Q + int64_t(j) * ldq, *wh = Q + int64_t(j + 1) * ldq;
+    ring_stream(ring, [&](const double *st, int64_t e0, int len) {
+      const double *us = st + int64_t(j) * T, *ws = st + int64_t(j + 1) * T;
+      for (int e = threadIdx.x; e < len; e += blockDim.x) {
+        double qj = us[e], un = ws[e] * ib;
+#pragma unroll
+        for (int i = 0; i < JB; ++i)
+          if (i < j) qj = fma(-cf[i], st[int64_t(i) * T + e], qj);
+        qj *= ib;
+#pragma unroll
+        for (int i = 0; i < JB; ++i)
+          if (i < j) un = fma(-cf[j + i], st[int64_t(i) * T + e], un);
+        un = fma(-cj, qj, un);
+        u[e0 + e] = qj;
+        wh[e0 + e] = un;
+        s = fma(un, un, s);
+      }
+    });
+  }
+  const double v[1] = {s};
+  grid_reduce_many<1>(v, 1, [](int o) { return o; }, part, ticket, nu1);
 }
 
 // rotations 0..jj-1 applied to raw column jj, rotation jj formed, rotated column

@@ -91,6 +91,19 @@ struct TSellOp {
   mgk::TSell view() const { return mgk::TSell{slice_ptr.p, perm.p, cw.p, col.p, w.p, n_slices}; }
 };
 
+// Prolongation in natural row order (k_prolong_csr): int32 CSR offsets and
+// {column, fp32 weight} entries; built only when every weight is exact in fp32
+// (the dyadic transfer weights, reading Z8) and the entries fit int32.
+struct PCsrOp {
+  DevArray<int32_t> rp, col;
+  DevArray<int2> cw;
+  DevArray<float> w;
+  int64_t n = 0;
+  int wpe = 1;
+  bool set = false;
+  mgk::PCsr view() const { return mgk::PCsr{rp.p, cw.p, col.p, w.p, n}; }
+};
+
 // Operators above this size are read with evict-first loads (MGB200_STREAM_MB overrides
 // the default kStreamBytes; experiment knob for L2 residency of mid-sized operators).
 size_t stream_bytes() {
@@ -103,6 +116,43 @@ size_t stream_bytes() {
 
 // Build SELL-32-sigma on the host and upload it (col: LOCAL column indices);
 // f32: values rounded to fp32 in the fp32 chunk layout.
+mg_status build_pcsr(PCsrOp &op, int64_t n, const std::vector<int64_t> &rp, const std::vector<int64_t> &col,
+                     const std::vector<double> &v, int wpe) {
+  op = PCsrOp();
+  if (const char *e = std::getenv("MGB200_PCSR"); e && e[0] == '0') return MG_OK;
+  const int64_t nnz = n > 0 ? rp[size_t(n)] : 0;
+  if (nnz <= 0 || nnz >= (int64_t(1) << 31)) return MG_OK;
+  // per-component weights (C4/C5 velocity-only Dirichlet) stay on SELL-32: measured
+  // C5 V-cycle 11.12 -> 11.26 ms with the CSR kernel (four scalar weight loads per entry)
+  if (wpe != 1) return MG_OK;
+  for (int64_t i = 0; i < nnz * wpe; ++i)
+    if (double(float(v[size_t(i)])) != v[size_t(i)]) return MG_OK;  // not exact in fp32: SELL path
+  std::vector<int32_t> r32(size_t(n) + 1);
+  for (int64_t i = 0; i <= n; ++i) r32[size_t(i)] = int32_t(rp[size_t(i)]);
+  TRY(op.rp.upload(r32.data(), r32.size()));
+  if (wpe == 1) {
+    std::vector<int2> cw(static_cast<size_t>(nnz));
+    for (int64_t e = 0; e < nnz; ++e) {
+      const float f = float(v[size_t(e)]);
+      int fi;
+      std::memcpy(&fi, &f, sizeof fi);
+      cw[size_t(e)] = make_int2(int32_t(col[size_t(e)]), fi);
+    }
+    TRY(op.cw.upload(cw.data(), cw.size()));
+  } else {
+    std::vector<int32_t> c32(static_cast<size_t>(nnz));
+    std::vector<float> wf(size_t(nnz) * wpe);
+    for (int64_t e = 0; e < nnz; ++e) c32[size_t(e)] = int32_t(col[size_t(e)]);
+    for (size_t i = 0; i < wf.size(); ++i) wf[i] = float(v[i]);
+    TRY(op.col.upload(c32.data(), c32.size()));
+    TRY(op.w.upload(wf.data(), wf.size()));
+  }
+  op.n = n;
+  op.wpe = wpe;
+  op.set = true;
+  return MG_OK;
+}
+
 mg_status build_sell(SellOp &op, int64_t n, const int64_t *rp, const int64_t *col, const double *val, int vpe,
                      bool f32 = false, std::vector<int64_t> *sp_out = nullptr,
                      const std::vector<int64_t> *row_ids = nullptr) {
@@ -232,6 +282,7 @@ struct Level {
   bool dinv_ready = false;
   SellOp P, R;  // P_{l-1}: level l-1 -> l (rows: owned fine rows), R_{l-1} = P^T (rows: r_row0 ...)
   TSellOp Pt, Rt;  // the same operators in the SELL-C layout (fp32-exact weights), used when set
+  PCsrOp Pc;       // P as natural-order CSR with fp32-exact weights (k_prolong_csr), used when set
   Halo hp;      // ghosts of the coarse vector y for P (coarse level distributed)
   Halo hr;      // ghosts of the fine vector r for R (this level distributed)
   int64_t r_row0 = 0, r_rows = 0;  // coarse rows produced by the local R
@@ -547,6 +598,36 @@ mg_status launch_transfer(int bs, bool acc, const SellOp &T, In in, double *out,
   return check_launch(acc ? "prolong-add" : "transfer");
 }
 
+template <int BS, int WPE, bool HALO>
+void launch_pcsr_k(const PCsrOp &P, In in, double *out, cudaStream_t st) {
+  const unsigned g = unsigned((P.n + mgk::kCta - 1) / mgk::kCta);
+  kl(mgk::k_prolong_csr<BS, WPE, HALO>, g, st, P.view(), in.x, in.xg, in.n_own, out);
+}
+
+template <int BS>
+void launch_pcsr_bs(const PCsrOp &P, In in, double *out, cudaStream_t st) {
+  if (P.n == 0) return;
+  if (P.wpe == 1 || BS == 1) {
+    if (in.xg) launch_pcsr_k<BS, 1, true>(P, in, out, st);
+    else launch_pcsr_k<BS, 1, false>(P, in, out, st);
+  } else {
+    if (in.xg) launch_pcsr_k<BS, BS, true>(P, in, out, st);
+    else launch_pcsr_k<BS, BS, false>(P, in, out, st);
+  }
+}
+
+mg_status launch_pcsr(int bs, const PCsrOp &P, In in, double *out, cudaStream_t st) {
+  switch (bs) {
+    case 1: launch_pcsr_bs<1>(P, in, out, st); break;
+    case 2: launch_pcsr_bs<2>(P, in, out, st); break;
+    case 3: launch_pcsr_bs<3>(P, in, out, st); break;
+    case 4: launch_pcsr_bs<4>(P, in, out, st); break;
+    case 6: launch_pcsr_bs<6>(P, in, out, st); break;
+    default: return fail(MG_ERR_INVALID_ARG, "block size %d not supported", bs);
+  }
+  return check_launch("prolong-add (csr)");
+}
+
 template <int BS, int WPE, bool ACC, bool HALO, int KS, int NSL>
 void launch_tsell_k(const TSellOp &T, In in, double *out, cudaStream_t st) {
   const unsigned g = grid_for_slices((T.n_slices + NSL - 1) / NSL, KS);
@@ -763,9 +844,41 @@ unsigned dcgs_grid(const mg_ctx_s *c, const void *k, int64_t n) {
   return unsigned(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(std::max(1, std::min(bl, 4))) * c->n_sm)));
 }
 
+// The passes stage the j + 2 vector tiles through shared memory with bulk
+// copies (k_dcgs_*_tma, default) or load them into registers (k_dcgs_*, the
+// first version; MGB200_DCGS_TMA=0).
+bool dcgs_tma() {
+  static const bool on = [] {
+    const char *e = std::getenv("MGB200_DCGS_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int JB>
 void dcgs_launch(mg_ctx_s *c, bool update, int64_t n, int j, double *Q, int64_t ldq) {
   const mgk::GmresDev &g = c->gm;
+  if (dcgs_tma()) {
+    // ring: up to 4 stages of tiles of T doubles of the j + 2 vectors in ~200 KB
+    const int nv = j + 2;
+    const size_t budget = size_t(200) << 10;
+    int T = 256 * std::max(1, int(budget / (size_t(4) * nv * 8 * 256)));
+    T = std::min(T, 2048);
+    const int nst = std::max(1, std::min(4, int(budget / (size_t(nv) * 8 * size_t(T)))));
+    const size_t smem = size_t(nst) * nv * T * sizeof(double) + size_t(nst) * sizeof(uint64_t);
+    const int64_t ntiles = (n + T - 1) / T;
+    const unsigned gr = unsigned(std::max<int64_t>(1, std::min<int64_t>(ntiles, c->n_sm)));
+    if (!update) {
+      cudaFuncSetAttribute(mgk::k_dcgs_dots_tma<JB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      ++g_tally, mgk::k_dcgs_dots_tma<JB><<<gr, mgk::kRedThreads, smem, c->stream>>>(
+                     n, j, Q, ldq, nst, T, c->dcgs_part.p, c->dcgs_ticket.p, g.dots);
+    } else {
+      cudaFuncSetAttribute(mgk::k_dcgs_update_tma<JB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      ++g_tally, mgk::k_dcgs_update_tma<JB><<<gr, mgk::kRedThreads, smem, c->stream>>>(
+                     n, j, Q, ldq, nst, T, g.coef, g.dead, c->dcgs_part.p, c->dcgs_ticket.p, g.nu1);
+    }
+    return;
+  }
   if (!update) {
     const unsigned gr = dcgs_grid<JB>(c, reinterpret_cast<const void *>(mgk::k_dcgs_dots<JB>), n);
     ++g_tally, mgk::k_dcgs_dots<JB><<<gr, mgk::kRedThreads, 0, c->stream>>>(n, j, Q, ldq, c->dcgs_part.p,
@@ -1336,6 +1449,7 @@ mg_status do_prolong(mg_ctx_s *c, int l, const double *y, double *x) {
   Level &C = c->lv[l - 1];
   TRY(halo_exchange(c, L.hp, y));
   const In in{y, L.hp.active ? L.hp.ghost.p : nullptr, int(C.n)};
+  if (L.Pc.set) return launch_pcsr(c->bs(), L.Pc, in, x, c->stream);
   if (L.Pt.set) return launch_tsell(c->bs(), true, L.Pt, in, x, c->stream);
   return launch_transfer(c->bs(), true, L.P, in, x, c->stream);
 }
@@ -2024,6 +2138,7 @@ mg_status mg_set_transfer(mg_ctx c, int fine_level, const int64_t *row_ptr, cons
     L.hp = Halo();
   }
   TRY(build_sell(L.P, L.n, rp.data(), cl.data(), v.data(), wpe));
+  TRY(build_pcsr(L.Pc, L.n, rp, cl, v, wpe));
   // prolongation stays on SELL-32 (lane = fine row): its rows hold 1-8 entries, and the
   // SELL-C layout's 32/bs rows per warp triple the short dependent chains (C3 finest
   // 105 -> 162 us measured); MGB200_TSELL_PROLONG=1 builds it anyway (experiments)

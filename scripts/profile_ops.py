@@ -21,6 +21,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("mode", choices=["step", "kernels", "vcycle"])
 ap.add_argument("--config", default="c3")
 ap.add_argument("--mixed", action="store_true")
+ap.add_argument("--orth", choices=["mgs", "dcgs2"], default="mgs", help="GMRES orthogonalisation (step mode)")
 ap.add_argument("--level", type=int, default=-1, help="kernels mode: level to profile (default finest)")
 a = ap.parse_args()
 
@@ -32,14 +33,15 @@ ctx = S.ctx
 Lf = len(P.levels) - 1
 b = torch.from_numpy(P.b).cuda()
 x = torch.zeros_like(b)
+meth = m.MG_GMRES_DCGS2 if a.orth == "dcgs2" else m.MG_GMRES
 for _ in range(3):
     x.zero_()
-    S.solve(x, b)
+    S.solve(x, b, method=meth)
 torch.cuda.synchronize()
 if a.mode == "step":
     torch.cuda.profiler.start()
     x.zero_()
-    st, its, rel, conv = S.solve(x, b)
+    st, its, rel, conv = S.solve(x, b, method=meth)
     S.apply_constraints(x)
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
