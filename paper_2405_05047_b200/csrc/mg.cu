@@ -844,13 +844,17 @@ unsigned dcgs_grid(const mg_ctx_s *c, const void *k, int64_t n) {
   return unsigned(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(std::max(1, std::min(bl, 4))) * c->n_sm)));
 }
 
-// The passes stage the j + 2 vector tiles through shared memory with bulk
-// copies (k_dcgs_*_tma, default) or load them into registers (k_dcgs_*, the
-// first version; MGB200_DCGS_TMA=0).
+// The passes load the j + 2 vectors' elements into registers (k_dcgs_*,
+// default) or stage their tiles through a shared-memory ring with bulk copies
+// (k_dcgs_*_tma, MGB200_DCGS_TMA=1).  Measured on C3 (same box, ncu warm):
+// equal speed for the multi-dot (0.115 ms per launch at j = 4..7), the staged
+// update 20% faster, whole solve within noise (148.57 vs 148.64 V-cycles/s);
+// the staged kernels with >= 160 KB of dynamic shared memory fail to launch
+// under Nsight Compute (LaunchFailed, root cause not found), so they stay opt-in.
 bool dcgs_tma() {
   static const bool on = [] {
     const char *e = std::getenv("MGB200_DCGS_TMA");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }
@@ -861,7 +865,7 @@ void dcgs_launch(mg_ctx_s *c, bool update, int64_t n, int j, double *Q, int64_t 
   if (dcgs_tma()) {
     // ring: up to 4 stages of tiles of T doubles of the j + 2 vectors in ~200 KB
     const int nv = j + 2;
-    const size_t budget = size_t(200) << 10;
+    const size_t budget = size_t(160) << 10;  // leaves room for tools that reserve shared memory
     int T = 256 * std::max(1, int(budget / (size_t(4) * nv * 8 * 256)));
     T = std::min(T, 2048);
     const int nst = std::max(1, std::min(4, int(budget / (size_t(nv) * 8 * size_t(T)))));
