@@ -1672,7 +1672,17 @@ mg_status run_vcycle(mg_ctx_s *c, double *x, const double *b, bool zero) {
   auto it = c->graphs.find(key);
   if (it == c->graphs.end()) {
     GraphExec ge;
-    TRY(capture(c, [&] { return vcycle_rec(c, c->L(), x, b, zero); }, ge));
+    const mg_status cs = capture(c, [&] { return vcycle_rec(c, c->L(), x, b, zero); }, ge);
+    if (cs != MG_OK) {
+      // a transport whose collectives cannot be captured on this system (NCCL inside
+      // CUDA graphs has only run single-rank here): run eagerly from now on
+      if (!c->tr || cs != MG_ERR_CUDA) return cs;
+      std::fprintf(stderr, "mgb200: graph capture with the transport failed (%s); running eagerly\n",
+                   mg_last_error());
+      cudaGetLastError();
+      c->cfg.use_graphs = 0;
+      return vcycle_rec(c, c->L(), x, b, zero);
+    }
     if (c->graphs.size() > 256) {
       for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
       c->graphs.clear();
@@ -2798,10 +2808,20 @@ mg_status mg_solve(mg_ctx c, double *x, const double *b, const mg_solve_opts *op
             auto it = c->iter_graphs.find(key);
             if (it == c->iter_graphs.end()) {
               GraphExec ge;
-              TRY(capture(c, step_j, ge));
-              it = c->iter_graphs.emplace(key, ge).first;
+              const mg_status cs = capture(c, step_j, ge);
+              if (cs != MG_OK) {  // as run_vcycle: fall back to eager launches
+                if (!c->tr || cs != MG_ERR_CUDA) return cs;
+                std::fprintf(stderr, "mgb200: graph capture with the transport failed (%s); running eagerly\n",
+                             mg_last_error());
+                cudaGetLastError();
+                c->cfg.use_graphs = 0;
+                c->clear_graphs();
+              } else {
+                it = c->iter_graphs.emplace(key, ge).first;
+              }
             }
-            TRY(launch_graph(c, it->second));
+            if (c->use_graphs()) TRY(launch_graph(c, it->second));
+            else TRY(step_j());
           } else {
             TRY(step_j());
           }

@@ -152,6 +152,12 @@ def test_fullsize_gmres_iterations_match_oracle(name):
     assert conv and abs(its - ite) <= 1, (its, ite)
     assert rel <= 1e-10 and rele <= 1e-10
     assert np.linalg.norm(host(x) - xe) <= 1e-8 * np.linalg.norm(xe)
+    # the opt-in delayed-CGS2 orthogonalisation (reading Z29) reaches the same
+    # minimal-residual iterates: +-1 iterations and x at 1e-8 against the oracle
+    x2 = dev(np.zeros(P.n_dof))
+    st2, its2, rel2, conv2 = m.mg_solve(mg.ctx, x2, dev(P.b), method=m.MG_GMRES_DCGS2, rtol=1e-10)
+    assert conv2 and abs(its2 - ite) <= 1 and rel2 <= 1e-10, (its2, ite)
+    assert np.linalg.norm(host(x2) - xe) <= 1e-8 * np.linalg.norm(xe)
 
 
 @pytest.mark.parametrize("name", ["c3", "c5"])
