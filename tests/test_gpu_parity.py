@@ -159,6 +159,8 @@ def test_vcycle_matches_oracle(name, graphs):
     m.mg_vcycle(mg.ctx, x, bd)
     exp = oracle.vcycle(h, Lf, x0.copy(), b)
     assert np.linalg.norm(host(x) - exp) <= TOL_VCYCLE * np.linalg.norm(exp)
+    # element-wise as well (every entry, scaled by the largest; the full-size criterion)
+    assert np.max(np.abs(host(x) - exp)) <= TOL_VCYCLE * np.max(np.abs(exp))
     # second cycle (graph replay) continues to match
     m.mg_vcycle(mg.ctx, x, bd)
     exp = oracle.vcycle(h, Lf, exp, b)
@@ -168,6 +170,7 @@ def test_vcycle_matches_oracle(name, graphs):
     m.mg_vcycle_zero(mg.ctx, z, bd)
     exp = oracle.vcycle(h, Lf, np.zeros_like(b), b)
     assert np.linalg.norm(host(z) - exp) <= TOL_VCYCLE * np.linalg.norm(exp)
+    assert np.max(np.abs(host(z) - exp)) <= TOL_VCYCLE * np.max(np.abs(exp))
 
 
 def test_vcycle_graph_and_eager_bitidentical():
