@@ -1137,6 +1137,219 @@ __global__ void __launch_bounds__(kRedThreads) k_dcgs_dots(int64_t n, int j, con
   grid_reduce_many<2 * JB + 2>(acc, 2 * j + 2, map, part, ticket, out);
 }
 
+// --- warp-split DCGS2 passes (default) -------------------------------------
+// Warp w of a CTA owns the basis vectors i = w, w + 8, ... (< j): VPW = ceil(j/8)
+// of them, so a thread holds 2 VPW accumulators and (2 + VPW) x U 16-byte loads
+// in flight instead of 2j + 2 accumulators (the per-thread version needed 220
+// registers at j = 16: one CTA per SM, 4.2-4.6 TB/s).  A CTA walks tiles of
+// 32 x U double2; every warp of the CTA walks every tile of the CTA for its own
+// vectors (u and w^ are re-read by the 8 warps from L1/L2, DRAM once).
+constexpr int kDcgsU = 4;
+
+// out = [a (j) | bb (j) | nu | mu]; the last warp also sums nu and mu
+template <int VPW>
+__global__ void __launch_bounds__(kRedThreads) k_dcgs_dots_ws(int64_t n, int j, const double *__restrict__ Q,
+                                                              int64_t ldq, double *part, unsigned *ticket,
+                                                              double *out) {
+  constexpr int U = kDcgsU;
+  __shared__ double sh[2 * 8 * VPW + 2];
+  __shared__ bool last;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nout = 2 * j + 2;
+  const double2 *u2 = reinterpret_cast<const double2 *>(Q + int64_t(j) * ldq);
+  const double2 *w2 = reinterpret_cast<const double2 *>(Q + int64_t(j + 1) * ldq);
+  const bool nm = w == kWarpsPerCta - 1;  // this warp also sums nu, mu
+  double aa[VPW], ab[VPW], nu = 0.0, mu = 0.0;
+#pragma unroll
+  for (int k = 0; k < VPW; ++k) aa[k] = ab[k] = 0.0;
+  const int64_t n2 = n / 2, ntiles = (n2 + 32 * U - 1) / (32 * U);
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t e0 = t * 32 * U + lane;
+    double2 uu[U], ww[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int64_t e = e0 + 32 * q;
+      uu[q] = e < n2 ? __ldg(u2 + e) : make_double2(0.0, 0.0);
+      ww[q] = e < n2 ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+    }
+    double2 qv[VPW][U];
+#pragma unroll
+    for (int k = 0; k < VPW; ++k) {
+      const int i = w + 8 * k;
+      if (i < j) {
+        const double2 *q2 = reinterpret_cast<const double2 *>(Q + int64_t(i) * ldq);
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int64_t e = e0 + 32 * q;
+          qv[k][q] = e < n2 ? __ldg(q2 + e) : make_double2(0.0, 0.0);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < VPW; ++k)
+      if (w + 8 * k < j)
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          aa[k] = fma(qv[k][q].y, uu[q].y, fma(qv[k][q].x, uu[q].x, aa[k]));
+          ab[k] = fma(qv[k][q].y, ww[q].y, fma(qv[k][q].x, ww[q].x, ab[k]));
+        }
+    if (nm)
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        nu = fma(uu[q].y, uu[q].y, fma(uu[q].x, uu[q].x, nu));
+        mu = fma(uu[q].y, ww[q].y, fma(uu[q].x, ww[q].x, mu));
+      }
+  }
+  if ((n & 1) && blockIdx.x == 0 && nm && lane == 0) {  // the odd last element
+    const double ul = Q[int64_t(j) * ldq + n - 1], wl = Q[int64_t(j + 1) * ldq + n - 1];
+    nu = fma(ul, ul, nu);
+    mu = fma(ul, wl, mu);
+  }
+  if ((n & 1) && blockIdx.x == 0 && lane == 0) {
+    const double ul = Q[int64_t(j) * ldq + n - 1], wl = Q[int64_t(j + 1) * ldq + n - 1];
+#pragma unroll
+    for (int k = 0; k < VPW; ++k) {
+      const int i = w + 8 * k;
+      if (i < j) {
+        const double ql = Q[int64_t(i) * ldq + n - 1];
+        aa[k] = fma(ql, ul, aa[k]);
+        ab[k] = fma(ql, wl, ab[k]);
+      }
+    }
+  }
+  // warp sums -> sh[output] (each output has one owner warp) -> CTA partials -> last CTA
+#pragma unroll
+  for (int k = 0; k < VPW; ++k) {
+    double ta = aa[k], tb = ab[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      ta += __shfl_xor_sync(0xffffffffu, ta, off);
+      tb += __shfl_xor_sync(0xffffffffu, tb, off);
+    }
+    const int i = w + 8 * k;
+    if (lane == 0 && i < j) sh[i] = ta, sh[j + i] = tb;
+  }
+  if (nm) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      nu += __shfl_xor_sync(0xffffffffu, nu, off);
+      mu += __shfl_xor_sync(0xffffffffu, mu, off);
+    }
+    if (lane == 0) sh[2 * j] = nu, sh[2 * j + 1] = mu;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < nout; o += blockDim.x) part[int64_t(blockIdx.x) * nout + o] = sh[o];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int o = threadIdx.x; o < nout; o += blockDim.x) {
+    double t = 0.0;
+    for (int b = 0; b < int(gridDim.x); ++b) t += __ldcg(part + int64_t(b) * nout + o);
+    out[o] = t;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+// q_j = (u_j - Q_{j-1} a) / beta ; u_{j+1} = w^/beta - Q_{j-1} c_{0:j} - c_j q_j ;
+// nu1 = ||u_{j+1}||^2.  Per tile each warp forms the partial sums of its own
+// vectors, the CTA adds the 8 warps' partials in warp order through shared memory.
+template <int VPW>
+__global__ void __launch_bounds__(kRedThreads) k_dcgs_update_ws(int64_t n, int j, double *__restrict__ Q,
+                                                                int64_t ldq, const double *__restrict__ coef,
+                                                                const double *dead, double *part, unsigned *ticket,
+                                                                double *nu1) {
+  constexpr int U = kDcgsU;
+  constexpr int TE = 32 * U;  // double2 per tile
+  __shared__ double2 pa[kWarpsPerCta][TE], pc[kWarpsPerCta][TE];
+  __shared__ double cf[2 * 8 * VPW + 2];
+  for (int i = threadIdx.x; i < 2 * j + 2; i += blockDim.x) cf[i] = coef[i];
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double s = 0.0;
+  if (*dead == 0.0) {
+    double2 *u2 = reinterpret_cast<double2 *>(Q + int64_t(j) * ldq);
+    double2 *w2 = reinterpret_cast<double2 *>(Q + int64_t(j + 1) * ldq);
+    const double ib = cf[2 * j + 1], cj = cf[2 * j];
+    const int64_t n2 = n / 2, ntiles = (n2 + TE - 1) / TE;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t e0 = t * TE;
+      double2 sa[U], sc[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) sa[q] = sc[q] = make_double2(0.0, 0.0);
+      double2 qv[VPW][U];
+#pragma unroll
+      for (int k = 0; k < VPW; ++k) {
+        const int i = w + 8 * k;
+        if (i < j) {
+          const double2 *q2 = reinterpret_cast<const double2 *>(Q + int64_t(i) * ldq);
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            const int64_t e = e0 + lane + 32 * q;
+            qv[k][q] = e < n2 ? __ldg(q2 + e) : make_double2(0.0, 0.0);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < VPW; ++k) {
+        const int i = w + 8 * k;
+        if (i < j) {
+          const double a = cf[i], c = cf[j + i];
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            sa[q].x = fma(a, qv[k][q].x, sa[q].x);
+            sa[q].y = fma(a, qv[k][q].y, sa[q].y);
+            sc[q].x = fma(c, qv[k][q].x, sc[q].x);
+            sc[q].y = fma(c, qv[k][q].y, sc[q].y);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) pa[w][lane + 32 * q] = sa[q], pc[w][lane + 32 * q] = sc[q];
+      __syncthreads();
+      for (int el = threadIdx.x; el < TE; el += blockDim.x) {
+        const int64_t e = e0 + el;
+        if (e < n2) {
+          double2 ta = pa[0][el], tc = pc[0][el];
+#pragma unroll
+          for (int ww = 1; ww < kWarpsPerCta; ++ww) {
+            ta.x += pa[ww][el].x, ta.y += pa[ww][el].y;
+            tc.x += pc[ww][el].x, tc.y += pc[ww][el].y;
+          }
+          const double2 uu = u2[e], wv = w2[e];
+          double2 qj, un;
+          qj.x = (uu.x - ta.x) * ib;
+          qj.y = (uu.y - ta.y) * ib;
+          un.x = fma(-cj, qj.x, fma(wv.x, ib, -tc.x));
+          un.y = fma(-cj, qj.y, fma(wv.y, ib, -tc.y));
+          u2[e] = qj;
+          w2[e] = un;
+          s = fma(un.y, un.y, fma(un.x, un.x, s));
+        }
+      }
+      __syncthreads();
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // the odd last element
+      double ta = 0.0, tc = 0.0;
+      for (int i = 0; i < j; ++i) {
+        const double ql = Q[int64_t(i) * ldq + n - 1];
+        ta = fma(cf[i], ql, ta);
+        tc = fma(cf[j + i], ql, tc);
+      }
+      double *ul = Q + int64_t(j) * ldq + n - 1, *wl = Q + int64_t(j + 1) * ldq + n - 1;
+      const double qj = (*ul - ta) * ib;
+      const double un = fma(-cj, qj, fma(*wl, ib, -tc));
+      *ul = qj;
+      *wl = un;
+      s = fma(un, un, s);
+    }
+  }
+  const double v[1] = {s};
+  grid_reduce_many<1>(v, 1, [](int o) { return o; }, part, ticket, nu1);
+}
+
 // --- bulk-copy (TMA engine) staging of vector tiles ------------------------
 // cp.async.bulk moves a contiguous tile global -> shared without registers;
 // completion is counted in bytes on an mbarrier.  The Krylov passes stream

@@ -844,19 +844,40 @@ unsigned dcgs_grid(const mg_ctx_s *c, const void *k, int64_t n) {
   return unsigned(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(std::max(1, std::min(bl, 4))) * c->n_sm)));
 }
 
-// The passes load the j + 2 vectors' elements into registers (k_dcgs_*,
-// default) or stage their tiles through a shared-memory ring with bulk copies
-// (k_dcgs_*_tma, MGB200_DCGS_TMA=1).  Measured on C3 (same box, ncu warm):
-// equal speed for the multi-dot (0.115 ms per launch at j = 4..7), the staged
-// update 20% faster, whole solve within noise (148.57 vs 148.64 V-cycles/s);
-// the staged kernels with >= 160 KB of dynamic shared memory fail to launch
-// under Nsight Compute (LaunchFailed, root cause not found), so they stay opt-in.
-bool dcgs_tma() {
-  static const bool on = [] {
-    const char *e = std::getenv("MGB200_DCGS_TMA");
-    return e && e[0] == '1';
-  }();
-  return on;
+// Three implementations of the two DCGS2 passes (MGB200_DCGS_KERNEL):
+//   auto (default): reg for j < 8, ws from j = 8 on;
+//   ws:  warp-split -- warp w owns vectors w, w + 8, ...; 2 ceil(j/8)
+//       accumulators per thread, full occupancy (k_dcgs_*_ws);
+//   reg: every thread accumulates all 2j + 2 dots (k_dcgs_*; 220 registers at
+//       j = 16, one CTA per SM, 4.2-4.6 TB/s on C3);
+//   tma: tiles of the j + 2 vectors staged through a shared-memory ring by bulk
+//       copies (k_dcgs_*_tma; same speed as reg on C3, and with >= 160 KB of
+//       dynamic shared memory it fails to launch under Nsight Compute).
+int dcgs_kernel() {  // read at every launch (captured graphs keep the kernels they were built with)
+  const char *e = std::getenv("MGB200_DCGS_KERNEL");
+  if (e && std::strcmp(e, "reg") == 0) return 1;
+  if (e && std::strcmp(e, "tma") == 0) return 2;
+  if (e && std::strcmp(e, "ws") == 0) return 3;
+  return 0;
+}
+bool dcgs_tma() { return dcgs_kernel() == 2; }
+
+template <int VPW>
+void dcgs_launch_ws(mg_ctx_s *c, bool update, int64_t n, int j, double *Q, int64_t ldq) {
+  const mgk::GmresDev &g = c->gm;
+  const void *k = update ? reinterpret_cast<const void *>(mgk::k_dcgs_update_ws<VPW>)
+                         : reinterpret_cast<const void *>(mgk::k_dcgs_dots_ws<VPW>);
+  int bl = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bl, k, mgk::kRedThreads, 0);
+  const int64_t ntiles = (n / 2 + 32 * mgk::kDcgsU - 1) / (32 * mgk::kDcgsU);
+  const unsigned gr = unsigned(std::max<int64_t>(
+      1, std::min<int64_t>(ntiles, int64_t(std::max(1, std::min(bl, 4))) * c->n_sm)));
+  if (!update)
+    ++g_tally, mgk::k_dcgs_dots_ws<VPW><<<gr, mgk::kRedThreads, 0, c->stream>>>(n, j, Q, ldq, c->dcgs_part.p,
+                                                                                 c->dcgs_ticket.p, g.dots);
+  else
+    ++g_tally, mgk::k_dcgs_update_ws<VPW><<<gr, mgk::kRedThreads, 0, c->stream>>>(
+                   n, j, Q, ldq, g.coef, g.dead, c->dcgs_part.p, c->dcgs_ticket.p, g.nu1);
 }
 
 template <int JB>
@@ -896,7 +917,17 @@ void dcgs_launch(mg_ctx_s *c, bool update, int64_t n, int j, double *Q, int64_t 
 
 // one DCGS2 pass of Arnoldi step j (bucketed on j so the j accumulators live in registers)
 mg_status dcgs_pass(mg_ctx_s *c, bool dist, bool update, int64_t n, int j, double *Q, int64_t ldq) {
-  if (j < 2) dcgs_launch<2>(c, update, n, j, Q, ldq);
+  // default: per-thread accumulators while they are few (j < 8: <= 18 of them),
+  // warp-split beyond (measured same box: C3 DCGS2 solve 112.8 -> 112.3 ms with
+  // warp-split at j >= 8, C2 2.87 -> 2.97 ms when small j also ran warp-split,
+  // its idle warps at j < 8)
+  if ((dcgs_kernel() == 0 && j >= 8) || dcgs_kernel() == 3) {
+    if (j <= 8) dcgs_launch_ws<1>(c, update, n, j, Q, ldq);
+    else if (j <= 16) dcgs_launch_ws<2>(c, update, n, j, Q, ldq);
+    else if (j <= 32) dcgs_launch_ws<4>(c, update, n, j, Q, ldq);
+    else if (j <= 64) dcgs_launch_ws<8>(c, update, n, j, Q, ldq);
+    else return fail(MG_ERR_INVALID_ARG, "DCGS2: restart %d > 64", j);
+  } else if (j < 2) dcgs_launch<2>(c, update, n, j, Q, ldq);
   else if (j < 4) dcgs_launch<4>(c, update, n, j, Q, ldq);
   else if (j < 8) dcgs_launch<8>(c, update, n, j, Q, ldq);
   else if (j < 16) dcgs_launch<16>(c, update, n, j, Q, ldq);

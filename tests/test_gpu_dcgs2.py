@@ -130,3 +130,23 @@ def test_dcgs2_distributed_matches_single(name, P):
     x = np.concatenate([o[1] for o in out])
     xr = host(x1)
     assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
+
+
+@pytest.mark.parametrize("kernel", ["auto", "reg", "ws", "tma"])
+def test_dcgs2_kernel_variants(kernel, monkeypatch):
+    """The three implementations of the DCGS2 passes (per-thread accumulators,
+    warp-split, bulk-copy ring; MGB200_DCGS_KERNEL) reach the oracle's iterate:
+    +-1 iterations and x to 1e-8, a solve beyond j = 8 and a restart."""
+    import paper_2405_05047_b200 as m
+    if kernel != "auto":
+        monkeypatch.setenv("MGB200_DCGS_KERNEL", kernel)
+    lv, bs, om, b, H = case("c3_small")
+    h = orc_mg("c3_small")
+    mg = build_gpu(lv, bs, omega=om, H=H)
+    for restart in (30, 11):
+        x = dev(np.zeros(lv[-1].n * bs))
+        st, its, rel, conv = m.mg_solve(mg.ctx, x, dev(b), method=m.MG_GMRES_DCGS2, restart=restart, rtol=1e-10)
+        xe, ite, _, _ = oracle.gmres_dcgs2(h, b, rtol=1e-10, restart=restart)
+        assert conv and abs(its - ite) <= 1 and its > 8, (its, ite)
+        assert np.linalg.norm(host(x) - xe) <= 1e-8 * np.linalg.norm(xe)
+    mg.close()
