@@ -1689,6 +1689,27 @@ __global__ void k_dcgs_backsolve(GmresDev st, int k, const double *kdev) {
   }
 }
 
+// *flag = 1 if any x[i] != 0 (the caller zeroes it first).  Used to take the
+// initial residual of a zero guess as b itself: b - A*0 == b exactly for the
+// finite operators mg_set_matrix accepts (every product a*0 is +-0, the row
+// sums are +0, b - (+0) = b), so the A-pass is skipped, not approximated.
+__global__ void k_nonzero_flag(int64_t n, const double *__restrict__ x, int vec, double *flag) {
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  bool nz = false;
+  if (vec) {
+    const int64_t n2 = n / 2;
+    for (int64_t i = tid; i < n2; i += stride) {
+      const double2 v = __ldg(reinterpret_cast<const double2 *>(x) + i);
+      nz |= (v.x != 0.0) | (v.y != 0.0);
+    }
+    if (tid == 0 && (n & 1)) nz |= x[n - 1] != 0.0;
+  } else {
+    for (int64_t i = tid; i < n; i += stride) nz |= __ldg(x + i) != 0.0;
+  }
+  if (__any_sync(0xffffffffu, nz) && (threadIdx.x & 31) == 0) *flag = 1.0;
+}
+
 // Halo pack: out[i] = v[idx[i]] (bs values per item).
 template <int BS>
 __global__ void k_pack(int64_t n, const int32_t *__restrict__ idx, const double *__restrict__ v,

@@ -14,3 +14,7 @@ done
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err; echo "ref rc=$?"
 MGB200_GMRES_LOOP=host timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/${TAG}_c3_step_launches.csv python scripts/profile_ops.py step --config c3 > gpurun_out/${TAG}_step.log 2>&1; echo "ncu step rc=$?"
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -s 3200 -c 1200 --csv --log-file gpurun_out/${TAG}_bench_launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-mixed --no-orth-side > gpurun_out/${TAG}_bench_under_ncu.log 2>&1; echo "ncu bench rc=$?"
+timeout 900 python bench.py --config ns > gpurun_out/${TAG}_ns.json 2> gpurun_out/${TAG}_ns.err; echo "bench ns rc=$?"
+timeout 900 python bench.py --config pres --no-cpu-solve > gpurun_out/${TAG}_pres.json 2> gpurun_out/${TAG}_pres.err; echo "bench pres rc=$?"
+# the N > 1 path (two processes time-slicing the one GPU through the IPC transport: functional)
+MGB200_TRANSPORT=ipc timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --config c5 --steps 3 --warmup 3 > gpurun_out/${TAG}_c5_n2_ipc.json 2> gpurun_out/${TAG}_c5_n2_ipc.err; echo "bench c5 n2 ipc rc=$?"

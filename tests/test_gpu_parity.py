@@ -460,3 +460,34 @@ def test_gmres_device_loop_equals_host_loop(name, monkeypatch):
     for (xh, ih, rh, ch, sh), (xd, idv, rd, cd, sd) in zip(*out):
         assert ih == idv and ch == cd and sh == sd
         assert np.array_equal(xh, xd) and rh == rd
+
+
+@pytest.mark.parametrize("method", ["mgs", "dcgs2", "richardson"])
+def test_solve_from_nonzero_and_zero_guess(method, monkeypatch):
+    """A nonzero initial guess takes the full b - A x0 (oracle with the same x0:
+    +-1 iterations, x at 1e-8); a zero guess (+0.0 or -0.0) started from r = b
+    without the A-pass (MGB200_ZERO_GUESS=1; b - A*0 == b exactly) gives the
+    bit-identical iterate of the solve that runs the A-pass (=0)."""
+    import paper_2405_05047_b200 as m
+    lv, bs, om, b, H = case("c3_small")
+    mg = gpu_mg("c3_small")
+    h = orc_mg("c3_small")
+    meth = {"mgs": m.MG_GMRES, "dcgs2": m.MG_GMRES_DCGS2, "richardson": m.MG_RICHARDSON}[method]
+    x0 = rng(77).standard_normal(lv[-1].n * bs) * 0.3
+    x = dev(x0.copy())
+    st, its, rel, conv = m.mg_solve(mg.ctx, x, dev(b), method=meth, rtol=1e-10)
+    if method == "richardson":
+        xe, ite, hist = oracle.richardson(h, b, x0=x0, rtol=1e-10)
+    else:
+        fn = oracle.gmres if method == "mgs" else oracle.gmres_dcgs2
+        xe, ite, _, _ = fn(h, b, x0=x0, rtol=1e-10)
+    assert conv and abs(its - ite) <= 1, (its, ite)
+    assert np.linalg.norm(host(x) - xe) <= 1e-8 * np.linalg.norm(xe)
+    outs = []
+    for z, zg in ((0.0, "1"), (-0.0, "1"), (0.0, "0")):
+        monkeypatch.setenv("MGB200_ZERO_GUESS", zg)
+        x = dev(np.full(lv[-1].n * bs, z))
+        st, its, rel, conv = m.mg_solve(mg.ctx, x, dev(b), method=meth, rtol=1e-10)
+        outs.append((host(x), its, rel))
+    for o in outs[1:]:
+        assert np.array_equal(outs[0][0], o[0]) and outs[0][1:] == o[1:]
