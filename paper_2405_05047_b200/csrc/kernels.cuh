@@ -1274,8 +1274,14 @@ __global__ void __launch_bounds__(kRedThreads) k_dcgs_update_ws(int64_t n, int j
     double2 *w2 = reinterpret_cast<double2 *>(Q + int64_t(j + 1) * ldq);
     const double ib = cf[2 * j + 1], cj = cf[2 * j];
     const int64_t n2 = n / 2, ntiles = (n2 + TE - 1) / TE;
+    static_assert(TE <= kRedThreads, "one combining thread per tile element");
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int64_t e0 = t * TE;
+      // the combining thread's u, w^ are loaded up front, with the basis loads
+      const int64_t ec = e0 + threadIdx.x;
+      const bool comb = threadIdx.x < TE && ec < n2;
+      double2 uu = make_double2(0.0, 0.0), wv = make_double2(0.0, 0.0);
+      if (comb) uu = u2[ec], wv = w2[ec];
       double2 sa[U], sc[U];
 #pragma unroll
       for (int q = 0; q < U; ++q) sa[q] = sc[q] = make_double2(0.0, 0.0);
@@ -1309,16 +1315,16 @@ __global__ void __launch_bounds__(kRedThreads) k_dcgs_update_ws(int64_t n, int j
 #pragma unroll
       for (int q = 0; q < U; ++q) pa[w][lane + 32 * q] = sa[q], pc[w][lane + 32 * q] = sc[q];
       __syncthreads();
-      for (int el = threadIdx.x; el < TE; el += blockDim.x) {
-        const int64_t e = e0 + el;
-        if (e < n2) {
+      if (comb) {
+        const int el = threadIdx.x;
+        const int64_t e = ec;
+        {
           double2 ta = pa[0][el], tc = pc[0][el];
 #pragma unroll
           for (int ww = 1; ww < kWarpsPerCta; ++ww) {
             ta.x += pa[ww][el].x, ta.y += pa[ww][el].y;
             tc.x += pc[ww][el].x, tc.y += pc[ww][el].y;
           }
-          const double2 uu = u2[e], wv = w2[e];
           double2 qj, un;
           qj.x = (uu.x - ta.x) * ib;
           qj.y = (uu.y - ta.y) * ib;
