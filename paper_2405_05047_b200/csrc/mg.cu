@@ -921,6 +921,7 @@ mg_status dcgs_pass(mg_ctx_s *c, bool dist, bool update, int64_t n, int j, doubl
   // warp-split beyond (measured same box: C3 DCGS2 solve 112.8 -> 112.3 ms with
   // warp-split at j >= 8, C2 2.87 -> 2.97 ms when small j also ran warp-split,
   // its idle warps at j < 8)
+  // (the warp-split update also for 2 <= j < 8 was measured: C3 unchanged, C2 2.85 -> 2.89 ms)
   if ((dcgs_kernel() == 0 && j >= 8) || dcgs_kernel() == 3) {
     if (j <= 8) dcgs_launch_ws<1>(c, update, n, j, Q, ldq);
     else if (j <= 16) dcgs_launch_ws<2>(c, update, n, j, Q, ldq);
