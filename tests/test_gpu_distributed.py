@@ -296,3 +296,25 @@ def test_distributed_rank_without_rows():
     out = run_ranks(2, work)
     assert np.array_equal(np.concatenate([o[0] for o in out]), host(z))
     assert all(o[1][3] for o in out) and abs(out[0][1][1] - its1) <= 1
+
+
+@pytest.mark.parametrize("name,P", [("c3_small", 2), ("c2_small", 3)])
+def test_distributed_zero_guess_shortcut(name, P, monkeypatch):
+    """The zero-guess test is all-reduced across ranks: with it forced on
+    (MGB200_ZERO_GUESS=1) every rank starts from r = b and the solve is bit-identical
+    to the one that runs the distributed A-pass (=0)."""
+    import paper_2405_05047_b200 as m
+    Pr, parts, extras, ranges, mgs = dist_mg(name, P)
+    fr = ranges[-1]
+    res = []
+    for zg in ("1", "0"):
+        monkeypatch.setenv("MGB200_ZERO_GUESS", zg)
+
+        def solve(r):
+            f0, f1 = fr[r]
+            x = dev(np.zeros((f1 - f0) * Pr.bs))
+            out = m.mg_solve(mgs[r].ctx, x, dev(extras[r][0]), rtol=1e-10)
+            return out, host(x)
+        res.append(run_ranks(P, solve))
+    for (o1, x1), (o0, x0) in zip(*res):
+        assert o1 == o0 and np.array_equal(x1, x0)
