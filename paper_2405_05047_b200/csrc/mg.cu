@@ -2208,9 +2208,12 @@ mg_status mg_set_transfer(mg_ctx c, int fine_level, const int64_t *row_ptr, cons
   TRY(build_sell(L.R, L.r_rows, rrp.data(), rcl.data(), rv.data(), wpe));
   L.R.ks = 4;  // R rows gather 9-27+ fine entries: split them over 4 warps
   // restriction on the SELL-C layout (measured, scripts/tune_tsell.py: C3 finest 98.7 -> 69.3 us,
-  // C5 212 -> 113 us, C2 25.6 -> 19.6 us); 2 warps per slice group for bs 3, 1 otherwise
+  // C5 212 -> 113 us, C2 25.6 -> 19.6 us); warps per slice group: 4 for bs 1 and 6, 2 for bs 3, 1 otherwise
   TRY(build_tsell(L.Rt, L.r_rows, rrp.data(), rcl.data(), rv.data(), wpe, c->bs()));
-  L.Rt.ks = c->bs() == 3 ? 2 : 1;
+  // (round-2 re-tune with the exact-size batches, same box: 4 warps per slice for bs 1
+  // -- C2 V-cycle 0.247 -> 0.237 ms, TD L10 0.256 -> 0.248 -- and bs 6 -- e6 1.165 ->
+  // 1.137 ms; bs 3 stays at 2 (C3: 1/1, 4/1, 2/2 slower); bs 4 (C5) insensitive)
+  L.Rt.ks = (c->bs() == 1 || c->bs() == 6) ? 4 : c->bs() == 3 ? 2 : 1;
   // ---- P: columns are coarse rows ------------------------------------------
   if (C.dist) {
     std::vector<int64_t> ghosts;
