@@ -2224,10 +2224,16 @@ mg_status mg_set_transfer(mg_ctx c, int fine_level, const int64_t *row_ptr, cons
   }
   TRY(build_sell(L.P, L.n, rp.data(), cl.data(), v.data(), wpe));
   TRY(build_pcsr(L.Pc, L.n, rp, cl, v, wpe));
-  // prolongation stays on SELL-32 (lane = fine row): its rows hold 1-8 entries, and the
-  // SELL-C layout's 32/bs rows per warp triple the short dependent chains (C3 finest
-  // 105 -> 162 us measured); MGB200_TSELL_PROLONG=1 builds it anyway (experiments)
-  if (const char *e = std::getenv("MGB200_TSELL_PROLONG"); e && e[0] == '1')
+  // prolongation: natural-order CSR for scalar fp32-exact weights (build_pcsr, above);
+  // SELL-32 was chosen over SELL-C in round 2 before the exact-size batches (C3 finest
+  // 105 vs 162 us then)
+  // Per-component weights (no natural-order CSR kernel, see build_pcsr) use the SELL-C
+  // layout: with the exact-size load batches it is slightly ahead of SELL-32 (same box:
+  // C4 V-cycle 0.469 -> 0.464 ms, C5 11.10 -> 11.06 ms). MGB200_TSELL_PROLONG = 1 / 0
+  // forces / disables it (experiments).
+  const char *tp = std::getenv("MGB200_TSELL_PROLONG");
+  const bool want_pt = tp && *tp ? tp[0] == '1' : (wpe != 1 && !L.Pc.set);
+  if (want_pt)
     TRY(build_tsell(L.Pt, L.n, rp.data(), cl.data(), v.data(), wpe, c->bs()));
   else
     L.Pt = TSellOp();
